@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""bench.py -- compact cell-updates/s of the B200 compact-fractal stencil engine.
+
+Workload (config.workload): Sierpinski triangle K(n,3,2) at r=20 (3^20 = 3.49e9
+compact cells, n = 2^20: the bounding box cannot exist), seed 42, density 0.5,
+B3/S23 Moore -- BASELINE.json configs[3], the north-star target; N GPUs split the
+compact array into contiguous tile-row ranges with a per-step NVLink halo
+exchange (NCCL send/recv via torch.distributed), so scaling is strong.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W untimed steps, then K steps bracketed by barrier + synchronize, timed
+with CUDA events on the engine's stream, max over ranks.  The state (6.97 GB) is
+54x the 126 MB L2, so no flush is needed between steps.
+
+One JSON line on rank 0 (see DESIGN.md "Measurement" for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compact cell-updates/sec (Sierpinski r=16/20) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "cell-updates/s"
+LEVEL = 20
+SEED, DENSITY = 42, 0.5
+BIRTH, SURVIVE = 0x8, 0xC  # B3/S23
+BYTES_PER_UPDATE = 2       # read own state byte + write next-state byte
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the step kernel from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own compact step (oracle/_ref) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(level, cells_target_s=1.0, steps=1, warmup=0, threads=None):
+    """Times Simulation::step_compact_linear (proj/src/stencil.cpp:334-368) of the
+    unmodified reference over a contiguous sample of the level-`level` compact index
+    range, split across all host threads like parallel_for.  Returns a dict."""
+    import oracle
+    from paper_2110_12952_b200.descriptor import builtin_descriptor
+    threads = threads or os.cpu_count() or 1
+    T = builtin_descriptor("sierpinski-triangle")
+    kind = "reference" if oracle.ref_available() else "port"
+    total = 3 ** level
+    if kind == "reference":
+        sim = oracle.RefSim(T.replicas, 3, 2, level, backend="compact", workers=threads,
+                            memory_cap=1 << 40)
+        # calibrate: ~4e6 cells/s/thread on the reference; aim for cells_target_s per sample
+        n = int(min(total, max(threads * 1e5, 4e6 * threads * cells_target_s)))
+        i0 = (total - n) // 2
+        sim.parallel_seed_range(SEED, DENSITY, i0, i0 + n, threads)
+        for _ in range(warmup):
+            sim.sample_step(BIRTH, SURVIVE, True, i0, i0 + n, threads)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            sim.sample_step(BIRTH, SURVIVE, True, i0, i0 + n, threads)
+        dt = (time.perf_counter() - t0) / steps
+        del sim
+    else:
+        o = oracle.Oracle(T.replicas, 3, 2, min(level, 16))
+        o.seed(SEED, DENSITY)
+        n = o.w * o.h
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o.step(BIRTH, SURVIVE, True, threads=threads)
+        dt = (time.perf_counter() - t0) / steps
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": (f"T r={level}: step_compact_linear over {n} contiguous compact cells "
+                       f"(of {total}), {threads} std::threads, {steps} timed sample(s)"
+                       if kind == "reference" else f"oracle port, T r={min(level, 16)} full steps"),
+            "seconds_per_sample": dt}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    steps, warmup = args.steps, args.warmup
+    # each step = one bounded sample sized so the whole run stays within minutes
+    budget = max(0.3, min(2.0, 150.0 / max(1, steps + warmup)))
+    res = cpu_reference_sample(LEVEL, cells_target_s=budget, steps=steps, warmup=warmup)
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": warmup, "ms_per_step": res["seconds_per_sample"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seed 42, density 0.5)", "impl": "reference",
+            "config": {"workload": "sierpinski-triangle r=20 compact, B3/S23 Moore",
+                       "level": LEVEL, "parallelism": "host threads"},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    from paper_2110_12952_b200 import (Backend, SimOptions, Simulation, builtin_descriptor,
+                                       conway_rule, _abi)
+    ws, rank, local = dist_env()
+    n = args.gpus if ws == 1 else ws
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local if ws > 1 else 0
+    T = builtin_descriptor("sierpinski-triangle")
+    rule = conway_rule()
+    L = _abi.lib()
+    sim = Simulation(T, LEVEL, Backend.GpuCompact, SimOptions(memory_cap=1 << 40, device=device))
+    h = sim.handle()
+    cells = 3 ** LEVEL
+    kern, q = sim.active_kernel()
+    sim.seed_random(SEED, DENSITY)
+
+    # ---- partition + halo plan (host-only lists; no communication needed) ----
+    peers = []
+    bufs = {}
+    if ws > 1:
+        _abi.check(L.nbbgpu_partition(h, rank, ws))
+        rep = _abi.replica_array(T.replicas)
+        for p in range(ws):
+            if p == rank:
+                continue
+            cnt = C.c_uint64()
+            _abi.check(L.nbbgpu_plan_needs(rep, 3, 2, LEVEL, -1, p, ws, rank, None, C.byref(cnt)))
+            sends = (C.c_uint64 * max(1, cnt.value))()
+            _abi.check(L.nbbgpu_plan_needs(rep, 3, 2, LEVEL, -1, p, ws, rank, sends, C.byref(cnt)))
+            _abi.check(L.nbbgpu_halo_set_sends(h, p, sends, cnt.value))
+            nrecv = C.c_uint64()
+            _abi.check(L.nbbgpu_halo_needs(h, p, None, C.byref(nrecv)))
+            if cnt.value or nrecv.value:
+                peers.append(p)
+                bufs[p] = (torch.empty(max(1, cnt.value), dtype=torch.uint8, device=f"cuda:{device}"),
+                           torch.empty(max(1, nrecv.value), dtype=torch.uint8, device=f"cuda:{device}"),
+                           cnt.value, nrecv.value)
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
+        owned = hi.value - lo.value
+    else:
+        owned = cells
+
+    def exchange():
+        if not peers:
+            return 0
+        ops = []
+        for p in peers:
+            sb, rb, ns, nr = bufs[p]
+            if ns:
+                _abi.check(L.nbbgpu_halo_pack(h, p, C.c_void_p(sb.data_ptr())))
+                ops.append(dist.P2POp(dist.isend, sb[:ns], p))
+            if nr:
+                ops.append(dist.P2POp(dist.irecv, rb[:nr], p))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        torch.cuda.synchronize(device)
+        launches = 0
+        for p in peers:
+            sb, rb, ns, nr = bufs[p]
+            if nr:
+                _abi.check(L.nbbgpu_halo_unpack(h, p, C.c_void_p(rb.data_ptr())))
+                launches += 1
+            launches += 1 if ns else 0
+        return launches
+
+    def barrier():
+        torch.cuda.synchronize(device)
+        if dist is not None:
+            dist.barrier()
+
+    # ---- warmup --------------------------------------------------------------
+    for _ in range(args.warmup):
+        sim.step(rule)
+        exchange()
+
+    # ---- timed: device-resident state, K steps ---------------------------------
+    stream = C.c_void_p()
+    _abi.check(L.nbbgpu_stream(h, C.byref(stream)))
+    ext = torch.cuda.ExternalStream(stream.value, device=f"cuda:{device}")
+    clocks = ClockSampler(device)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kernel_ms = 0.0
+    launches = 0
+    t_wall = time.perf_counter()
+    ev0.record(ext)
+    if ws == 1:
+        # one launch per step, back to back on the engine stream
+        kernel_ms = sim.step_timed(rule, args.steps)
+        launches += args.steps
+    else:
+        for _ in range(args.steps):
+            kernel_ms += sim.step_timed(rule, 1)
+            launches += 1 + exchange()
+    ev1.record(ext)
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    step_ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        tt = torch.tensor([step_ms, kernel_ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms, kernel_ms = float(tt[0]), float(tt[1])
+    ms_per_step = step_ms / args.steps
+    value = cells * args.steps / (step_ms / 1e3)
+
+    # ---- parity sanity: hash of the final state equals across GPU counts -------
+    if ws > 1:
+        hv = C.c_uint64()
+        _abi.check(L.nbbgpu_state_hash_owned(h, C.byref(hv)))
+        t = torch.tensor([hv.value & ((1 << 63) - 1), hv.value >> 63], dtype=torch.int64,
+                         device=f"cuda:{device}")
+        parts = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(parts, t)
+        final_hash = sum(int(p[0]) + (int(p[1]) << 63) for p in parts) & (2**64 - 1)
+    else:
+        final_hash = sim.state_hash()
+
+    # ---- e2e through the public API with host buffers ----------------------------
+    # upload the initial state from pinned host memory, K synchronous
+    # Simulation.step calls (one C-ABI call each, like nbb::Simulation::step),
+    # download the final state into pinned host memory.  All inside the region.
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(cells, dtype=torch.uint8).pin_memory()
+        host_out = torch.empty(cells, dtype=torch.uint8).pin_memory()
+        _abi.check(L.nbbgpu_download(h, C.c_void_p(host_in.data_ptr()), cells))
+        barrier()
+        t0 = time.perf_counter()
+        _abi.check(L.nbbgpu_upload(h, C.c_void_p(host_in.data_ptr()), cells))
+        for _ in range(args.steps):
+            sim.step(rule)
+            exchange()
+        _abi.check(L.nbbgpu_download(h, C.c_void_p(host_out.data_ptr()), cells))
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+        e2e = {"value": cells * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": cells / args.steps, "d2h_bytes_per_step": cells / args.steps,
+               "how": "upload(pinned host state) + K x nbbgpu_step(1) + download(pinned host), wall clock"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = peaks()
+    kernel_ms_per_launch = kernel_ms / args.steps
+    achieved = BYTES_PER_UPDATE * owned / (kernel_ms_per_launch / 1e3) / 1e9
+    traffic, ncu = ncu_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic: seed_random(42, 0.5) generated on the device (rng.hpp cell_alive)",
+        "config": {"workload": "sierpinski-triangle K(2^20,3,2) r=20 compact, B3/S23 Moore "
+                               "(BASELINE.json configs[3]; north-star target)",
+                   "level": LEVEL, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
+                   "parallelism": f"partitioned x{n}" if n > 1 else "single GPU",
+                   "l2": "state 6.97 GB >> 126 MB L2: inputs larger than L2, no flush"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "model": "2 B per compact cell-update (SURVEY.md 8d) x owned cells per launch",
+                     "peak_source": peak_src, "kernel_ms_per_launch": kernel_ms_per_launch},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "final_state_hash": f"{final_hash:016x}",
+        "wall_s": t_wall,
+    }
+    if ncu:
+        line["roofline"]["ncu"] = {k: v for k, v in ncu.items() if k != "dram_bytes_per_launch"}
+    if not args.no_cpu_baseline and n == 1:
+        try:
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(LEVEL, 2.0, 3, 1).items()
+                                    if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

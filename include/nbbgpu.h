@@ -1,0 +1,171 @@
+/*
+ * nbbgpu.h -- C ABI of the B200 (sm_100a) compact-fractal stencil engine.
+ *
+ * The drop-in boundary for the reference's hot path.  The reference has no plugin
+ * API: its seam is the closed `Backend` enum and the `nbb::Simulation` methods
+ * (proj/include/nbb/stencil.hpp:50-122).  Each export below replaces one of those
+ * members for the two GPU backends `gpu-compact` / `gpu-bb`; the reference-side
+ * adapter that forwards to them is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - every function returns an nbbgpu_status (0 = ok); exceptions never cross the
+ *    ABI.  Codes 1..4 map 1:1 to the reference's ParseError / NotInFractal /
+ *    OutOfDomain / CapacityError (proj/include/nbb/errors.hpp:10-27);
+ *    NBBGPU_ERR_CUDA maps to std::runtime_error (CLI exit 1, tools/main.cpp:267-303).
+ *  - nbbgpu_last_error() returns the message of the last failure on the calling
+ *    thread (thread-local storage, valid until the next failing call).
+ *  - buffers are plain host pointers unless stated otherwise; byte order is the
+ *    reference's: compact `cy*w + cx` (k^r bytes, proj/src/grid.cpp:46-53) or
+ *    embedded `y*n + x` (n^2 bytes, proj/src/grid.cpp:44-45).
+ *  - a handle is single-owner and not re-entrant (Simulation is single-owner,
+ *    SPEC.md:288).  Every call is synchronous on return, like Simulation::step.
+ *  - cell states are binary {0,1}.  The reference only ever produces 0/1 (seeding,
+ *    rules); uploads / set_cell of any other byte return NBBGPU_ERR_OUT_OF_DOMAIN.
+ */
+#ifndef NBBGPU_H
+#define NBBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nbbgpu_sim* nbbgpu_t;
+
+typedef enum {
+    NBBGPU_OK = 0,
+    NBBGPU_ERR_PARSE = 1,          /* nbb::ParseError     */
+    NBBGPU_ERR_NOT_IN_FRACTAL = 2, /* nbb::NotInFractal   */
+    NBBGPU_ERR_OUT_OF_DOMAIN = 3,  /* nbb::OutOfDomain    */
+    NBBGPU_ERR_CAPACITY = 4,       /* nbb::CapacityError ("memory cap" in the message) */
+    NBBGPU_ERR_CUDA = 5,           /* std::runtime_error from the CUDA runtime */
+    NBBGPU_ERR_INVALID = 6         /* null handle / bad argument */
+} nbbgpu_status;
+
+/* Storage layout of a handle: the reference's Layout::LinearCompact for
+ * Backend::Compact and Layout::Embedded for Backend::BoundingBox
+ * (proj/src/stencil.cpp:108-112). */
+enum { NBBGPU_MODE_COMPACT = 0, NBBGPU_MODE_BB = 1 };
+
+/* Step kernels (nbbgpu_set_kernel).  AUTO picks TILED when the level admits a
+ * tile level, else NAIVE.  NAIVE is the paper's per-cell kernel: lambda of the
+ * own cell plus nu of each neighbour (proj/src/stencil.cpp:354-367); its map
+ * variant is chosen by nbbgpu_set_map_variant. */
+enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2 };
+
+/* lambda / nu map variants: CUDA-core digit loop, or the paper's matrix form on
+ * the tensor cores (exact integer MMA, u8 x u8 -> s32). */
+enum { NBBGPU_MAP_DIGIT = 0, NBBGPU_MAP_MMA = 1 };
+
+const char* nbbgpu_last_error(void);
+int nbbgpu_version(void);
+/* Number of visible CUDA devices (0 when none; never fails). */
+int nbbgpu_device_count(void);
+
+/* Simulation::Simulation (proj/src/stencil.cpp:116-136).  replicas_xy holds k
+ * (gx, gy) pairs in replica-ID order (FractalDescriptor::replicas,
+ * descriptor.hpp:23-36); the descriptor is validated like
+ * FractalDescriptor::validate (descriptor.cpp:12-44).  memory_cap is the per-grid
+ * cell cap of Grid::Grid (grid.cpp:18-22; default 2 GiB, grid.hpp:13). */
+int nbbgpu_create(const int32_t* replicas_xy, int k, int s, int level, int mode, int device,
+                  uint64_t memory_cap, nbbgpu_t* out);
+int nbbgpu_destroy(nbbgpu_t h);
+
+/* Simulation::seed_random (stencil.cpp:138-180): both buffers zeroed, iteration
+ * reset, every fractal cell alive iff cell_alive(seed, x, y, density)
+ * (rng.hpp:27-33).  density outside [0,1] -> NBBGPU_ERR_OUT_OF_DOMAIN. */
+int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density);
+
+/* nsteps x Simulation::step (stencil.cpp:262-289) with rule
+ * StencilRule{birth, survive, moore ? Moore : VonNeumann} (stencil.hpp:18-31). */
+int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps);
+
+/* Same as nbbgpu_step, also returning the device time of the nsteps step
+ * kernels measured with CUDA events on the handle's stream. */
+int nbbgpu_step_timed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
+                      float* device_ms);
+
+/* Simulation::state_hash (stencil.cpp:196-234): wrapping uint64 sum of
+ * coord_mix(x, y) over alive cells. */
+int nbbgpu_state_hash(nbbgpu_t h, uint64_t* out);
+
+/* Simulation::iteration() */
+int nbbgpu_iteration(nbbgpu_t h, int64_t* out);
+
+/* Grid::stored_cell_count() of the front buffer (k^r or n^2). */
+int nbbgpu_stored_cells(nbbgpu_t h, uint64_t* out);
+/* compact width / height / embedded side (CoordMapper, maps.hpp:39-42). */
+int nbbgpu_dims(nbbgpu_t h, int64_t* w, int64_t* hgt, int64_t* side);
+
+/* front().data() as a host copy (`bytes` must equal stored_cells). */
+int nbbgpu_download(nbbgpu_t h, uint8_t* dst, uint64_t bytes);
+/* Replaces the front buffer (reference byte order; holes must be 0 in bb mode). */
+int nbbgpu_upload(nbbgpu_t h, const uint8_t* src, uint64_t bytes);
+
+/* Simulation::cell / set_cell (stencil.cpp:182-194). */
+int nbbgpu_get_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t* out);
+int nbbgpu_set_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t state);
+
+/* Device bytes held by the handle (both state buffers + tables + scratch). */
+int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out);
+
+/* Kernel selection (NBBGPU_KERNEL_*) and the naive kernel's map variant. */
+int nbbgpu_set_kernel(nbbgpu_t h, int kernel);
+int nbbgpu_set_map_variant(nbbgpu_t h, int variant);
+/* The kernel the next step will launch (resolves AUTO) and its tile level q. */
+int nbbgpu_active_kernel(nbbgpu_t h, int* kernel, int* tile_level);
+
+/* The handle's CUDA stream (cudaStream_t) for external event timing. */
+int nbbgpu_stream(nbbgpu_t h, void** stream);
+
+/* Batched maps of the handle's fractal (CoordMapper::to_embedded /
+ * try_to_compact, maps.cpp:80-146).  Pointers may be host or device memory.
+ *   lambda: in = count (cx, cy) int32 pairs -> out = count (x, y) int32 pairs
+ *   nu:     in = count (x, y) pairs -> out = count (cx, cy) pairs, (-1, -1) for a
+ *           hole or an out-of-box coordinate.
+ * variant = NBBGPU_MAP_DIGIT or NBBGPU_MAP_MMA.  device_ms (optional) receives
+ * the kernel time. */
+int nbbgpu_lambda_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,
+                        float* device_ms);
+int nbbgpu_nu_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,
+                    float* device_ms);
+
+/* ---- multi-GPU partitioning (one process per GPU) ---------------------------
+ * A handle may own a contiguous range of tile rows [row0, row1) of the compact
+ * array (tile rows of h_q compact rows each; the whole array when nranks == 1).
+ * It keeps a full-size copy of the state, updates only its rows, and exchanges
+ * halo bytes with its peers between steps. */
+int nbbgpu_partition(nbbgpu_t h, int rank, int nranks);
+/* Owned compact byte range [lo, hi). */
+int nbbgpu_owned_range(nbbgpu_t h, uint64_t* lo, uint64_t* hi);
+/* Compact byte offsets this rank needs from `peer` (sorted, unique).  Pass
+ * offsets == NULL to query the count.  Computed on the host at partition time. */
+int nbbgpu_halo_needs(nbbgpu_t h, int peer, uint64_t* offsets, uint64_t* count);
+/* Registers the offsets `peer` needs from this rank (its halo_needs(self)). */
+int nbbgpu_halo_set_sends(nbbgpu_t h, int peer, const uint64_t* offsets, uint64_t count);
+/* Gather the registered send bytes for `peer` from the front buffer into a DEVICE
+ * buffer / scatter received bytes from a DEVICE buffer into the front buffer. */
+int nbbgpu_halo_pack(nbbgpu_t h, int peer, void* dev_dst);
+int nbbgpu_halo_unpack(nbbgpu_t h, int peer, const void* dev_src);
+/* state_hash over the owned range only (sum over ranks = global hash). */
+int nbbgpu_state_hash_owned(nbbgpu_t h, uint64_t* out);
+/* Raw device pointer of the front buffer (for peer-to-peer transports). */
+int nbbgpu_front_device_ptr(nbbgpu_t h, void** out);
+
+/* ---- host-only planning (no GPU needed; same geometry as above) ------------
+ * tile_level < 0 selects the level nbbgpu_create would choose for the compact
+ * backend (0 = no tiling: partition rows are compact rows). */
+int nbbgpu_plan_tile_level(const int32_t* replicas_xy, int k, int s, int level, int* tile_level);
+int nbbgpu_plan_partition(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                          int rank, int nranks, uint64_t* owned_lo, uint64_t* owned_hi);
+int nbbgpu_plan_needs(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                      int rank, int nranks, int peer, uint64_t* offsets, uint64_t* count);
+/* info = [q, wq, C, nH, L, Wc, Hc, dmask] of the tile plan. */
+int nbbgpu_plan_tiles(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                      int moore, int32_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBBGPU_H */

@@ -1,0 +1,884 @@
+// nbbgpu.cu -- the C ABI of include/nbbgpu.h: handle, device memory, dispatch.
+//
+// Host side of the drop-in: what nbb::Simulation (proj/src/stencil.cpp) does on
+// the CPU, done here with device buffers and the kernels of naive.cuh, tiled.cuh
+// and maps.cuh.  No CPU fallback exists: every state transition runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/nbbgpu.h"
+#include "common.cuh"
+#include "maps.cuh"
+#include "naive.cuh"
+#include "tiled.cuh"
+
+using namespace nbbgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct NbbError : std::runtime_error {
+    int code;
+    NbbError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void raise(int code, const std::string& m) { throw NbbError(code, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation)
+            raise(NBBGPU_ERR_CAPACITY, std::string(what) + ": device memory exhausted (memory cap)");
+        raise(NBBGPU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return NBBGPU_OK;
+    } catch (const NbbError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return NBBGPU_ERR_CAPACITY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NBBGPU_ERR_CUDA;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host mirror of CoordMapper (maps.cpp:45-146) for set/get_cell and the tables.
+// ---------------------------------------------------------------------------
+struct HostFrac {
+    int k = 0, s = 0, r = 0;
+    int64_t side = 1, w = 1, h = 1;
+    std::vector<int> id;  // s*s
+    std::vector<int> gx, gy;
+    std::vector<int64_t> spow;
+
+    static int64_t ipow(int64_t b, int e) {
+        int64_t r = 1;
+        for (int i = 0; i < e; ++i) {
+            if (b != 0 && r > INT64_MAX / b) raise(NBBGPU_ERR_CAPACITY, "integer overflow computing " + std::to_string(b) + "^" + std::to_string(e));
+            r *= b;
+        }
+        return r;
+    }
+
+    void init(const int32_t* rep, int k_, int s_, int r_) {
+        // FractalDescriptor::validate (descriptor.cpp:12-44)
+        if (k_ < 1) raise(NBBGPU_ERR_PARSE, "descriptor: k must be >= 1, got " + std::to_string(k_));
+        if (s_ < 2) raise(NBBGPU_ERR_PARSE, "descriptor: invalid growth factor s=" + std::to_string(s_) + " (s >= 2 required)");
+        if ((int64_t)k_ > (int64_t)s_ * s_) raise(NBBGPU_ERR_PARSE, "descriptor: k=" + std::to_string(k_) + " exceeds s*s=" + std::to_string(s_ * s_));
+        if (s_ > kMaxS) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "growth factor s=" + std::to_string(s_) + " exceeds the engine limit of 16");
+        if (r_ < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "scale level must be >= 0");
+        k = k_; s = s_; r = r_;
+        id.assign(s * s, -1);
+        gx.resize(k);
+        gy.resize(k);
+        for (int i = 0; i < k; ++i) {
+            const int x = rep[2 * i], y = rep[2 * i + 1];
+            if (x < 0 || y < 0 || x >= s || y >= s)
+                raise(NBBGPU_ERR_PARSE, "descriptor: replica " + std::to_string(i) + " position (" + std::to_string(x) + "," + std::to_string(y) + ") outside the " + std::to_string(s) + "x" + std::to_string(s) + " grid");
+            if (id[y * s + x] >= 0)
+                raise(NBBGPU_ERR_PARSE, "descriptor: duplicate replica position (" + std::to_string(x) + "," + std::to_string(y) + ")");
+            id[y * s + x] = i;
+            gx[i] = x;
+            gy[i] = y;
+        }
+        side = ipow(s, r);
+        w = ipow(k, (r + 1) / 2);
+        h = ipow(k, r / 2);
+        spow.resize(r + 1);
+        spow[0] = 1;
+        for (int mu = 0; mu < r; ++mu) spow[mu + 1] = spow[mu] * s;
+    }
+    // try_to_compact at level `lev` (maps.cpp:80-107)
+    bool nu(int64_t x, int64_t y, int64_t& cx, int64_t& cy, int lev) const {
+        int64_t ax = 0, ay = 0, p = 1;
+        for (int mu = 0; mu < lev; ++mu) {
+            const int i = id[(y % s) * s + (x % s)];
+            if (i < 0) return false;
+            if ((mu & 1) == 0) ax += i * p;
+            else { ay += i * p; p *= k; }
+            x /= s;
+            y /= s;
+        }
+        cx = ax;
+        cy = ay;
+        return true;
+    }
+    // to_embedded at level `lev` (maps.cpp:123-146)
+    void lambda(int64_t cx, int64_t cy, int64_t& x, int64_t& y, int lev) const {
+        int64_t ex = 0, ey = 0, sp = 1;
+        for (int mu = 0; mu < lev; ++mu) {
+            int d;
+            if ((mu & 1) == 0) { d = (int)(cx % k); cx /= k; }
+            else { d = (int)(cy % k); cy /= k; }
+            ex += gx[d] * sp;
+            ey += gy[d] * sp;
+            sp *= s;
+        }
+        x = ex;
+        y = ey;
+    }
+    // host twin of coarse_neighbor (tiled.cuh)
+    bool coarse_neighbor(int L, int64_t X, int64_t Y, int dx, int dy, int64_t& X2, int64_t& Y2) const {
+        int64_t cx = X, cy = Y, pw = 1, nx = X, ny = Y;
+        for (int mu = 0; mu < L; ++mu) {
+            if (dx == 0 && dy == 0) break;
+            int d;
+            if ((mu & 1) == 0) { d = (int)(cx % k); cx /= k; }
+            else { d = (int)(cy % k); cy /= k; }
+            int ggx = gx[d] + dx, ggy = gy[d] + dy;
+            dx = ggx < 0 ? -1 : (ggx >= s ? 1 : 0);
+            ggx -= dx * s;
+            dy = ggy < 0 ? -1 : (ggy >= s ? 1 : 0);
+            ggy -= dy * s;
+            const int i2 = id[ggy * s + ggx];
+            if (i2 < 0) return false;
+            if ((mu & 1) == 0) nx += (int64_t)(i2 - d) * pw;
+            else { ny += (int64_t)(i2 - d) * pw; pw *= k; }
+        }
+        X2 = nx;
+        Y2 = ny;
+        return dx == 0 && dy == 0;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Tile plan (tiled.cuh): local neighbour table + halo slots for tile level q.
+// ---------------------------------------------------------------------------
+struct TilePlan {
+    int q = 0, wq = 1, C = 1, nH = 0, L = 0;
+    int64_t Wc = 0, Hc = 0;
+    uint32_t dmask = 0;
+    std::vector<uint32_t> nbr;  // C*8 byte offsets
+    std::vector<uint8_t> hD;
+    std::vector<uint16_t> ha, hc;
+    uint16_t first[10] = {0};
+    uint32_t wpg = 0, smem_per_warp = 0;
+    int G = 1;
+};
+
+const int kOff[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {1, 1}, {1, -1}, {-1, 1}, {-1, -1}};
+
+TilePlan build_plan(const HostFrac& F, int q, int deg) {
+    TilePlan P;
+    P.q = q;
+    P.wq = (int)HostFrac::ipow(F.k, q / 2);
+    P.C = P.wq * P.wq;
+    P.L = F.r - q;
+    P.Wc = F.w / P.wq;
+    P.Hc = F.h / P.wq;
+    const int64_t tside = F.spow[q];
+    struct Slot { int D, a, c; };
+    std::vector<Slot> slots;
+    std::map<std::tuple<int, int, int>, int> slot_of;
+    std::vector<std::vector<int>> raw(P.C);  // neighbour: >= 0 local, < 0 -> -(slot+1), absent skipped
+    for (int i = 0; i < P.C; ++i) {
+        const int c = i % P.wq, a = i / P.wq;
+        int64_t lx, ly;
+        F.lambda(c, a, lx, ly, q);
+        for (int j = 0; j < deg; ++j) {
+            int64_t nx = lx + kOff[j][0], ny = ly + kOff[j][1];
+            const int Dx = nx < 0 ? -1 : (nx >= tside ? 1 : 0);
+            const int Dy = ny < 0 ? -1 : (ny >= tside ? 1 : 0);
+            int64_t ncx, ncy;
+            if (!F.nu(nx - Dx * tside, ny - Dy * tside, ncx, ncy, q)) continue;  // hole
+            if (Dx == 0 && Dy == 0) {
+                raw[i].push_back((int)(ncy * P.wq + ncx));
+            } else {
+                const int D = (Dy + 1) * 3 + (Dx + 1);
+                auto key = std::make_tuple(D, (int)ncy, (int)ncx);
+                auto it = slot_of.find(key);
+                int sidx;
+                if (it == slot_of.end()) {
+                    sidx = (int)slots.size();
+                    slot_of[key] = sidx;
+                    slots.push_back({D, (int)ncy, (int)ncx});
+                } else {
+                    sidx = it->second;
+                }
+                raw[i].push_back(-(sidx + 1));
+            }
+        }
+    }
+    // sort slots by D, renumber
+    std::vector<int> order(slots.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return slots[x].D < slots[y].D; });
+    std::vector<int> newidx(slots.size());
+    for (size_t i = 0; i < order.size(); ++i) newidx[order[i]] = (int)i;
+    P.nH = (int)slots.size();
+    if (P.nH > kMaxHalo) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "tile halo too large");
+    P.hD.resize(P.nH);
+    P.ha.resize(P.nH);
+    P.hc.resize(P.nH);
+    for (int i = 0; i < P.nH; ++i) {
+        const Slot& s = slots[order[i]];
+        P.hD[i] = (uint8_t)s.D;
+        P.ha[i] = (uint16_t)s.a;
+        P.hc[i] = (uint16_t)s.c;
+        P.dmask |= 1u << s.D;
+    }
+    for (int D = 0; D <= 9; ++D) {
+        int cnt = 0;
+        for (int i = 0; i < P.nH; ++i) cnt += P.hD[i] < D;
+        P.first[D] = (uint16_t)cnt;
+    }
+    const uint32_t zero_word = (uint32_t)(P.C + P.nH);
+    P.nbr.assign((size_t)P.C * 8, zero_word * 4);
+    for (int i = 0; i < P.C; ++i)
+        for (size_t j = 0; j < raw[i].size(); ++j) {
+            const int v = raw[i][j];
+            const uint32_t word = v >= 0 ? (uint32_t)v : (uint32_t)(P.C + newidx[-v - 1]);
+            P.nbr[(size_t)i * 8 + j] = word * 4;
+        }
+    P.wpg = (uint32_t)((P.C + P.nH + 1 + 3) & ~3);
+    P.G = std::max(1, 32 / P.wq);
+    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + P.C) * 4 + P.G * 9 * 32 * 8);
+    return P;
+}
+
+bool tiled_width_supported(int wq) {
+    switch (wq) {
+        case 3: case 4: case 5: case 7: case 8: case 9: case 12: case 16: case 25: case 27: return true;
+        default: return false;
+    }
+}
+
+// Largest even q <= r with a supported tile width and k^q <= 1024 cells.
+int choose_tile_level(const HostFrac& F) {
+    int best = 0;
+    for (int q = 2; q <= F.r; q += 2) {
+        int64_t wq = 1;
+        bool ok = true;
+        for (int i = 0; i < q / 2; ++i) {
+            wq *= F.k;
+            if (wq > 32) { ok = false; break; }
+        }
+        if (!ok) break;
+        if (wq * wq > 1024) break;
+        if (tiled_width_supported((int)wq)) best = q;
+    }
+    return best;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the handle
+// ---------------------------------------------------------------------------
+struct nbbgpu_sim {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    HostFrac hf;
+    Frac frac{};
+    MmaTables mt{};
+    int mode = NBBGPU_MODE_COMPACT;
+    uint64_t cells = 0;      // stored cells per buffer
+    uint8_t* buf[2] = {nullptr, nullptr};
+    int cur = 0;             // front = buf[cur]
+    int64_t iteration = 0;
+    unsigned long long* d_acc = nullptr;
+    int* d_flag = nullptr;
+    int kernel = NBBGPU_KERNEL_AUTO;
+    int map_variant = NBBGPU_MAP_DIGIT;
+    uint64_t bytes_held = 0;
+    // tiling
+    int q = 0;               // chosen tile level (0 = none)
+    TilePlan plan[2];        // [moore]
+    bool plan_built[2] = {false, false};
+    uint32_t* d_nbr[2] = {nullptr, nullptr};
+    uint8_t* d_hD[2] = {nullptr, nullptr};
+    uint16_t* d_ha[2] = {nullptr, nullptr};
+    uint16_t* d_hc[2] = {nullptr, nullptr};
+    // partition (rows of the partition unit: tiles when q > 0, compact rows otherwise)
+    int rank = 0, nranks = 1;
+    int part_q = 0;           // tile level the partition is expressed in
+    int64_t unit_rows = 1;    // compact rows per partition row (k^(q/2))
+    int64_t prow0 = 0, prow1 = 0;  // owned partition rows
+    std::vector<std::vector<uint64_t>> needs;   // per peer: offsets I need from peer
+    std::vector<uint64_t*> d_sends;             // per peer: offsets peer needs from me
+    std::vector<uint64_t> n_sends;
+    std::vector<uint64_t*> d_recvs;             // per peer: offsets I receive from peer
+    std::vector<uint64_t> n_recvs;
+
+    uint8_t* front() const { return buf[cur]; }
+    uint8_t* back() const { return buf[cur ^ 1]; }
+};
+
+namespace {
+
+int grid_for(uint64_t n, int block) {
+    uint64_t g = (n + block - 1) / block;
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 32));
+}
+
+void check_handle(nbbgpu_t h) {
+    if (!h) raise(NBBGPU_ERR_INVALID, "null nbbgpu handle");
+    CK(cudaSetDevice(h->device));
+}
+
+// (k, s) specialisations for the digit loops (constant divisors); 0,0 = runtime.
+#define NBB_DISPATCH_KS(F, ...)                                              \
+    do {                                                                     \
+        const int _k = (F).k, _s = (F).s;                                    \
+        if (_k == 3 && _s == 2) { NBB_CALL(3, 2, __VA_ARGS__); }             \
+        else if (_k == 8 && _s == 3) { NBB_CALL(8, 3, __VA_ARGS__); }        \
+        else if (_k == 5 && _s == 3) { NBB_CALL(5, 3, __VA_ARGS__); }        \
+        else if (_k == 7 && _s == 3) { NBB_CALL(7, 3, __VA_ARGS__); }        \
+        else if (_k == 12 && _s == 4) { NBB_CALL(12, 4, __VA_ARGS__); }      \
+        else if (_k == 4 && _s == 2) { NBB_CALL(4, 2, __VA_ARGS__); }        \
+        else { NBB_CALL(0, 0, __VA_ARGS__); }                                \
+    } while (0)
+
+void ensure_plan(nbbgpu_t h, int moore) {
+    if (h->q == 0 || h->plan_built[moore]) return;
+    TilePlan P = build_plan(h->hf, h->q, moore ? 8 : 4);
+    CK(cudaMalloc(&h->d_nbr[moore], P.nbr.size() * 4));
+    CK(cudaMemcpy(h->d_nbr[moore], P.nbr.data(), P.nbr.size() * 4, cudaMemcpyHostToDevice));
+    const size_t nh = std::max<size_t>(1, P.hD.size());
+    CK(cudaMalloc(&h->d_hD[moore], nh));
+    CK(cudaMalloc(&h->d_ha[moore], nh * 2));
+    CK(cudaMalloc(&h->d_hc[moore], nh * 2));
+    if (P.nH) {
+        CK(cudaMemcpy(h->d_hD[moore], P.hD.data(), P.nH, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->d_ha[moore], P.ha.data(), P.nH * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->d_hc[moore], P.hc.data(), P.nH * 2, cudaMemcpyHostToDevice));
+    }
+    h->bytes_held += P.nbr.size() * 4 + nh * 5;
+    h->plan[moore] = std::move(P);
+    h->plan_built[moore] = true;
+}
+
+int resolve_kernel(nbbgpu_t h) {
+    if (h->mode == NBBGPU_MODE_BB) return NBBGPU_KERNEL_NAIVE;
+    if (h->kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
+    if (h->q > 0) return NBBGPU_KERNEL_TILED;
+    if (h->kernel == NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
+    return NBBGPU_KERNEL_NAIVE;
+}
+
+template <int WQ, bool CONWAY>
+void launch_tiled_t(nbbgpu_t h, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
+    const size_t smem = (size_t)p.smem_per_warp * kTiledWarps;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(step_tiled_kernel<WQ, CONWAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    const uint64_t groups = (uint64_t)(p.row1 - p.row0) * p.gpr;
+    constexpr int G = (32 / WQ) > 0 ? 32 / WQ : 1;
+    const uint64_t warps = (groups + G - 1) / G;
+    int dev_blocks_per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dev_blocks_per_sm, step_tiled_kernel<WQ, CONWAY>, kTiledWarps * 32, smem));
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const uint64_t max_blocks = (uint64_t)std::max(1, dev_blocks_per_sm) * sms;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((warps + kTiledWarps - 1) / kTiledWarps, max_blocks));
+    step_tiled_kernel<WQ, CONWAY><<<(unsigned)blocks, kTiledWarps * 32, smem, h->stream>>>(p, src, dst);
+}
+
+template <bool CONWAY>
+void launch_tiled_w(nbbgpu_t h, int wq, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
+    switch (wq) {
+        case 3: launch_tiled_t<3, CONWAY>(h, p, src, dst); break;
+        case 4: launch_tiled_t<4, CONWAY>(h, p, src, dst); break;
+        case 5: launch_tiled_t<5, CONWAY>(h, p, src, dst); break;
+        case 7: launch_tiled_t<7, CONWAY>(h, p, src, dst); break;
+        case 8: launch_tiled_t<8, CONWAY>(h, p, src, dst); break;
+        case 9: launch_tiled_t<9, CONWAY>(h, p, src, dst); break;
+        case 12: launch_tiled_t<12, CONWAY>(h, p, src, dst); break;
+        case 16: launch_tiled_t<16, CONWAY>(h, p, src, dst); break;
+        case 25: launch_tiled_t<25, CONWAY>(h, p, src, dst); break;
+        case 27: launch_tiled_t<27, CONWAY>(h, p, src, dst); break;
+        default: raise(NBBGPU_ERR_OUT_OF_DOMAIN, "unsupported tile width");
+    }
+}
+
+// owned compact-index range
+void owned_range(nbbgpu_t h, uint64_t& lo, uint64_t& hi) {
+    if (h->mode == NBBGPU_MODE_BB || h->nranks == 1) {
+        lo = 0;
+        hi = h->cells;
+        return;
+    }
+    lo = (uint64_t)h->prow0 * h->unit_rows * h->hf.w;
+    hi = (uint64_t)h->prow1 * h->unit_rows * h->hf.w;
+}
+
+void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
+    const int deg = moore ? 8 : 4;
+    const uint8_t* src = h->front();
+    uint8_t* dst = h->back();
+    if (h->mode == NBBGPU_MODE_BB) {
+        const uint64_t n = (uint64_t)h->hf.side * h->hf.side;
+#define NBB_CALL(K, S, ...) step_bb_naive_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, src, dst, birth, survive, deg)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        return;
+    }
+    const int kern = resolve_kernel(h);
+    if (kern == NBBGPU_KERNEL_NAIVE) {
+        uint64_t lo, hi;
+        owned_range(h, lo, hi);
+#define NBB_CALL(K, S, ...) step_compact_naive_kernel<K, S><<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(h->frac, src, dst, lo, hi, birth, survive, deg)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        return;
+    }
+    ensure_plan(h, moore);
+    const TilePlan& P = h->plan[moore];
+    TiledParams p{};
+    p.f = h->frac;
+    p.L = P.L;
+    p.C = P.C;
+    p.nH = P.nH;
+    p.dmask = P.dmask;
+    for (int i = 0; i < 10; ++i) p.halo_first[i] = P.first[i];
+    p.Wc = (uint32_t)P.Wc;
+    p.Hc = (uint32_t)P.Hc;
+    p.gpr = (uint32_t)((P.Wc + 31) / 32);
+    if (h->nranks > 1) {
+        p.row0 = (uint32_t)h->prow0;
+        p.row1 = (uint32_t)h->prow1;
+    } else {
+        p.row0 = 0;
+        p.row1 = (uint32_t)P.Hc;
+    }
+    p.w = (uint64_t)h->hf.w;
+    p.birth = birth;
+    p.survive = survive;
+    p.nbr = h->d_nbr[moore];
+    p.halo_D = h->d_hD[moore];
+    p.halo_a = h->d_ha[moore];
+    p.halo_c = h->d_hc[moore];
+    p.smem_per_warp = P.smem_per_warp;
+    p.words_per_group = P.wpg;
+    if (p.row1 <= p.row0) return;
+    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
+    if (conway) launch_tiled_w<true>(h, P.wq, p, src, dst);
+    else launch_tiled_w<false>(h, P.wq, p, src, dst);
+}
+
+void free_all(nbbgpu_t h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    for (auto*& p : h->buf) if (p) { cudaFree(p); p = nullptr; }
+    if (h->d_acc) cudaFree(h->d_acc);
+    if (h->d_flag) cudaFree(h->d_flag);
+    for (int m = 0; m < 2; ++m) {
+        if (h->d_nbr[m]) cudaFree(h->d_nbr[m]);
+        if (h->d_hD[m]) cudaFree(h->d_hD[m]);
+        if (h->d_ha[m]) cudaFree(h->d_ha[m]);
+        if (h->d_hc[m]) cudaFree(h->d_hc[m]);
+    }
+    for (auto* p : h->d_sends) if (p) cudaFree(p);
+    for (auto* p : h->d_recvs) if (p) cudaFree(p);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+uint64_t device_hash(nbbgpu_t h, uint64_t lo, uint64_t hi) {
+    CK(cudaMemsetAsync(h->d_acc, 0, sizeof(unsigned long long), h->stream));
+    if (h->mode == NBBGPU_MODE_BB) {
+        hash_bb_kernel<<<grid_for((uint64_t)h->hf.side * h->hf.side, 256), 256, 0, h->stream>>>((uint32_t)h->hf.side, h->front(), h->d_acc);
+    } else if (hi > lo) {
+#define NBB_CALL(K, S, ...) hash_compact_kernel<K, S><<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(h->frac, h->front(), lo, hi, h->d_acc)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+    }
+    CK(cudaGetLastError());
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, h->d_acc, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return v;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// storage index of an embedded coordinate (Grid::storage_index, grid.cpp:38-66)
+bool storage_index(nbbgpu_t h, int64_t x, int64_t y, uint64_t& idx) {
+    int64_t cx, cy;
+    if (!h->hf.nu(x, y, cx, cy, h->hf.r)) return false;
+    idx = h->mode == NBBGPU_MODE_BB ? (uint64_t)(y * h->hf.side + x) : (uint64_t)(cy * h->hf.w + cx);
+    return true;
+}
+
+void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, int32_t* out,
+                   int64_t count, float* ms) {
+    if (count < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "count must be >= 0");
+    if (variant != NBBGPU_MAP_DIGIT && variant != NBBGPU_MAP_MMA) raise(NBBGPU_ERR_INVALID, "unknown map variant");
+    if (variant == NBBGPU_MAP_MMA && h->hf.r > 32) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "MMA maps support levels <= 32");
+    if (count == 0) { if (ms) *ms = 0.f; return; }
+    const size_t bytes = (size_t)count * 8;
+    const bool din = is_device_ptr(in), dout = is_device_ptr(out);
+    int2* dI = nullptr;
+    int2* dO = nullptr;
+    if (din) dI = (int2*)in; else { CK(cudaMalloc(&dI, bytes)); CK(cudaMemcpyAsync(dI, in, bytes, cudaMemcpyHostToDevice, h->stream)); }
+    if (dout) dO = (int2*)out; else CK(cudaMalloc(&dO, bytes));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    const uint64_t n = (uint64_t)count;
+    if (variant == NBBGPU_MAP_DIGIT) {
+        if (is_lambda) {
+#define NBB_CALL(K, S, ...) lambda_digit_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else {
+#define NBB_CALL(K, S, ...) nu_digit_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+    } else {
+        const int blocks = grid_for((n + 15) / 16 * 32, 256);
+        if (is_lambda) {
+#define NBB_CALL(K, S, ...) lambda_mma_kernel<K><<<blocks, 256, 0, h->stream>>>(h->frac, h->mt, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else {
+#define NBB_CALL(K, S, ...) nu_mma_kernel<S><<<blocks, 256, 0, h->stream>>>(h->frac, h->mt, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev1, h->stream));
+    if (!dout) CK(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+    if (!din) cudaFree(dI);
+    if (!dout) cudaFree(dO);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* nbbgpu_last_error(void) { return g_err.c_str(); }
+int nbbgpu_version(void) { return 1; }
+
+int nbbgpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int nbbgpu_create(const int32_t* rep, int k, int s, int level, int mode, int device,
+                  uint64_t memory_cap, nbbgpu_t* out) {
+    if (!out) { g_err = "null output handle"; return NBBGPU_ERR_INVALID; }
+    *out = nullptr;
+    nbbgpu_t h = new (std::nothrow) nbbgpu_sim();
+    if (!h) { g_err = "host allocation failed"; return NBBGPU_ERR_CAPACITY; }
+    const int rc = guarded([&] {
+        if (!rep && k > 0) raise(NBBGPU_ERR_INVALID, "null replica table");
+        if (mode != NBBGPU_MODE_COMPACT && mode != NBBGPU_MODE_BB) raise(NBBGPU_ERR_INVALID, "unknown mode");
+        h->hf.init(rep, k, s, level);
+        if (h->hf.side > (int64_t)1 << 31 || h->hf.w > (int64_t)1 << 31)
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "level " + std::to_string(level) + " exceeds the engine's 32-bit coordinate range");
+        h->mode = mode;
+        // Grid::Grid cap check (grid.cpp:16-22): per grid, cells > memory_cap
+        const int64_t cells = mode == NBBGPU_MODE_BB ? HostFrac::ipow(h->hf.side, 2) : h->hf.w * h->hf.h;
+        if ((uint64_t)cells > memory_cap)
+            raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(cells) + " cells exceeds the memory cap of " + std::to_string(memory_cap) + " bytes");
+        h->cells = (uint64_t)cells;
+        h->device = device;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&h->ev0));
+        CK(cudaEventCreate(&h->ev1));
+        // device tables
+        Frac& f = h->frac;
+        memset(&f, 0, sizeof(f));
+        f.k = k; f.s = s; f.r = level;
+        f.w = (uint32_t)h->hf.w; f.h = (uint32_t)h->hf.h; f.side = (uint32_t)h->hf.side;
+        for (int i = 0; i < kMaxS * kMaxS; ++i) f.id_of_subbox[i] = -1;
+        for (int i = 0; i < s * s; ++i) f.id_of_subbox[i] = (int8_t)h->hf.id[i];
+        for (int i = 0; i < k; ++i) { f.gx[i] = (uint8_t)h->hf.gx[i]; f.gy[i] = (uint8_t)h->hf.gy[i]; }
+        for (int mu = 0; mu < 32 && mu < level; ++mu) {
+            h->mt.spow[mu] = (uint32_t)h->hf.spow[mu];
+            int64_t t = 1;
+            for (int j = 0; j < mu / 2; ++j) t *= k;
+            h->mt.tau[mu] = (uint32_t)t;
+        }
+        // double buffer + 64 B slack for the tiled kernel's aligned 16-B accesses
+        const size_t bytes = (size_t)cells + 64;
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaMalloc(&h->buf[b], bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(cells) + " cells exceeds the device memory (memory cap)");
+            }
+            CK(cudaMemsetAsync(h->buf[b], 0, bytes, h->stream));
+        }
+        CK(cudaMalloc(&h->d_acc, sizeof(unsigned long long)));
+        CK(cudaMalloc(&h->d_flag, sizeof(int)));
+        h->bytes_held = 2 * bytes + 16;
+        h->q = mode == NBBGPU_MODE_COMPACT ? choose_tile_level(h->hf) : 0;
+        h->part_q = 0;
+        h->unit_rows = 1;
+        h->prow0 = 0;
+        h->prow1 = h->hf.h;
+        CK(cudaStreamSynchronize(h->stream));
+    });
+    if (rc != NBBGPU_OK) {
+        free_all(h);
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return NBBGPU_OK;
+}
+
+int nbbgpu_destroy(nbbgpu_t h) {
+    if (!h) return NBBGPU_OK;
+    free_all(h);
+    delete h;
+    return NBBGPU_OK;
+}
+
+int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
+    return guarded([&] {
+        check_handle(h);
+        if (!(density >= 0.0 && density <= 1.0)) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "density must be in [0,1]");
+        for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
+        h->iteration = 0;
+        const uint64_t mix = splitmix64(seed);
+        if (h->mode == NBBGPU_MODE_BB) {
+            const uint64_t n = h->cells;
+#define NBB_CALL(K, S, ...) seed_bb_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, h->front(), mix, density)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else {
+            const uint64_t n = h->cells;
+#define NBB_CALL(K, S, ...) seed_compact_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, h->front(), n, mix, density)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
+                      float* ms) {
+    check_handle(h);
+    if (nsteps < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "steps must be >= 0");
+    moore = moore ? 1 : 0;
+    if (resolve_kernel(h) == NBBGPU_KERNEL_TILED) ensure_plan(h, moore);
+    CK(cudaEventRecord(h->ev0, h->stream));
+    for (int64_t i = 0; i < nsteps; ++i) {
+        launch_step(h, birth, survive, moore);
+        h->cur ^= 1;
+        ++h->iteration;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+}
+
+int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps) {
+    return guarded([&] { step_impl(h, birth, survive, moore, nsteps, nullptr); });
+}
+
+int nbbgpu_step_timed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
+                      float* device_ms) {
+    return guarded([&] { step_impl(h, birth, survive, moore, nsteps, device_ms); });
+}
+
+int nbbgpu_state_hash(nbbgpu_t h, uint64_t* out) {
+    return guarded([&] {
+        check_handle(h);
+        if (!out) raise(NBBGPU_ERR_INVALID, "null output");
+        *out = device_hash(h, 0, h->cells);
+    });
+}
+
+int nbbgpu_state_hash_owned(nbbgpu_t h, uint64_t* out) {
+    return guarded([&] {
+        check_handle(h);
+        if (!out) raise(NBBGPU_ERR_INVALID, "null output");
+        uint64_t lo, hi;
+        owned_range(h, lo, hi);
+        *out = device_hash(h, lo, hi);
+    });
+}
+
+int nbbgpu_iteration(nbbgpu_t h, int64_t* out) {
+    return guarded([&] {
+        if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
+        *out = h->iteration;
+    });
+}
+
+int nbbgpu_stored_cells(nbbgpu_t h, uint64_t* out) {
+    return guarded([&] {
+        if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
+        *out = h->cells;
+    });
+}
+
+int nbbgpu_dims(nbbgpu_t h, int64_t* w, int64_t* hg, int64_t* side) {
+    return guarded([&] {
+        if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
+        if (w) *w = h->hf.w;
+        if (hg) *hg = h->hf.h;
+        if (side) *side = h->hf.side;
+    });
+}
+
+int nbbgpu_download(nbbgpu_t h, uint8_t* dst, uint64_t bytes) {
+    return guarded([&] {
+        check_handle(h);
+        if (bytes != h->cells) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "download size " + std::to_string(bytes) + " != stored cells " + std::to_string(h->cells));
+        if (!dst) raise(NBBGPU_ERR_INVALID, "null destination");
+        CK(cudaMemcpyAsync(dst, h->front(), bytes, cudaMemcpyDefault, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int nbbgpu_upload(nbbgpu_t h, const uint8_t* src, uint64_t bytes) {
+    return guarded([&] {
+        check_handle(h);
+        if (bytes != h->cells) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "upload size " + std::to_string(bytes) + " != stored cells " + std::to_string(h->cells));
+        if (!src) raise(NBBGPU_ERR_INVALID, "null source");
+        // stage into the back buffer, validate binary states, then publish
+        CK(cudaMemcpyAsync(h->back(), src, bytes, cudaMemcpyDefault, h->stream));
+        CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+        check_binary_kernel<<<grid_for(bytes, 256), 256, 0, h->stream>>>(h->back(), bytes, h->d_flag);
+        int flag = 0;
+        CK(cudaMemcpyAsync(&flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (flag) {
+            CK(cudaMemsetAsync(h->back(), 0, bytes, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "GPU backends store binary cell states (bytes 0/1)");
+        }
+        CK(cudaMemcpyAsync(h->front(), h->back(), bytes, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemsetAsync(h->back(), 0, bytes, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int nbbgpu_get_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t* out) {
+    return guarded([&] {
+        check_handle(h);
+        if (!out) raise(NBBGPU_ERR_INVALID, "null output");
+        // Simulation::cell (stencil.cpp:182-188)
+        if (x < 0 || y < 0 || x >= h->hf.side || y >= h->hf.side) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "embedded coordinate outside the bounding box");
+        uint64_t idx;
+        if (!storage_index(h, x, y, idx)) { *out = 0; return; }
+        CK(cudaMemcpyAsync(out, h->front() + idx, 1, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int nbbgpu_set_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t state) {
+    return guarded([&] {
+        check_handle(h);
+        // Simulation::set_cell (stencil.cpp:190-194): fractal cells only
+        if (x < 0 || y < 0 || x >= h->hf.side || y >= h->hf.side) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "embedded coordinate (" + std::to_string(x) + "," + std::to_string(y) + ") outside [0," + std::to_string(h->hf.side) + ")^2");
+        uint64_t idx;
+        if (!storage_index(h, x, y, idx)) raise(NBBGPU_ERR_NOT_IN_FRACTAL, "set_cell requires a fractal cell");
+        if (state > 1) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "GPU backends store binary cell states (bytes 0/1)");
+        CK(cudaMemcpyAsync(h->front() + idx, &state, 1, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out) {
+    return guarded([&] {
+        if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
+        *out = h->bytes_held;
+    });
+}
+
+int nbbgpu_set_kernel(nbbgpu_t h, int kernel) {
+    return guarded([&] {
+        if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
+        if (kernel < NBBGPU_KERNEL_AUTO || kernel > NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_INVALID, "unknown kernel");
+        if (kernel == NBBGPU_KERNEL_TILED && (h->mode != NBBGPU_MODE_COMPACT || h->q == 0))
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
+        if (h->nranks > 1 && kernel != h->kernel) raise(NBBGPU_ERR_INVALID, "kernel is fixed once partitioned");
+        h->kernel = kernel;
+    });
+}
+
+int nbbgpu_set_map_variant(nbbgpu_t h, int variant) {
+    return guarded([&] {
+        if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
+        if (variant != NBBGPU_MAP_DIGIT && variant != NBBGPU_MAP_MMA) raise(NBBGPU_ERR_INVALID, "unknown map variant");
+        h->map_variant = variant;
+    });
+}
+
+int nbbgpu_active_kernel(nbbgpu_t h, int* kernel, int* tile_level) {
+    return guarded([&] {
+        if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
+        const int k = resolve_kernel(h);
+        if (kernel) *kernel = k;
+        if (tile_level) *tile_level = k == NBBGPU_KERNEL_TILED ? h->q : 0;
+    });
+}
+
+int nbbgpu_stream(nbbgpu_t h, void** stream) {
+    return guarded([&] {
+        if (!h || !stream) raise(NBBGPU_ERR_INVALID, "null argument");
+        *stream = (void*)h->stream;
+    });
+}
+
+int nbbgpu_lambda_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,
+                        float* device_ms) {
+    return guarded([&] {
+        check_handle(h);
+        run_map_batch(h, true, variant, in, out, count, device_ms);
+    });
+}
+
+int nbbgpu_nu_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,
+                    float* device_ms) {
+    return guarded([&] {
+        check_handle(h);
+        run_map_batch(h, false, variant, in, out, count, device_ms);
+    });
+}
+
+int nbbgpu_front_device_ptr(nbbgpu_t h, void** out) {
+    return guarded([&] {
+        if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
+        *out = h->front();
+    });
+}
+
+}  // extern "C"
+
+#include "partition.inc"

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the golden vectors of
+the unmodified reference and against the C oracle.  Bit-exact byte equality of
+the compact state (cy*w+cx) after every step, plus state_hash equality at the
+levels where a CPU byte dump is slow.  Mirrors the reference's own tests
+(proj/tests/test_stencil.cpp, acceptance.cpp C5/C8/C9)."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import desc_from_trace
+from paper_2110_12952_b200 import (Backend, SimOptions, Simulation, StencilRule, conway_rule,
+                                   Neighborhood, builtin_descriptor, run_simulation)
+from paper_2110_12952_b200.descriptor import FractalDescriptor
+from paper_2110_12952_b200.errors import CapacityError, NotInFractal, OutOfDomain
+
+pytestmark = pytest.mark.gpu
+
+T = builtin_descriptor("sierpinski-triangle")
+CARPET = builtin_descriptor("sierpinski-carpet")
+VICSEK = builtin_descriptor("vicsek")
+SOLID = FractalDescriptor("solid", 4, 2, [(0, 0), (1, 0), (0, 1), (1, 1)])
+
+
+def rule_of(t):
+    return StencilRule(t["birth"], t["survive"],
+                       Neighborhood.Moore if t["moore"] else Neighborhood.VonNeumann)
+
+
+def fnv(buf):
+    return f"{oracle.fnv1a64(buf):016x}"
+
+
+def run_trace(t, backend, kernel="auto"):
+    d = desc_from_trace(t)
+    sim = Simulation(d, t["level"], backend, SimOptions(kernel=kernel, memory_cap=1 << 40))
+    sim.seed_random(t["seed"], t["density"])
+    rule = rule_of(t)
+    cur = 0
+    dumps = t.get("dumps", {}) if backend == Backend.GpuCompact else t.get("bb_dumps", {})
+    for s in sorted(int(k) for k in t["steps"]):
+        if s > cur:
+            sim.step(rule, s - cur)
+            cur = s
+        g = t["steps"][str(s)]
+        assert f"{sim.state_hash():016x}" == g["state_hash"], (t["fractal"], t["level"], s, kernel)
+        key = "fnv" if backend == Backend.GpuCompact else "bb_fnv"
+        if key in g:
+            assert fnv(sim.front().data) == g[key], (t["fractal"], t["level"], s, kernel, backend)
+        if str(s) in dumps:
+            assert sim.front().data.tobytes().hex() == dumps[str(s)]
+    sim.close()
+
+
+@pytest.mark.parametrize("kernel", ["auto", "naive"])
+def test_golden_traces_compact(golden, kernel):
+    for t in golden["traces"]:
+        run_trace(t, Backend.GpuCompact, kernel)
+
+
+def test_golden_traces_bb(golden):
+    for t in golden["traces"]:
+        if t["level"] <= 10 and any("bb_fnv" in v for v in t["steps"].values()):
+            run_trace(t, Backend.GpuBoundingBox)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "naive"])
+def test_golden_random_trials(golden, kernel):
+    # acceptance.cpp:202-219 (C5, 50 trials) and test_stencil.cpp:155-182
+    for t in golden["random_c5"] + golden["random_xbackend"]:
+        run_trace(t, Backend.GpuCompact, kernel)
+        if kernel == "auto":
+            run_trace(t, Backend.GpuBoundingBox)
+
+
+def test_tiled_kernel_is_used_at_scale():
+    sim = Simulation(T, 12, Backend.GpuCompact)
+    assert sim.active_kernel() == ("tiled", 6)
+    sim2 = Simulation(T, 12, Backend.GpuCompact, SimOptions(kernel="naive"))
+    assert sim2.active_kernel() == ("naive", 0)
+
+
+def _lockstep_vs_oracle(desc, r, rule, seed, density, steps, kernel="auto"):
+    o = oracle.Oracle(desc.replicas, desc.k, desc.s, r)
+    o.seed(seed, density)
+    sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 40))
+    sim.seed_random(seed, density)
+    assert np.array_equal(sim.front().data, o.front)
+    for i in range(steps):
+        o.step(rule.birth, rule.survive, rule.moore)
+        sim.step(rule)
+        got = sim.front().data
+        if not np.array_equal(got, o.front):
+            bad = np.nonzero(got != o.front)[0]
+            raise AssertionError(f"{desc.name} r={r} step {i + 1}: {bad.size} cells differ, first "
+                                 f"{bad[:8].tolist()} ({rule.to_string()}, moore={rule.moore})")
+    sim.close()
+
+
+def test_tiled_randomized_lockstep():
+    rng = np.random.default_rng(1234)
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    cases = [(T, 2), (T, 3), (T, 4), (T, 5), (T, 6), (T, 7), (T, 8), (T, 9), (T, 11),
+             (CARPET, 2), (CARPET, 3), (CARPET, 4), (VICSEK, 4), (VICSEK, 5), (H, 3), (H, 4),
+             (Y, 2), (Y, 3), (SOLID, 4), (SOLID, 5), (SOLID, 7)]
+    for desc, r in cases:
+        for trial in range(3):
+            rule = StencilRule(int(rng.integers(0, 512)), int(rng.integers(0, 512)),
+                               Neighborhood.Moore if trial != 1 else Neighborhood.VonNeumann)
+            if trial == 0:
+                rule = conway_rule()
+            _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)),
+                                float(rng.uniform(0.1, 0.9)), 4)
+
+
+def test_large_levels_hash(golden, golden_long):
+    cases = [t for t in golden["traces"] if t["level"] >= 13]
+    for key in ("t16", "c9", "t18", "h10", "y8", "t20"):
+        if key in golden_long:
+            cases.append(golden_long[key])
+    for t in cases:
+        d = desc_from_trace(t)
+        sim = Simulation(d, t["level"], Backend.GpuCompact, SimOptions(memory_cap=1 << 40))
+        sim.seed_random(t["seed"], t["density"])
+        rule = rule_of(t)
+        hashes = t.get("state_hash") or {k: v["state_hash"] for k, v in t["steps"].items()}
+        cur = 0
+        for s in sorted(int(k) for k in hashes):
+            sim.step(rule, s - cur)
+            cur = s
+            assert f"{sim.state_hash():016x}" == hashes[str(s)], (t["fractal"], t["level"], s)
+        sim.close()
+
+
+def test_survey_r20_hash():
+    # T r=20 (3^20 cells), seed 42, density 0.5, B3/S23, reference hashes
+    sim = Simulation(T, 20, Backend.GpuCompact, SimOptions(memory_cap=1 << 40))
+    sim.seed_random(42, 0.5)
+    assert f"{sim.state_hash():016x}" == "b97b1b7132951b93"
+    sim.step(conway_rule())
+    assert f"{sim.state_hash():016x}" == "4cc6771ca85cba3d"
+    sim.close()
+
+
+def test_trivial_steps():
+    # test_stencil.cpp:51-67
+    for backend in (Backend.GpuBoundingBox, Backend.GpuCompact):
+        sim = Simulation(T, 3, backend)
+        sim.seed_random(1, 0.0)
+        sim.step(conway_rule())
+        assert sim.state_hash() == 0
+        sim.seed_random(1, 0.0)
+        sim.set_cell((0, 0), 1)
+        sim.step(conway_rule())
+        assert sim.state_hash() == 0
+
+
+def test_blinker_on_solid_grid():
+    # test_stencil.cpp:69-95
+    for backend in (Backend.GpuBoundingBox, Backend.GpuCompact):
+        for kernel in ("auto", "naive"):
+            if backend == Backend.GpuBoundingBox and kernel != "auto":
+                continue
+            sim = Simulation(SOLID, 2, backend, SimOptions(kernel=kernel))
+            sim.seed_random(0, 0.0)
+            for y in range(3):
+                sim.set_cell((1, y), 1)
+            sim.step(conway_rule())
+            assert [sim.cell(p) for p in [(0, 1), (1, 1), (2, 1), (1, 0), (1, 2)]] == [1, 1, 1, 0, 0]
+            sim.step(conway_rule())
+            assert [sim.cell(p) for p in [(1, 0), (1, 2), (3, 0), (3, 3)]] == [1, 1, 0, 0]
+
+
+def test_b0_rule_keeps_holes_dead():
+    # test_stencil.cpp:185-210
+    rule = StencilRule.parse("B012345678/S012345678")
+    sim = Simulation(T, 3, Backend.GpuBoundingBox)
+    sim.seed_random(5, 0.5)
+    sim.step(rule, 4)
+    buf = sim.front().data.reshape(8, 8)
+    for y in range(8):
+        for x in range(8):
+            if x & y:
+                assert buf[y, x] == 0
+
+
+def test_seeding_layout_independent():
+    # test_stencil.cpp:97-122
+    bb = Simulation(CARPET, 3, Backend.GpuBoundingBox)
+    cp = Simulation(CARPET, 3, Backend.GpuCompact)
+    bb.seed_random(1234, 0.4)
+    cp.seed_random(1234, 0.4)
+    o = oracle.Oracle(CARPET.replicas, 8, 3, 3)
+    for y in range(27):
+        for x in range(27):
+            if o.to_compact(x, y) is not None:
+                assert bb.cell((x, y)) == cp.cell((x, y))
+    with pytest.raises(OutOfDomain):
+        cp.seed_random(7, 1.5)
+    with pytest.raises(OutOfDomain):
+        cp.seed_random(7, -0.1)
+
+
+def test_errors_and_validation():
+    sim = Simulation(T, 2, Backend.GpuCompact)
+    with pytest.raises(NotInFractal):
+        sim.set_cell((1, 1), 1)
+    with pytest.raises(OutOfDomain):
+        sim.cell((4, 0))
+    with pytest.raises(OutOfDomain):
+        sim.set_cell((0, 0), 2)  # binary states only on the GPU
+    with pytest.raises(OutOfDomain):
+        sim.upload(np.full(9, 3, dtype=np.uint8))
+    assert sim.cell((1, 1)) == 0  # holes read dead
+    # memory cap semantics (grid.cpp:18-22, acceptance C8)
+    with pytest.raises(CapacityError, match="memory cap"):
+        Simulation(T, 16, Backend.GpuBoundingBox)
+    Simulation(T, 16, Backend.GpuCompact).close()
+    with pytest.raises(OutOfDomain):
+        Simulation(T, 3, Backend.GpuCompact, SimOptions(block_size=2))
+
+
+def test_upload_download_roundtrip():
+    o = oracle.Oracle(T.replicas, 3, 2, 9)
+    o.seed(77, 0.3)
+    sim = Simulation(T, 9, Backend.GpuCompact)
+    sim.upload(o.front)
+    assert np.array_equal(sim.front().data, o.front)
+    assert sim.state_hash() == o.state_hash()
+
+
+def test_run_simulation_determinism():
+    # test_stencil.cpp:212-229
+    a = run_simulation(VICSEK, 3, Backend.GpuCompact, conway_rule(), 20, 7, 0.5)
+    b = run_simulation(VICSEK, 3, Backend.GpuCompact, conway_rule(), 20, 7, 0.5)
+    assert a.state_hash == b.state_hash and a.steps == 20 and len(a.step_ms) == 20
+    zero = run_simulation(VICSEK, 3, Backend.GpuCompact, conway_rule(), 0, 7, 0.5)
+    o = oracle.Oracle(VICSEK.replicas, 5, 3, 3)
+    o.seed(7, 0.5)
+    assert zero.state_hash == o.state_hash()
+    with pytest.raises(OutOfDomain):
+        run_simulation(T, 3, Backend.GpuCompact, conway_rule(), -1, 0, 0.5)
