@@ -250,7 +250,8 @@ TilePlan build_plan(const HostFrac& F, int q, int deg) {
         }
     P.wpg = (uint32_t)((P.C + P.nH + 1 + 3) & ~3);
     P.G = std::max(1, 32 / P.wq);
-    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + P.C) * 4 + P.G * 9 * 32 * 8);
+    const uint32_t cpad = (uint32_t)((P.C + 3) & ~3);
+    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + cpad) * 4 + P.G * 9 * 32 * 8);  // 16-B multiple
     return P;
 }
 

@@ -183,14 +183,15 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
     constexpr int C = WQ * WQ;
     constexpr int G = (32 / HQ) > 0 ? (32 / HQ) : 1;    // groups per warp
     constexpr int NW = (32 * WQ + 31) / 32;             // words of a 32-tile row
+    constexpr int CP = (C + 3) & ~3;                    // WO words, padded to 16 B
     extern __shared__ __align__(16) uint8_t smem_raw[];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw + warp * p.smem_per_warp);
-    // per group slot: WD [words_per_group] | WO [C] ; then HB: G x 9 x 32 u64
+    // per group slot: WD [words_per_group] | WO [CP] ; then HB: G x 9 x 32 u64
     const uint32_t wpg = p.words_per_group;
-    uint64_t* HB = reinterpret_cast<uint64_t*>(wbase + G * (wpg + C));
+    uint64_t* HB = reinterpret_cast<uint64_t*>(wbase + G * (wpg + CP));
 
     uint32_t KB[9], KS[9];
 #pragma unroll
@@ -266,7 +267,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                     R[b] = v & mask;
                 }
                 transpose32(R);  // R[c] bit b = tile b, local (a, c)
-                uint32_t* WD = wbase + gs * (wpg + C);
+                uint32_t* WD = wbase + gs * (wpg + CP);
 #pragma unroll
                 for (int c = 0; c < WQ; ++c) WD[a * WQ + c] = R[c];
             }
@@ -274,7 +275,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
         // ---------------- halo words -----------------------------------------
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
-            uint32_t* WD = wbase + gs * (wpg + C);
+            uint32_t* WD = wbase + gs * (wpg + CP);
 #pragma unroll 1
             for (int j0 = 0; j0 < p.nH; j0 += kHaloBatch) {
                 uint8_t hv[kHaloBatch];
@@ -301,8 +302,8 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
 #pragma unroll 1
         for (int i = lane; i < G * C; i += 32) {
             const int gs = i / C, li = i - gs * C;
-            const uint32_t* WD = wbase + gs * (wpg + C);
-            uint32_t* WO = wbase + gs * (wpg + C) + wpg;
+            const uint32_t* WD = wbase + gs * (wpg + CP);
+            uint32_t* WO = wbase + gs * (wpg + CP) + wpg;
             const uint4 n0 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8));
             const uint4 n1 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8) + 1);
             const uint8_t* WB = reinterpret_cast<const uint8_t*>(WD);
@@ -329,7 +330,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                 const uint64_t seg = ((uint64_t)Y * HQ + a) * p.w + (uint64_t)X0 * WQ;
                 const int segbytes = nb * WQ;
                 const int delta = (int)(seg & 15);
-                const uint32_t* WO = wbase + gs * (wpg + C) + wpg;
+                const uint32_t* WO = wbase + gs * (wpg + CP) + wpg;
                 uint32_t R[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) R[c] = c < WQ ? WO[a * WQ + c] : 0u;
