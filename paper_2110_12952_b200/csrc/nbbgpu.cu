@@ -172,6 +172,9 @@ struct TilePlan {
     uint16_t first[10] = {0};
     uint32_t wpg = 0, smem_per_warp = 0;
     int G = 1;
+    int nD = 0;
+    int8_t dlist[8] = {0};
+    std::vector<uint8_t> hDslot;  // per slot: index into dlist
 };
 
 const int kOff[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {1, 1}, {1, -1}, {-1, 1}, {-1, -1}};
@@ -240,6 +243,12 @@ TilePlan build_plan(const HostFrac& F, int q, int deg) {
         for (int i = 0; i < P.nH; ++i) cnt += P.hD[i] < D;
         P.first[D] = (uint16_t)cnt;
     }
+    for (int D = 0; D < 9; ++D)
+        if ((P.dmask >> D) & 1u) P.dlist[P.nD++] = (int8_t)D;
+    P.hDslot.resize(P.nH);
+    for (int i = 0; i < P.nH; ++i)
+        for (int ds = 0; ds < P.nD; ++ds)
+            if (P.dlist[ds] == P.hD[i]) P.hDslot[i] = (uint8_t)ds;
     const uint32_t zero_word = (uint32_t)(P.C + P.nH);
     P.nbr.assign((size_t)P.C * 8, zero_word * 4);
     for (int i = 0; i < P.C; ++i)
@@ -251,7 +260,7 @@ TilePlan build_plan(const HostFrac& F, int q, int deg) {
     P.wpg = (uint32_t)((P.C + P.nH + 1 + 3) & ~3);
     P.G = std::max(1, 32 / P.wq);
     const uint32_t cpad = (uint32_t)((P.C + 3) & ~3);
-    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + cpad) * 4 + P.G * 9 * 32 * 8);  // 16-B multiple
+    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + cpad) * 4 + P.G * 8 * 32 * 4);  // 16-B multiple
     return P;
 }
 
@@ -274,6 +283,8 @@ int choose_tile_level(const HostFrac& F) {
         }
         if (!ok) break;
         if (wq * wq > 1024) break;
+        // the kernel packs coarse tile coordinates into 16 bits each
+        if (F.w / wq > 65535 || F.h / wq > 65535) continue;
         if (tiled_width_supported((int)wq)) best = q;
     }
     return best;
@@ -359,7 +370,7 @@ void ensure_plan(nbbgpu_t h, int moore) {
     CK(cudaMalloc(&h->d_ha[moore], nh * 2));
     CK(cudaMalloc(&h->d_hc[moore], nh * 2));
     if (P.nH) {
-        CK(cudaMemcpy(h->d_hD[moore], P.hD.data(), P.nH, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->d_hD[moore], P.hDslot.data(), P.nH, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->d_ha[moore], P.ha.data(), P.nH * 2, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->d_hc[moore], P.hc.data(), P.nH * 2, cudaMemcpyHostToDevice));
     }
@@ -376,41 +387,41 @@ int resolve_kernel(nbbgpu_t h) {
     return NBBGPU_KERNEL_NAIVE;
 }
 
-template <int WQ, bool CONWAY>
+template <int WQ, int K, int S, bool CONWAY>
 void launch_tiled_t(nbbgpu_t h, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
+    auto kern = step_tiled_kernel<WQ, K, S, CONWAY>;
     const size_t smem = (size_t)p.smem_per_warp * kTiledWarps;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(step_tiled_kernel<WQ, CONWAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_set = true;
     }
     const uint64_t groups = (uint64_t)(p.row1 - p.row0) * p.gpr;
     constexpr int G = (32 / WQ) > 0 ? 32 / WQ : 1;
     const uint64_t warps = (groups + G - 1) / G;
-    int dev_blocks_per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dev_blocks_per_sm, step_tiled_kernel<WQ, CONWAY>, kTiledWarps * 32, smem));
+    int blocks_per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kTiledWarps * 32, smem));
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    const uint64_t max_blocks = (uint64_t)std::max(1, dev_blocks_per_sm) * sms;
+    const uint64_t max_blocks = (uint64_t)std::max(1, blocks_per_sm) * sms;
     const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((warps + kTiledWarps - 1) / kTiledWarps, max_blocks));
-    step_tiled_kernel<WQ, CONWAY><<<(unsigned)blocks, kTiledWarps * 32, smem, h->stream>>>(p, src, dst);
+    kern<<<(unsigned)blocks, kTiledWarps * 32, smem, h->stream>>>(p, src, dst);
 }
 
 template <bool CONWAY>
 void launch_tiled_w(nbbgpu_t h, int wq, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
-    switch (wq) {
-        case 3: launch_tiled_t<3, CONWAY>(h, p, src, dst); break;
-        case 4: launch_tiled_t<4, CONWAY>(h, p, src, dst); break;
-        case 5: launch_tiled_t<5, CONWAY>(h, p, src, dst); break;
-        case 7: launch_tiled_t<7, CONWAY>(h, p, src, dst); break;
-        case 8: launch_tiled_t<8, CONWAY>(h, p, src, dst); break;
-        case 9: launch_tiled_t<9, CONWAY>(h, p, src, dst); break;
-        case 12: launch_tiled_t<12, CONWAY>(h, p, src, dst); break;
-        case 16: launch_tiled_t<16, CONWAY>(h, p, src, dst); break;
-        case 25: launch_tiled_t<25, CONWAY>(h, p, src, dst); break;
-        case 27: launch_tiled_t<27, CONWAY>(h, p, src, dst); break;
-        default: raise(NBBGPU_ERR_OUT_OF_DOMAIN, "unsupported tile width");
-    }
+    const int k = h->hf.k, s = h->hf.s;
+#define NBB_TILE(W, KK, SS) if (wq == W && k == KK && s == SS) return launch_tiled_t<W, KK, SS, CONWAY>(h, p, src, dst)
+#define NBB_TILE_ANY(W) if (wq == W) return launch_tiled_t<W, 0, 0, CONWAY>(h, p, src, dst)
+    // specialised (k, s): the coarse carry walk divides by constants
+    NBB_TILE(27, 3, 2); NBB_TILE(9, 3, 2); NBB_TILE(3, 3, 2);
+    NBB_TILE(8, 8, 3); NBB_TILE(25, 5, 3); NBB_TILE(5, 5, 3); NBB_TILE(7, 7, 3);
+    NBB_TILE(12, 12, 4); NBB_TILE(16, 4, 2); NBB_TILE(4, 4, 2);
+    NBB_TILE_ANY(3); NBB_TILE_ANY(4); NBB_TILE_ANY(5); NBB_TILE_ANY(7); NBB_TILE_ANY(8);
+    NBB_TILE_ANY(9); NBB_TILE_ANY(12); NBB_TILE_ANY(16); NBB_TILE_ANY(25); NBB_TILE_ANY(27);
+#undef NBB_TILE
+#undef NBB_TILE_ANY
+    raise(NBBGPU_ERR_OUT_OF_DOMAIN, "unsupported tile width");
 }
 
 // owned compact-index range
@@ -451,8 +462,8 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.L = P.L;
     p.C = P.C;
     p.nH = P.nH;
-    p.dmask = P.dmask;
-    for (int i = 0; i < 10; ++i) p.halo_first[i] = P.first[i];
+    p.nD = P.nD;
+    for (int i = 0; i < 8; ++i) p.dlist[i] = P.dlist[i];
     p.Wc = (uint32_t)P.Wc;
     p.Hc = (uint32_t)P.Hc;
     p.gpr = (uint32_t)((P.Wc + 31) / 32);

@@ -10,11 +10,11 @@
 // Bit b of a 32-bit word is tile b of the group (SIMD over tiles), so the
 // stencil of a local cell is a fixed bit-sliced adder over the words of its
 // neighbours -- no per-cell maps at all.  Per group and per local row a, one lane
-//   forward : loads the 32*WQ contiguous bytes of row a (16-B vector loads),
+//   forward : loads the 32*WQ contiguous bytes of row a (32-B vector loads),
 //             packs bytes to bits, cuts the 32 WQ-bit tile rows and transposes
 //             the 32x32 bit matrix in registers -> WQ words W[a][c] (bit b);
 //   program : all lanes run the table-driven bit-sliced Life step per word;
-//   backward: transposes back, unpacks bits to bytes, stores 16-B vectors.
+//   backward: transposes back, unpacks bits to bytes, stores 32-B vectors.
 // The reference semantics (stencil.cpp:334-368) are preserved bit for bit:
 // out-of-box and hole neighbours count 0, states are read from src and written
 // to dst only (double buffer).
@@ -33,15 +33,15 @@ struct TiledParams {
     int L;                   // coarse level r - q
     int C;                   // cells per tile k^q
     int nH;                  // halo slots
-    uint32_t dmask;          // bit D (= (dy+1)*3 + dx+1) set if direction D has slots
-    uint16_t halo_first[10]; // slots sorted by D: [halo_first[D], halo_first[D+1])
-    uint32_t Wc, Hc;         // coarse compact dims
+    int nD;                  // directions with halo slots
+    int8_t dlist[8];         // D (= (dy+1)*3 + dx+1) of each used direction slot
+    uint32_t Wc, Hc;         // coarse compact dims (< 65535)
     uint32_t gpr;            // groups per coarse row = ceil(Wc / 32)
     uint32_t row0, row1;     // owned coarse rows [row0, row1)
     uint64_t w;              // compact row stride (bytes)
     uint32_t birth, survive;
     const uint32_t* nbr;     // C x 8 smem byte offsets into the group's word array
-    const uint8_t* halo_D;   // per slot: direction index
+    const uint8_t* halo_D;   // per slot: direction slot (index into dlist)
     const uint16_t* halo_a;  // per slot: source local row in the neighbour tile
     const uint16_t* halo_c;  // per slot: source local column
     uint32_t smem_per_warp;  // bytes
@@ -54,17 +54,18 @@ struct TiledParams {
 // composition CoordMapper::to_embedded -> offset -> try_to_compact
 // (maps.cpp:80-146) restricted to the changed digits.
 // ---------------------------------------------------------------------------
+template <int K, int S>
 __device__ __forceinline__ bool coarse_neighbor(const Frac& f, int L, uint32_t X, uint32_t Y,
                                                 int dx, int dy, uint32_t& X2, uint32_t& Y2) {
-    const int k = f.k, s = f.s;
+    const int k = K ? K : f.k, s = S ? S : f.s;
     uint32_t cx = X, cy = Y;
     int pw = 1;
     int nx = (int)X, ny = (int)Y;
     for (int mu = 0; mu < L; ++mu) {
         if (dx == 0 && dy == 0) break;
         int d;
-        if ((mu & 1) == 0) { d = (int)(cx % k); cx /= k; }
-        else               { d = (int)(cy % k); cy /= k; }
+        if ((mu & 1) == 0) { d = (int)(cx % (uint32_t)k); cx /= (uint32_t)k; }
+        else               { d = (int)(cy % (uint32_t)k); cy /= (uint32_t)k; }
         int gx = f.gx[d] + dx, gy = f.gy[d] + dy;
         dx = gx < 0 ? -1 : (gx >= s ? 1 : 0);
         gx -= dx * s;
@@ -80,23 +81,43 @@ __device__ __forceinline__ bool coarse_neighbor(const Frac& f, int L, uint32_t X
     return dx == 0 && dy == 0;
 }
 
-// bytes (each 0/1) of a 16-B vector -> 16 bits, bit t = byte t
-__device__ __forceinline__ uint32_t pack16(const uint4 v) {
-    const uint32_t m = 0x10204080u;  // byte j bit0 -> bit 28+j, no carries for 0/1 bytes
-    const uint32_t a = (v.x * m) >> 28, b = (v.y * m) >> 28;
-    const uint32_t c = (v.z * m) >> 28, d = (v.w * m) >> 28;
-    return a | (b << 4) | (c << 8) | (d << 12);
+struct u32x8 { uint32_t v[8]; };
+
+__device__ __forceinline__ u32x8 ldg256(const void* p) {
+    u32x8 r;
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]),
+                   "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7])
+                 : "l"(p));
+    return r;
 }
 
-// 16 bits -> 16 bytes of 0/1
-__device__ __forceinline__ uint4 unpack16(uint32_t p) {
-    const uint32_t m = 0x00204081u;  // bit j -> bit 8j
-    uint4 v;
-    v.x = ((p & 0xFu) * m) & 0x01010101u;
-    v.y = (((p >> 4) & 0xFu) * m) & 0x01010101u;
-    v.z = (((p >> 8) & 0xFu) * m) & 0x01010101u;
-    v.w = (((p >> 12) & 0xFu) * m) & 0x01010101u;
-    return v;
+__device__ __forceinline__ void stg256(void* p, const u32x8& r) {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(r.v[0]), "r"(r.v[1]), "r"(r.v[2]), "r"(r.v[3]),
+                    "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]), "r"(r.v[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
+// 32 bytes (each 0/1) -> 32 bits, bit t = byte t.
+// (v * 0x10204080) >> 28 moves byte j's bit 0 to bit j with no carries for 0/1 bytes.
+__device__ __forceinline__ uint32_t pack32(const u32x8& r) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w |= ((r.v[j] * 0x10204080u) >> 28) << (4 * j);
+    return w;
+}
+
+// 32 bits -> 32 bytes of 0/1 (bit j of a nibble -> bit 8j via * 0x00204081)
+__device__ __forceinline__ u32x8 unpack32(uint32_t w) {
+    u32x8 r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = (((w >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return r;
 }
 
 // In-register 32x32 bit transpose: A[i] bit j -> A[j] bit i (Hacker's Delight 7-3).
@@ -112,23 +133,34 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
     }
 }
 
-// Store bytes [lo, hi) of a 16-B vector (0 <= lo < hi <= 16) with aligned pieces.
-__device__ __forceinline__ void store_partial16(uint8_t* p16, const uint4 v, int lo, int hi) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    int i = lo;
-    while (i < hi) {
-        if ((i & 7) == 0 && i + 8 <= hi) {
-            *reinterpret_cast<uint2*>(p16 + i) = make_uint2(w[i >> 2], w[(i >> 2) + 1]);
-            i += 8;
-        } else if ((i & 3) == 0 && i + 4 <= hi) {
-            *reinterpret_cast<uint32_t*>(p16 + i) = w[i >> 2];
-            i += 4;
-        } else if ((i & 1) == 0 && i + 2 <= hi) {
-            *reinterpret_cast<uint16_t*>(p16 + i) = (uint16_t)(w[i >> 2] >> ((i & 3) * 8));
-            i += 2;
-        } else {
-            p16[i] = (uint8_t)(w[i >> 2] >> ((i & 3) * 8));
-            i += 1;
+// Byte-exact store of bytes [lo, hi) of a 32-B chunk (0 <= lo < hi <= 32):
+// statically indexed 8/4/2/1-byte pieces (no dynamic register indexing).
+__device__ __forceinline__ void store_range32(uint8_t* p32, const u32x8& r, int lo, int hi) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // 8-byte slots
+        const int s0 = 8 * q;
+        if (lo <= s0 && s0 + 8 <= hi) {
+            *reinterpret_cast<uint2*>(p32 + s0) = make_uint2(r.v[2 * q], r.v[2 * q + 1]);
+            continue;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // words
+            const int w0 = s0 + 4 * h;
+            const uint32_t v = r.v[2 * q + h];
+            if (lo <= w0 && w0 + 4 <= hi) {
+                *reinterpret_cast<uint32_t*>(p32 + w0) = v;
+                continue;
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {  // half-words
+                const int h0 = w0 + 2 * e;
+                if (lo <= h0 && h0 + 2 <= hi) {
+                    *reinterpret_cast<uint16_t*>(p32 + h0) = (uint16_t)(v >> (16 * e));
+                } else {
+                    if (lo <= h0 && h0 < hi) p32[h0] = (uint8_t)(v >> (16 * e));
+                    if (lo <= h0 + 1 && h0 + 1 < hi) p32[h0 + 1] = (uint8_t)(v >> (16 * e + 8));
+                }
+            }
         }
     }
 }
@@ -176,22 +208,22 @@ __device__ __forceinline__ uint32_t apply_rule_bits(const Count4& c, uint32_t al
     }
 }
 
-template <int WQ, bool CONWAY>
-__global__ void __launch_bounds__(kTiledWarps * 32)
+template <int WQ, int K, int S, bool CONWAY>
+__global__ void __launch_bounds__(kTiledWarps * 32, 3)
 step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
     constexpr int HQ = WQ;
     constexpr int C = WQ * WQ;
     constexpr int G = (32 / HQ) > 0 ? (32 / HQ) : 1;    // groups per warp
-    constexpr int NW = (32 * WQ + 31) / 32;             // words of a 32-tile row
+    constexpr int NW = WQ;                              // 32-bit words of a 32-tile row
     constexpr int CP = (C + 3) & ~3;                    // WO words, padded to 16 B
     extern __shared__ __align__(16) uint8_t smem_raw[];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw + warp * p.smem_per_warp);
-    // per group slot: WD [words_per_group] | WO [CP] ; then HB: G x 9 x 32 u64
+    // per group slot: WD [words_per_group] | WO [CP] ; then HB: G x 8 x 32 packed tiles
     const uint32_t wpg = p.words_per_group;
-    uint64_t* HB = reinterpret_cast<uint64_t*>(wbase + G * (wpg + CP));
+    uint32_t* HB = wbase + G * (wpg + CP);
 
     uint32_t KB[9], KS[9];
 #pragma unroll
@@ -205,66 +237,101 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
     const uint64_t warp_global = (uint64_t)blockIdx.x * kTiledWarps + warp;
     const uint64_t nwarps = (uint64_t)gridDim.x * kTiledWarps;
 
+    // row segment of (group g, local row a): first byte and length
+    auto row_seg = [&](uint64_t g, int a, uint64_t& seg, int& segbytes) {
+        const uint32_t Y = p.row0 + (uint32_t)(g / p.gpr);
+        const uint32_t X0 = (uint32_t)(g % p.gpr) * 32;
+        segbytes = (int)min(32u, p.Wc - X0) * WQ;
+        seg = ((uint64_t)Y * HQ + a) * p.w + (uint64_t)X0 * WQ;
+    };
+    auto prefetch_group = [&](uint64_t gbase) {
+        const int gs = lane / HQ, a = lane % HQ;
+        const uint64_t g = gbase + gs;
+        if (gs < G && g < total_groups) {
+            uint64_t seg; int sb;
+            row_seg(g, a, seg, sb);
+            const uint64_t a0 = seg & ~31ull, a1 = (seg + sb + 31) & ~31ull;
+            prefetch_l2(src + a0, (uint32_t)(a1 - a0));
+        }
+    };
+
+    prefetch_group(warp_global * G);
     for (uint64_t g0 = warp_global * G; g0 < total_groups; g0 += nwarps * G) {
-        // ---------------- halo: coarse neighbour tile bases -------------------
+        // ---- L2 prefetch of the rows this warp processes next --------------------
+        prefetch_group(g0 + nwarps * G);
+        // ---- halo: coarse neighbour tiles (lane = tile b) ------------------------
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
             const uint64_t g = g0 + gs;
             const bool gvalid = g < total_groups;
             const uint32_t Y = p.row0 + (uint32_t)(gvalid ? g / p.gpr : 0);
-            const uint32_t X0 = (uint32_t)(gvalid ? (g % p.gpr) : 0) * 32;
-            const uint32_t X = X0 + lane;
+            const uint32_t X = (uint32_t)(gvalid ? (g % p.gpr) : 0) * 32 + lane;
             const bool tvalid = gvalid && X < p.Wc;
-#pragma unroll
-            for (int D = 0; D < 9; ++D) {
-                if (!((p.dmask >> D) & 1u)) continue;
-                uint64_t base = ~0ull;
-                uint32_t X2, Y2;
-                if (tvalid && coarse_neighbor(p.f, p.L, X, Y, D % 3 - 1, D / 3 - 1, X2, Y2))
-                    base = (uint64_t)Y2 * HQ * p.w + (uint64_t)X2 * WQ;
-                HB[(gs * 9 + D) * 32 + lane] = base;
+#pragma unroll 1
+            for (int ds = 0; ds < p.nD; ++ds) {
+                const int D = p.dlist[ds];
+                uint32_t packed = 0xFFFFFFFFu, X2, Y2;
+                if (tvalid && coarse_neighbor<K, S>(p.f, p.L, X, Y, D % 3 - 1, D / 3 - 1, X2, Y2))
+                    packed = (Y2 << 16) | X2;
+                HB[(gs * 8 + ds) * 32 + lane] = packed;
             }
         }
         __syncwarp();
-        // ---------------- forward: bytes -> bit-sliced words -------------------
+        // first halo batch of group slot 0: loads in flight during the forward phase
+        uint8_t hv0[kHaloBatch];
+#pragma unroll
+        for (int jj = 0; jj < kHaloBatch; ++jj) {
+            hv0[jj] = 0;
+            if (jj < p.nH) {
+                const uint32_t t = HB[p.halo_D[jj] * 32 + lane];
+                if (t != 0xFFFFFFFFu)
+                    hv0[jj] = __ldg(src + ((uint64_t)(t >> 16) * HQ + p.halo_a[jj]) * p.w +
+                                    (uint64_t)(t & 0xFFFFu) * WQ + p.halo_c[jj]);
+            }
+        }
+        // ---- forward: bytes -> bit-sliced words ------------------------------------
         {
             const int gs = lane / HQ, a = lane % HQ;
             const uint64_t g = g0 + gs;
             if (gs < G && g < total_groups) {
-                const uint32_t Y = p.row0 + (uint32_t)(g / p.gpr);
-                const uint32_t X0 = (uint32_t)(g % p.gpr) * 32;
-                const int nb = (int)min(32u, p.Wc - X0);
-                const uint64_t seg = ((uint64_t)Y * HQ + a) * p.w + (uint64_t)X0 * WQ;
-                const int segbytes = nb * WQ;
-                const int delta = (int)(seg & 15);
-                const uint4* ap = reinterpret_cast<const uint4*>(src + (seg - delta));
-                const int nchunks = (delta + segbytes + 15) >> 4;
-                // aligned bit string AW (bit t = byte abase + t), NW+1 words
-                uint32_t AW[NW + 1];
+                uint64_t seg; int segbytes;
+                row_seg(g, a, seg, segbytes);
+                const int delta = (int)(seg & 31);
+                const uint8_t* ap = src + (seg - delta);
+                const int nchunks = (delta + segbytes + 31) >> 5;
+                const int nb = segbytes / WQ;
+                // Streamed: aligned word t (bit i = byte abase+32t+i) -> delta-shifted
+                // word SW_t -> every tile row R_b whose last bit lies in SW_t.
+                // Loads run PF chunks ahead; only a 2-word window stays live.
+                constexpr int PF = 2;
+                constexpr uint32_t mask = (WQ >= 32) ? 0xFFFFFFFFu : ((1u << WQ) - 1u);
+                u32x8 q[PF];
 #pragma unroll
-                for (int t = 0; t <= NW; ++t) {
-                    uint32_t lo = 0, hi = 0;
-                    if (2 * t < nchunks) lo = pack16(__ldg(ap + 2 * t));
-                    if (2 * t + 1 < nchunks) hi = pack16(__ldg(ap + 2 * t + 1));
-                    AW[t] = lo | (hi << 16);
-                }
-                // shift by delta -> SW (bit t = byte seg + t), clip to segbytes
-                uint32_t SW[NW];
-#pragma unroll
-                for (int t = 0; t < NW; ++t) {
-                    uint32_t v = __funnelshift_r(AW[t], AW[t + 1], delta);
-                    const int rem = segbytes - 32 * t;
-                    if (rem < 32) v = rem <= 0 ? 0u : (v & ((1u << rem) - 1u));
-                    SW[t] = v;
-                }
+                for (int i = 0; i < PF; ++i)
+                    if (i + 1 <= NW && i + 1 < nchunks) q[i] = ldg256(ap + 32 * (i + 1));
+                uint32_t awcur = pack32(ldg256(ap)), swprev = 0;
                 uint32_t R[32];
 #pragma unroll
-                for (int b = 0; b < 32; ++b) {
-                    constexpr uint32_t mask = (WQ >= 32) ? 0xFFFFFFFFu : ((1u << WQ) - 1u);
-                    const int bit = WQ * b, t0 = bit >> 5, sh = bit & 31;
-                    uint32_t v = SW[t0] >> sh;
-                    if (sh + WQ > 32 && t0 + 1 < NW) v = __funnelshift_r(SW[t0], SW[t0 + 1], sh);
-                    R[b] = v & mask;
+                for (int t = 0; t < NW; ++t) {
+                    const uint32_t awnext = (t + 1 < nchunks) ? pack32(q[t % PF]) : 0u;
+                    if (t + 1 + PF <= NW && t + 1 + PF < nchunks) q[t % PF] = ldg256(ap + 32 * (t + 1 + PF));
+                    const uint32_t sw = __funnelshift_r(awcur, awnext, delta);
+#pragma unroll
+                    for (int b = 0; b < 32; ++b) {
+                        const int bit = WQ * b, t0 = bit >> 5, sh = bit & 31;
+                        const int tend = (bit + WQ - 1) >> 5;
+                        if (tend == t) {
+                            const uint32_t v = (t0 == t) ? (sw >> sh) : __funnelshift_r(swprev, sw, sh);
+                            R[b] = v & mask;
+                        }
+                    }
+                    swprev = sw;
+                    awcur = awnext;
+                }
+                if (nb < 32) {
+#pragma unroll
+                    for (int b = 0; b < 32; ++b)
+                        if (b >= nb) R[b] = 0;
                 }
                 transpose32(R);  // R[c] bit b = tile b, local (a, c)
                 uint32_t* WD = wbase + gs * (wpg + CP);
@@ -272,21 +339,27 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                 for (int c = 0; c < WQ; ++c) WD[a * WQ + c] = R[c];
             }
         }
-        // ---------------- halo words -----------------------------------------
+        // ---- halo words ---------------------------------------------------------------
+#pragma unroll
+        for (int jj = 0; jj < kHaloBatch; ++jj) {
+            const uint32_t word = __ballot_sync(0xffffffffu, hv0[jj] != 0);
+            if (lane == jj && jj < p.nH) wbase[C + jj] = word;
+        }
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
             uint32_t* WD = wbase + gs * (wpg + CP);
 #pragma unroll 1
-            for (int j0 = 0; j0 < p.nH; j0 += kHaloBatch) {
+            for (int j0 = gs == 0 ? kHaloBatch : 0; j0 < p.nH; j0 += kHaloBatch) {
                 uint8_t hv[kHaloBatch];
 #pragma unroll
                 for (int jj = 0; jj < kHaloBatch; ++jj) {
                     const int j = j0 + jj;
                     hv[jj] = 0;
                     if (j < p.nH) {
-                        const uint64_t base = HB[(gs * 9 + p.halo_D[j]) * 32 + lane];
-                        if (base != ~0ull)
-                            hv[jj] = __ldg(src + base + (uint64_t)p.halo_a[j] * p.w + p.halo_c[j]);
+                        const uint32_t t = HB[(gs * 8 + p.halo_D[j]) * 32 + lane];
+                        if (t != 0xFFFFFFFFu)
+                            hv[jj] = __ldg(src + ((uint64_t)(t >> 16) * HQ + p.halo_a[j]) * p.w +
+                                           (uint64_t)(t & 0xFFFFu) * WQ + p.halo_c[j]);
                     }
                 }
 #pragma unroll
@@ -298,7 +371,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
             if (lane == 0) WD[C + p.nH] = 0u;  // the "absent" neighbour
         }
         __syncwarp();
-        // ---------------- program: bit-sliced step on every local cell ---------
+        // ---- program: bit-sliced step on every local cell ------------------------
 #pragma unroll 1
         for (int i = lane; i < G * C; i += 32) {
             const int gs = i / C, li = i - gs * C;
@@ -319,55 +392,46 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
             WO[li] = apply_rule_bits<CONWAY>(cnt, WD[li], KB, KS);
         }
         __syncwarp();
-        // ---------------- backward: words -> bytes -----------------------------
+        // ---- backward: words -> bytes ----------------------------------------------
         {
             const int gs = lane / HQ, a = lane % HQ;
             const uint64_t g = g0 + gs;
             if (gs < G && g < total_groups) {
-                const uint32_t Y = p.row0 + (uint32_t)(g / p.gpr);
-                const uint32_t X0 = (uint32_t)(g % p.gpr) * 32;
-                const int nb = (int)min(32u, p.Wc - X0);
-                const uint64_t seg = ((uint64_t)Y * HQ + a) * p.w + (uint64_t)X0 * WQ;
-                const int segbytes = nb * WQ;
-                const int delta = (int)(seg & 15);
+                uint64_t seg; int segbytes;
+                row_seg(g, a, seg, segbytes);
+                const int delta = (int)(seg & 31);
                 const uint32_t* WO = wbase + gs * (wpg + CP) + wpg;
                 uint32_t R[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) R[c] = c < WQ ? WO[a * WQ + c] : 0u;
                 transpose32(R);  // R[b] bit c
-                uint32_t SW[NW];
-#pragma unroll
-                for (int t = 0; t < NW; ++t) SW[t] = 0;
-#pragma unroll
-                for (int b = 0; b < 32; ++b) {
-                    const int bit = WQ * b, t0 = bit >> 5, sh = bit & 31;
-                    SW[t0] |= R[b] << sh;
-                    if (sh + WQ > 32 && t0 + 1 < NW) SW[t0 + 1] |= R[b] >> (32 - sh);
-                }
-                // shift left by delta into the aligned frame
-                uint32_t AW[NW + 1];
-                AW[0] = SW[0] << delta;
-#pragma unroll
-                for (int t = 1; t < NW; ++t) AW[t] = __funnelshift_l(SW[t - 1], SW[t], delta);
-                AW[NW] = delta ? (SW[NW - 1] >> (32 - delta)) : 0u;
                 uint8_t* ap = dst + (seg - delta);
-                const int end = delta + segbytes;  // exclusive, in aligned frame
-                const int nchunks = (end + 15) >> 4;
+                const int end = delta + segbytes;  // exclusive, in the aligned frame
+                const int nchunks = (end + 31) >> 5;
+                // Streamed: SW_t (bit i = byte seg+32t+i) is complete once every R_b
+                // overlapping it is or-ed in; aligned word t = funnel(SW_{t-1}, SW_t).
+                uint32_t swprev = 0;
 #pragma unroll
                 for (int t = 0; t <= NW; ++t) {
+                    uint32_t sw = 0;
+                    if (t < NW) {
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int ch = 2 * t + hh;
-                        if (ch < nchunks) {
-                            const uint4 v = unpack16(hh ? (AW[t] >> 16) : (AW[t] & 0xFFFFu));
-                            const int lo = ch == 0 ? delta : 0;
-                            const int hi = min(16, end - 16 * ch);
-                            if (lo == 0 && hi == 16)
-                                *reinterpret_cast<uint4*>(ap + 16 * ch) = v;
-                            else
-                                store_partial16(ap + 16 * ch, v, lo, hi);
+                        for (int b = 0; b < 32; ++b) {
+                            const int bit = WQ * b, t0 = bit >> 5, sh = bit & 31;
+                            const int tend = (bit + WQ - 1) >> 5;
+                            if (t0 == t) sw |= R[b] << sh;
+                            else if (tend == t) sw |= R[b] >> (32 - sh);
                         }
                     }
+                    if (t < nchunks) {
+                        const uint32_t wv = __funnelshift_l(swprev, sw, delta);
+                        const u32x8 v = unpack32(wv);
+                        const int lo = t == 0 ? delta : 0;
+                        const int hi = min(32, end - 32 * t);
+                        if (lo == 0 && hi == 32) stg256(ap + 32 * t, v);
+                        else store_range32(ap + 32 * t, v, lo, hi);
+                    }
+                    swprev = sw;
                 }
             }
         }
