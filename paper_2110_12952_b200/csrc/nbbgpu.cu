@@ -259,8 +259,8 @@ TilePlan build_plan(const HostFrac& F, int q, int deg) {
         }
     P.wpg = (uint32_t)((P.C + P.nH + 1 + 3) & ~3);
     P.G = std::max(1, 32 / P.wq);
-    const uint32_t cpad = (uint32_t)((P.C + 3) & ~3);
-    P.smem_per_warp = (uint32_t)(P.G * (P.wpg + cpad) * 4 + P.G * 8 * 32 * 4);  // 16-B multiple
+    // per warp: G x word arrays, G x 8 x 32 packed neighbour tiles, 32 cp.async rings
+    P.smem_per_warp = (uint32_t)(P.G * P.wpg * 4 + P.G * 8 * 32 * 4 + 32 * kRingLaneBytes);
     return P;
 }
 

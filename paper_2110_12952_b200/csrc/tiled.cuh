@@ -24,7 +24,9 @@
 
 namespace nbbgpu {
 
-constexpr int kTiledWarps = 8;       // warps per block
+constexpr int kTiledWarps = 4;       // warps per block
+constexpr int kRing = 6;             // cp.async ring slots (32 B) per lane
+constexpr int kRingLaneBytes = kRing * 32 + 16;  // +16: conflict-free LDS.128 across lanes
 constexpr int kHaloBatch = 8;        // halo slots gathered per batch
 constexpr int kMaxHalo = 512;
 
@@ -101,6 +103,23 @@ __device__ __forceinline__ void stg256(void* p, const u32x8& r) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
+// cp.async (LDGSTS): global -> shared without holding registers; per-thread groups.
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+__device__ __forceinline__ u32x8 lds256(uint32_t saddr) {
+    u32x8 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]) : "r"(saddr));
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7]) : "r"(saddr + 16));
+    return r;
 }
 
 // 32 bytes (each 0/1) -> 32 bits, bit t = byte t.
@@ -209,21 +228,23 @@ __device__ __forceinline__ uint32_t apply_rule_bits(const Count4& c, uint32_t al
 }
 
 template <int WQ, int K, int S, bool CONWAY>
-__global__ void __launch_bounds__(kTiledWarps * 32, 3)
+__global__ void __launch_bounds__(kTiledWarps * 32, 5)
 step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
     constexpr int HQ = WQ;
     constexpr int C = WQ * WQ;
     constexpr int G = (32 / HQ) > 0 ? (32 / HQ) : 1;    // groups per warp
     constexpr int NW = WQ;                              // 32-bit words of a 32-tile row
-    constexpr int CP = (C + 3) & ~3;                    // WO words, padded to 16 B
+    constexpr int NPL = (G * C + 31) / 32;              // program cells per lane
     extern __shared__ __align__(16) uint8_t smem_raw[];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw + warp * p.smem_per_warp);
-    // per group slot: WD [words_per_group] | WO [CP] ; then HB: G x 8 x 32 packed tiles
+    // per group slot: WD [words_per_group]; then HB: G x 8 x 32 packed tiles; then the
+    // per-lane cp.async rings (32 x kRingLaneBytes)
     const uint32_t wpg = p.words_per_group;
-    uint32_t* HB = wbase + G * (wpg + CP);
+    uint32_t* HB = wbase + G * wpg;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(HB + G * 8 * 32) + lane * kRingLaneBytes;
 
     uint32_t KB[9], KS[9];
 #pragma unroll
@@ -244,21 +265,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
         segbytes = (int)min(32u, p.Wc - X0) * WQ;
         seg = ((uint64_t)Y * HQ + a) * p.w + (uint64_t)X0 * WQ;
     };
-    auto prefetch_group = [&](uint64_t gbase) {
-        const int gs = lane / HQ, a = lane % HQ;
-        const uint64_t g = gbase + gs;
-        if (gs < G && g < total_groups) {
-            uint64_t seg; int sb;
-            row_seg(g, a, seg, sb);
-            const uint64_t a0 = seg & ~31ull, a1 = (seg + sb + 31) & ~31ull;
-            prefetch_l2(src + a0, (uint32_t)(a1 - a0));
-        }
-    };
-
-    prefetch_group(warp_global * G);
     for (uint64_t g0 = warp_global * G; g0 < total_groups; g0 += nwarps * G) {
-        // ---- L2 prefetch of the rows this warp processes next --------------------
-        prefetch_group(g0 + nwarps * G);
         // ---- halo: coarse neighbour tiles (lane = tile b) ------------------------
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
@@ -303,18 +310,32 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                 // Streamed: aligned word t (bit i = byte abase+32t+i) -> delta-shifted
                 // word SW_t -> every tile row R_b whose last bit lies in SW_t.
                 // Loads run PF chunks ahead; only a 2-word window stays live.
-                constexpr int PF = 2;
                 constexpr uint32_t mask = (WQ >= 32) ? 0xFFFFFFFFu : ((1u << WQ) - 1u);
-                u32x8 q[PF];
+                // chunk c -> ring slot c % kRing; kRing-1 chunks stay in flight
 #pragma unroll
-                for (int i = 0; i < PF; ++i)
-                    if (i + 1 <= NW && i + 1 < nchunks) q[i] = ldg256(ap + 32 * (i + 1));
-                uint32_t awcur = pack32(ldg256(ap)), swprev = 0;
+                for (int c = 0; c < kRing - 1; ++c) {
+                    if (c <= NW && c < nchunks) {
+                        cp_async16(ring + 32 * c, ap + 32 * c);
+                        cp_async16(ring + 32 * c + 16, ap + 32 * c + 16);
+                    }
+                    cp_async_commit();
+                }
+                cp_async_wait<kRing - 2>();
+                uint32_t awcur = pack32(lds256(ring)), swprev = 0;
                 uint32_t R[32];
 #pragma unroll
                 for (int t = 0; t < NW; ++t) {
-                    const uint32_t awnext = (t + 1 < nchunks) ? pack32(q[t % PF]) : 0u;
-                    if (t + 1 + PF <= NW && t + 1 + PF < nchunks) q[t % PF] = ldg256(ap + 32 * (t + 1 + PF));
+                    // refill: chunk t + kRing - 1 into the slot chunk t just vacated
+                    {
+                        const int c = t + kRing - 1;
+                        if (c <= NW && c < nchunks) {
+                            cp_async16(ring + 32 * (c % kRing), ap + 32 * c);
+                            cp_async16(ring + 32 * (c % kRing) + 16, ap + 32 * c + 16);
+                        }
+                        cp_async_commit();
+                    }
+                    cp_async_wait<kRing - 2>();  // chunk t + 1 has landed
+                    const uint32_t awnext = (t + 1 < nchunks) ? pack32(lds256(ring + 32 * ((t + 1) % kRing))) : 0u;
                     const uint32_t sw = __funnelshift_r(awcur, awnext, delta);
 #pragma unroll
                     for (int b = 0; b < 32; ++b) {
@@ -328,13 +349,14 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                     swprev = sw;
                     awcur = awnext;
                 }
+                cp_async_wait<0>();
                 if (nb < 32) {
 #pragma unroll
                     for (int b = 0; b < 32; ++b)
                         if (b >= nb) R[b] = 0;
                 }
                 transpose32(R);  // R[c] bit b = tile b, local (a, c)
-                uint32_t* WD = wbase + gs * (wpg + CP);
+                uint32_t* WD = wbase + gs * wpg;
 #pragma unroll
                 for (int c = 0; c < WQ; ++c) WD[a * WQ + c] = R[c];
             }
@@ -347,7 +369,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
         }
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
-            uint32_t* WD = wbase + gs * (wpg + CP);
+            uint32_t* WD = wbase + gs * wpg;
 #pragma unroll 1
             for (int j0 = gs == 0 ? kHaloBatch : 0; j0 < p.nH; j0 += kHaloBatch) {
                 uint8_t hv[kHaloBatch];
@@ -372,24 +394,37 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
         }
         __syncwarp();
         // ---- program: bit-sliced step on every local cell ------------------------
-#pragma unroll 1
-        for (int i = lane; i < G * C; i += 32) {
-            const int gs = i / C, li = i - gs * C;
-            const uint32_t* WD = wbase + gs * (wpg + CP);
-            uint32_t* WO = wbase + gs * (wpg + CP) + wpg;
-            const uint4 n0 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8));
-            const uint4 n1 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8) + 1);
-            const uint8_t* WB = reinterpret_cast<const uint8_t*>(WD);
-            const uint32_t x0 = *reinterpret_cast<const uint32_t*>(WB + n0.x);
-            const uint32_t x1 = *reinterpret_cast<const uint32_t*>(WB + n0.y);
-            const uint32_t x2 = *reinterpret_cast<const uint32_t*>(WB + n0.z);
-            const uint32_t x3 = *reinterpret_cast<const uint32_t*>(WB + n0.w);
-            const uint32_t x4 = *reinterpret_cast<const uint32_t*>(WB + n1.x);
-            const uint32_t x5 = *reinterpret_cast<const uint32_t*>(WB + n1.y);
-            const uint32_t x6 = *reinterpret_cast<const uint32_t*>(WB + n1.z);
-            const uint32_t x7 = *reinterpret_cast<const uint32_t*>(WB + n1.w);
-            const Count4 cnt = count8(x0, x1, x2, x3, x4, x5, x6, x7);
-            WO[li] = apply_rule_bits<CONWAY>(cnt, WD[li], KB, KS);
+        // results stay in registers until every lane has read WD, then overwrite it
+        uint32_t res[NPL];
+#pragma unroll
+        for (int m = 0; m < NPL; ++m) {
+            const int i = lane + 32 * m;
+            if (i < G * C) {
+                const int gs = i / C, li = i - gs * C;
+                const uint32_t* WD = wbase + gs * wpg;
+                const uint4 n0 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8));
+                const uint4 n1 = __ldg(reinterpret_cast<const uint4*>(p.nbr + li * 8) + 1);
+                const uint8_t* WB = reinterpret_cast<const uint8_t*>(WD);
+                const uint32_t x0 = *reinterpret_cast<const uint32_t*>(WB + n0.x);
+                const uint32_t x1 = *reinterpret_cast<const uint32_t*>(WB + n0.y);
+                const uint32_t x2 = *reinterpret_cast<const uint32_t*>(WB + n0.z);
+                const uint32_t x3 = *reinterpret_cast<const uint32_t*>(WB + n0.w);
+                const uint32_t x4 = *reinterpret_cast<const uint32_t*>(WB + n1.x);
+                const uint32_t x5 = *reinterpret_cast<const uint32_t*>(WB + n1.y);
+                const uint32_t x6 = *reinterpret_cast<const uint32_t*>(WB + n1.z);
+                const uint32_t x7 = *reinterpret_cast<const uint32_t*>(WB + n1.w);
+                const Count4 cnt = count8(x0, x1, x2, x3, x4, x5, x6, x7);
+                res[m] = apply_rule_bits<CONWAY>(cnt, WD[li], KB, KS);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < NPL; ++m) {
+            const int i = lane + 32 * m;
+            if (i < G * C) {
+                const int gs = i / C, li = i - gs * C;
+                wbase[gs * wpg + li] = res[m];
+            }
         }
         __syncwarp();
         // ---- backward: words -> bytes ----------------------------------------------
@@ -400,7 +435,7 @@ step_tiled_kernel(const TiledParams p, const uint8_t* __restrict__ src, uint8_t*
                 uint64_t seg; int segbytes;
                 row_seg(g, a, seg, segbytes);
                 const int delta = (int)(seg & 31);
-                const uint32_t* WO = wbase + gs * (wpg + CP) + wpg;
+                const uint32_t* WO = wbase + gs * wpg;  // program output overwrote WD
                 uint32_t R[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) R[c] = c < WQ ? WO[a * WQ + c] : 0u;
