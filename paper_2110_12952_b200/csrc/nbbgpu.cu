@@ -260,7 +260,7 @@ TilePlan build_plan(const HostFrac& F, int q, int deg) {
     P.wpg = (uint32_t)((P.C + P.nH + 1 + 3) & ~3);
     P.G = std::max(1, 32 / P.wq);
     // per warp: G x word arrays, G x 8 x 32 packed neighbour tiles, 32 cp.async rings
-    P.smem_per_warp = (uint32_t)(P.G * P.wpg * 4 + P.G * 8 * 32 * 4 + 32 * kRingLaneBytes);
+    P.smem_per_warp = tiled_smem_per_warp(P.wq, P.wpg);
     return P;
 }
 
@@ -317,9 +317,11 @@ struct nbbgpu_sim {
     TilePlan plan[2];        // [moore]
     bool plan_built[2] = {false, false};
     uint32_t* d_nbr[2] = {nullptr, nullptr};
+    uint32_t* d_ntab[2] = {nullptr, nullptr};  // coarse neighbour tiles [nD][Hc][Wc]
     uint8_t* d_hD[2] = {nullptr, nullptr};
     uint16_t* d_ha[2] = {nullptr, nullptr};
     uint16_t* d_hc[2] = {nullptr, nullptr};
+    uint64_t* d_hoff[2] = {nullptr, nullptr};
     // partition (rows of the partition unit: tiles when q > 0, compact rows otherwise)
     int rank = 0, nranks = 1;
     int part_q = 0;           // tile level the partition is expressed in
@@ -369,12 +371,32 @@ void ensure_plan(nbbgpu_t h, int moore) {
     CK(cudaMalloc(&h->d_hD[moore], nh));
     CK(cudaMalloc(&h->d_ha[moore], nh * 2));
     CK(cudaMalloc(&h->d_hc[moore], nh * 2));
+    CK(cudaMalloc(&h->d_hoff[moore], nh * 8));
     if (P.nH) {
+        std::vector<uint64_t> off(P.nH);
+        for (int j = 0; j < P.nH; ++j) off[j] = (uint64_t)P.ha[j] * (uint64_t)h->hf.w + P.hc[j];
+        CK(cudaMemcpy(h->d_hoff[moore], off.data(), P.nH * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->d_hD[moore], P.hDslot.data(), P.nH, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->d_ha[moore], P.ha.data(), P.nH * 2, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->d_hc[moore], P.hc.data(), P.nH * 2, cudaMemcpyHostToDevice));
     }
     h->bytes_held += P.nbr.size() * 4 + nh * 5;
+    // static coarse-neighbour table (Wc, Hc < 65536 by choose_tile_level)
+    const uint64_t ntiles = (uint64_t)P.Wc * P.Hc;
+    const size_t tbytes = std::max<size_t>(4, (size_t)P.nD * ntiles * 4);
+    if (cudaMalloc(&h->d_ntab[moore], tbytes) != cudaSuccess) {
+        cudaGetLastError();
+        raise(NBBGPU_ERR_CAPACITY, "coarse neighbour table exceeds the device memory (memory cap)");
+    }
+    h->bytes_held += tbytes;
+    if (P.nD > 0) {
+        const int8_t* d = P.dlist;
+#define NBB_CALL(K, S, ...) build_ntab_kernel<K, S><<<grid_for(ntiles, 256), 256, 0, h->stream>>>(h->frac, P.L, (uint32_t)P.Wc, (uint32_t)P.Hc, P.nD, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], h->d_ntab[moore])
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    }
     h->plan[moore] = std::move(P);
     h->plan_built[moore] = true;
 }
@@ -478,9 +500,11 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.birth = birth;
     p.survive = survive;
     p.nbr = h->d_nbr[moore];
+    p.ntab = h->d_ntab[moore];
     p.halo_D = h->d_hD[moore];
     p.halo_a = h->d_ha[moore];
     p.halo_c = h->d_hc[moore];
+    p.halo_off = h->d_hoff[moore];
     p.smem_per_warp = P.smem_per_warp;
     p.words_per_group = P.wpg;
     if (p.row1 <= p.row0) return;
@@ -497,9 +521,11 @@ void free_all(nbbgpu_t h) {
     if (h->d_flag) cudaFree(h->d_flag);
     for (int m = 0; m < 2; ++m) {
         if (h->d_nbr[m]) cudaFree(h->d_nbr[m]);
+        if (h->d_ntab[m]) cudaFree(h->d_ntab[m]);
         if (h->d_hD[m]) cudaFree(h->d_hD[m]);
         if (h->d_ha[m]) cudaFree(h->d_ha[m]);
         if (h->d_hc[m]) cudaFree(h->d_hc[m]);
+        if (h->d_hoff[m]) cudaFree(h->d_hoff[m]);
     }
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
