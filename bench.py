@@ -161,13 +161,13 @@ def run_reference(args):
     steps, warmup = args.steps, args.warmup
     # each step = one bounded sample sized so the whole run stays within minutes
     budget = max(0.3, min(2.0, 150.0 / max(1, steps + warmup)))
-    res = cpu_reference_sample(LEVEL, cells_target_s=budget, steps=steps, warmup=warmup)
+    res = cpu_reference_sample(args.level, cells_target_s=budget, steps=steps, warmup=warmup)
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": warmup, "ms_per_step": res["seconds_per_sample"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seed 42, density 0.5)", "impl": "reference",
-            "config": {"workload": "sierpinski-triangle r=20 compact, B3/S23 Moore",
-                       "level": LEVEL, "parallelism": "host threads"},
+            "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore",
+                       "level": args.level, "parallelism": "host threads"},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -185,69 +185,37 @@ def run_ours(args):
     ws, rank, local = dist_env()
     n = args.gpus if ws == 1 else ws
     dist = None
+    device = (local if ws > 1 else 0) if args.device is None else args.device
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = local if ws > 1 else 0
+        torch.cuda.set_device(device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:  # test knob: several ranks sharing one GPU, halo staged through the host
+            dist.init_process_group("gloo")
     T = builtin_descriptor("sierpinski-triangle")
     rule = conway_rule()
     L = _abi.lib()
-    sim = Simulation(T, LEVEL, Backend.GpuCompact, SimOptions(memory_cap=1 << 40, device=device))
+    sim = Simulation(T, args.level, Backend.GpuCompact, SimOptions(memory_cap=1 << 40, device=device))
     h = sim.handle()
-    cells = 3 ** LEVEL
+    cells = 3 ** args.level
     kern, q = sim.active_kernel()
     sim.seed_random(SEED, DENSITY)
 
     # ---- partition + halo plan (host-only lists; no communication needed) ----
-    peers = []
-    bufs = {}
+    dsim = None
     if ws > 1:
-        _abi.check(L.nbbgpu_partition(h, rank, ws))
-        rep = _abi.replica_array(T.replicas)
-        for p in range(ws):
-            if p == rank:
-                continue
-            cnt = C.c_uint64()
-            _abi.check(L.nbbgpu_plan_needs(rep, 3, 2, LEVEL, -1, p, ws, rank, None, C.byref(cnt)))
-            sends = (C.c_uint64 * max(1, cnt.value))()
-            _abi.check(L.nbbgpu_plan_needs(rep, 3, 2, LEVEL, -1, p, ws, rank, sends, C.byref(cnt)))
-            _abi.check(L.nbbgpu_halo_set_sends(h, p, sends, cnt.value))
-            nrecv = C.c_uint64()
-            _abi.check(L.nbbgpu_halo_needs(h, p, None, C.byref(nrecv)))
-            if cnt.value or nrecv.value:
-                peers.append(p)
-                bufs[p] = (torch.empty(max(1, cnt.value), dtype=torch.uint8, device=f"cuda:{device}"),
-                           torch.empty(max(1, nrecv.value), dtype=torch.uint8, device=f"cuda:{device}"),
-                           cnt.value, nrecv.value)
-        lo, hi = C.c_uint64(), C.c_uint64()
-        _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
-        owned = hi.value - lo.value
+        from paper_2110_12952_b200.distributed import DistributedSimulation
+        dsim = DistributedSimulation(sim, dist, rank, ws, host_transport=args.dist_backend == "gloo")
+        owned = dsim.plan.hi - dsim.plan.lo
     else:
         owned = cells
 
     def exchange():
-        if not peers:
+        if dsim is None:
             return 0
-        ops = []
-        for p in peers:
-            sb, rb, ns, nr = bufs[p]
-            if ns:
-                _abi.check(L.nbbgpu_halo_pack(h, p, C.c_void_p(sb.data_ptr())))
-                ops.append(dist.P2POp(dist.isend, sb[:ns], p))
-            if nr:
-                ops.append(dist.P2POp(dist.irecv, rb[:nr], p))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        torch.cuda.synchronize(device)
-        launches = 0
-        for p in peers:
-            sb, rb, ns, nr = bufs[p]
-            if nr:
-                _abi.check(L.nbbgpu_halo_unpack(h, p, C.c_void_p(rb.data_ptr())))
-                launches += 1
-            launches += 1 if ns else 0
-        return launches
+        dsim.exchange()
+        return dsim.launches_per_exchange
 
     def barrier():
         torch.cuda.synchronize(device)
@@ -286,23 +254,15 @@ def run_ours(args):
     clk = clocks.stop()
     step_ms = ev0.elapsed_time(ev1)
     if dist is not None:
-        tt = torch.tensor([step_ms, kernel_ms], dtype=torch.float64, device=f"cuda:{device}")
+        tt = torch.tensor([step_ms, kernel_ms], dtype=torch.float64,
+                          device=f"cuda:{device}" if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms, kernel_ms = float(tt[0]), float(tt[1])
     ms_per_step = step_ms / args.steps
     value = cells * args.steps / (step_ms / 1e3)
 
     # ---- parity sanity: hash of the final state equals across GPU counts -------
-    if ws > 1:
-        hv = C.c_uint64()
-        _abi.check(L.nbbgpu_state_hash_owned(h, C.byref(hv)))
-        t = torch.tensor([hv.value & ((1 << 63) - 1), hv.value >> 63], dtype=torch.int64,
-                         device=f"cuda:{device}")
-        parts = [torch.zeros_like(t) for _ in range(ws)]
-        dist.all_gather(parts, t)
-        final_hash = sum(int(p[0]) + (int(p[1]) << 63) for p in parts) & (2**64 - 1)
-    else:
-        final_hash = sim.state_hash()
+    final_hash = dsim.state_hash() if dsim is not None else sim.state_hash()
 
     # ---- e2e through the public API with host buffers ----------------------------
     # upload the initial state from pinned host memory, K synchronous
@@ -323,7 +283,8 @@ def run_ours(args):
         barrier()
         e2e_s = time.perf_counter() - t0
         if dist is not None:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+            tt = torch.tensor([e2e_s], dtype=torch.float64,
+                              device=f"cuda:{device}" if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt[0])
         e2e = {"value": cells * args.steps / e2e_s, "unit": UNIT,
@@ -345,9 +306,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic: seed_random(42, 0.5) generated on the device (rng.hpp cell_alive)",
-        "config": {"workload": "sierpinski-triangle K(2^20,3,2) r=20 compact, B3/S23 Moore "
+        "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore "
                                "(BASELINE.json configs[3]; north-star target)",
-                   "level": LEVEL, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
+                   "level": args.level, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
                    "parallelism": f"partitioned x{n}" if n > 1 else "single GPU",
                    "l2": "state 6.97 GB >> 126 MB L2: inputs larger than L2, no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -364,7 +325,7 @@ def run_ours(args):
         line["roofline"]["ncu"] = {k: v for k, v in ncu.items() if k != "dram_bytes_per_launch"}
     if not args.no_cpu_baseline and n == 1:
         try:
-            line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(LEVEL, 2.0, 3, 1).items()
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(args.level, 2.0, 3, 1).items()
                                     if k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
@@ -383,6 +344,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--level", type=int, default=LEVEL, help="triangle level (default 20)")
+    ap.add_argument("--device", type=int, default=None, help="test knob: force the CUDA device")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="test knob: gloo lets several ranks share one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -74,6 +74,8 @@ def lib():
         L.nbbo_seed.restype = None
         L.nbbo_state_hash.argtypes = [P(_Mapper), C.c_int, C.c_void_p]
         L.nbbo_state_hash.restype = C.c_uint64
+        L.nbbo_state_hash_range.argtypes = [P(_Mapper), C.c_void_p, C.c_int64, C.c_int64]
+        L.nbbo_state_hash_range.restype = C.c_uint64
         L.nbbo_step_compact.argtypes = [P(_Mapper), C.c_uint16, C.c_uint16, C.c_int, C.c_void_p,
                                         C.c_void_p, C.c_int64, C.c_int64]
         L.nbbo_step_compact.restype = None
@@ -152,6 +154,9 @@ class Oracle:
 
     def state_hash(self) -> int:
         return int(lib().nbbo_state_hash(C.byref(self.m), self.mode, self.front.ctypes.data))
+
+    def state_hash_range(self, i0: int, i1: int) -> int:
+        return int(lib().nbbo_state_hash_range(C.byref(self.m), self.front.ctypes.data, i0, i1))
 
     def fnv(self) -> int:
         return fnv1a64(self.front)

@@ -176,6 +176,19 @@ uint64_t nbbo_state_hash(const nbbo_mapper* m, int mode, const uint8_t* f) {
     return hash;
 }
 
+/* state_hash restricted to linear-compact indices [i0, i1) (the partial sums of
+ * stencil.cpp:207-216 add up to the full hash: the sum is order independent). */
+uint64_t nbbo_state_hash_range(const nbbo_mapper* m, const uint8_t* f, int64_t i0, int64_t i1) {
+    uint64_t hash = 0;
+    for (int64_t i = i0; i < i1; ++i)
+        if (f[i]) {
+            int64_t x, y;
+            nbbo_to_embedded(m, i % m->w, i / m->w, &x, &y);
+            hash += nbbo_coord_mix(x, y);
+        }
+    return hash;
+}
+
 /* neighbor_offsets, proj/src/stencil.cpp:55-61 */
 static const int kOff[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1},
                                {1, 1}, {1, -1}, {-1, 1}, {-1, -1}};

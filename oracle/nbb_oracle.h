@@ -56,6 +56,9 @@ void nbbo_seed(const nbbo_mapper* m, int mode, uint64_t seed, double density, ui
 /* state_hash, proj/src/stencil.cpp:196-234. */
 uint64_t nbbo_state_hash(const nbbo_mapper* m, int mode, const uint8_t* f);
 
+/* state_hash over linear-compact indices [i0, i1) (partial sums add up). */
+uint64_t nbbo_state_hash_range(const nbbo_mapper* m, const uint8_t* f, int64_t i0, int64_t i1);
+
 /* step_compact_linear over compact indices [i0, i1), proj/src/stencil.cpp:334-368.
  * moore != 0 -> 8 Moore offsets, else 4 von Neumann (proj/src/stencil.cpp:55-61). */
 void nbbo_step_compact(const nbbo_mapper* m, uint16_t birth, uint16_t survive, int moore,

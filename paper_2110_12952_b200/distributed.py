@@ -1,0 +1,164 @@
+"""Multi-GPU partitioning with a per-step halo exchange (north-star item 4).
+
+One process per GPU.  Every rank keeps a full-size compact state, updates only
+its contiguous range of partition rows (tile rows of k^(q/2) compact rows, or
+compact rows when no tile level applies) and, after each step, exchanges the
+halo bytes: the source cells of the tile-halo links that cross a partition
+boundary (partition.inc).  The lists are computed on the host once and need no
+communication: what rank p needs from me is exactly plan_needs(rank=p, peer=me).
+
+The transport is torch.distributed point-to-point (NCCL over NVLink on the GPU
+box, gloo in the CPU tests) with grouped isend/irecv, so the same host logic is
+exercised by both.  The partial state hashes add up to the global hash
+(Simulation::state_hash is an order-independent wrapping sum, stencil.cpp:196-234).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List
+
+import numpy as np
+
+from . import _abi
+from .descriptor import FractalDescriptor
+
+
+def _needs(desc: FractalDescriptor, level: int, tile_level: int, rank: int, nranks: int,
+           peer: int) -> np.ndarray:
+    L = _abi.lib()
+    rep = _abi.replica_array(desc.replicas)
+    cnt = C.c_uint64()
+    _abi.check(L.nbbgpu_plan_needs(rep, desc.k, desc.s, level, tile_level, rank, nranks, peer,
+                                   None, C.byref(cnt)))
+    out = np.zeros(max(1, cnt.value), dtype=np.uint64)
+    _abi.check(L.nbbgpu_plan_needs(rep, desc.k, desc.s, level, tile_level, rank, nranks, peer,
+                                   out.ctypes.data, C.byref(cnt)))
+    return out[:cnt.value]
+
+
+def plan_tile_level(desc: FractalDescriptor, level: int) -> int:
+    q = C.c_int()
+    _abi.check(_abi.lib().nbbgpu_plan_tile_level(_abi.replica_array(desc.replicas), desc.k, desc.s,
+                                                 level, C.byref(q)))
+    return q.value
+
+
+@dataclass
+class PartitionPlan:
+    """Owned compact range and halo lists of one rank (host only, no GPU)."""
+    desc: FractalDescriptor
+    level: int
+    rank: int
+    nranks: int
+    tile_level: int = -1
+    lo: int = 0
+    hi: int = 0
+    recv: Dict[int, np.ndarray] = field(default_factory=dict)  # offsets I need from peer
+    send: Dict[int, np.ndarray] = field(default_factory=dict)  # offsets peer needs from me
+
+    def __post_init__(self):
+        L = _abi.lib()
+        rep = _abi.replica_array(self.desc.replicas)
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _abi.check(L.nbbgpu_plan_partition(rep, self.desc.k, self.desc.s, self.level, self.tile_level,
+                                           self.rank, self.nranks, C.byref(lo), C.byref(hi)))
+        self.lo, self.hi = lo.value, hi.value
+        for p in range(self.nranks):
+            if p == self.rank:
+                continue
+            self.recv[p] = _needs(self.desc, self.level, self.tile_level, self.rank, self.nranks, p)
+            self.send[p] = _needs(self.desc, self.level, self.tile_level, p, self.nranks, self.rank)
+
+    @property
+    def peers(self) -> List[int]:
+        return [p for p in sorted(self.recv) if self.recv[p].size or self.send[p].size]
+
+    def halo_bytes(self) -> int:
+        return int(sum(v.size for v in self.recv.values()))
+
+
+def exchange(plan: PartitionPlan, dist, pack: Callable[[int], "object"],
+             recv_buffer: Callable[[int, int], "object"], unpack: Callable[[int, "object"], None]):
+    """One halo exchange: pack(peer) -> tensor of plan.send[peer].size bytes,
+    recv_buffer(peer, n) -> tensor to receive into, unpack(peer, tensor)."""
+    ops, recvs = [], {}
+    for p in plan.peers:
+        if plan.send[p].size:
+            ops.append(dist.P2POp(dist.isend, pack(p), p))
+        if plan.recv[p].size:
+            recvs[p] = recv_buffer(p, int(plan.recv[p].size))
+            ops.append(dist.P2POp(dist.irecv, recvs[p], p))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for p, buf in recvs.items():
+        unpack(p, buf)
+
+
+def wrap_u64_sum(values) -> int:
+    return int(sum(int(v) & (2**64 - 1) for v in values)) & (2**64 - 1)
+
+
+class DistributedSimulation:
+    """A GPU Simulation that owns one partition of the compact array and exchanges
+    halos with its peers over torch.distributed (NCCL) after every step."""
+
+    def __init__(self, sim, dist, rank: int, nranks: int, host_transport: bool = False):
+        """host_transport=True stages the halo through host tensors (gloo: used to
+        exercise this path with several ranks on a single test GPU)."""
+        import torch
+        self.sim, self.dist, self.rank, self.nranks = sim, dist, rank, nranks
+        self.host = host_transport
+        h = sim.handle()
+        L = _abi.lib()
+        _abi.check(L.nbbgpu_partition(h, rank, nranks))
+        self.plan = PartitionPlan(sim.desc, sim.level(), rank, nranks)
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
+        assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"
+        dev = torch.device("cuda", sim.options.device)
+        self._send_bufs, self._recv_bufs = {}, {}
+        for p in self.plan.peers:
+            s = self.plan.send[p]
+            _abi.check(L.nbbgpu_halo_set_sends(h, p, s.ctypes.data if s.size else None, s.size))
+            self._send_bufs[p] = torch.empty(max(1, s.size), dtype=torch.uint8, device=dev)
+            self._recv_bufs[p] = torch.empty(max(1, self.plan.recv[p].size), dtype=torch.uint8,
+                                             device=dev)
+        self.launches_per_exchange = sum(int(self.plan.send[p].size > 0) + int(self.plan.recv[p].size > 0)
+                                         for p in self.plan.peers)
+
+    def exchange(self) -> None:
+        import torch
+        L, h = _abi.lib(), self.sim.handle()
+
+        def pack(p):
+            n = int(self.plan.send[p].size)
+            _abi.check(L.nbbgpu_halo_pack(h, p, C.c_void_p(self._send_bufs[p].data_ptr())))
+            return self._send_bufs[p][:n].cpu() if self.host else self._send_bufs[p][:n]
+
+        def recv_buffer(p, n):
+            return torch.empty(n, dtype=torch.uint8) if self.host else self._recv_bufs[p][:n]
+
+        def unpack(p, buf):
+            if self.host:
+                self._recv_bufs[p][:buf.numel()].copy_(buf)
+            torch.cuda.current_stream().synchronize()
+            _abi.check(L.nbbgpu_halo_unpack(h, p, C.c_void_p(self._recv_bufs[p].data_ptr())))
+
+        exchange(self.plan, self.dist, pack, recv_buffer, unpack)
+
+    def step(self, rule, nsteps: int = 1) -> None:
+        for _ in range(nsteps):
+            self.sim.step(rule)
+            self.exchange()
+
+    def state_hash(self) -> int:
+        import torch
+        v = C.c_uint64()
+        _abi.check(_abi.lib().nbbgpu_state_hash_owned(self.sim.handle(), C.byref(v)))
+        t = torch.tensor([v.value & 0xFFFFFFFF, v.value >> 32], dtype=torch.int64,
+                         device="cpu" if self.host else torch.device("cuda", self.sim.options.device))
+        parts = [torch.zeros_like(t) for _ in range(self.nranks)]
+        self.dist.all_gather(parts, t)
+        return wrap_u64_sum(int(q[0]) | (int(q[1]) << 32) for q in parts)
