@@ -150,6 +150,14 @@ int nbbgpu_halo_pack(nbbgpu_t h, int peer, void* dev_dst);
 int nbbgpu_halo_unpack(nbbgpu_t h, int peer, const void* dev_src);
 /* state_hash over the owned range only (sum over ranks = global hash). */
 int nbbgpu_state_hash_owned(nbbgpu_t h, uint64_t* out);
+/* In-library NCCL transport: rank 0 creates an ncclUniqueId (128 bytes), the
+ * caller broadcasts it (e.g. torch.distributed), every rank attaches it after
+ * nbbgpu_partition.  From then on nbbgpu_step enqueues, after each step kernel,
+ * the halo pack kernel, grouped ncclSend/ncclRecv over NVLink and the unpack
+ * kernel on the handle's stream (no host synchronisation between steps). */
+int nbbgpu_nccl_unique_id(uint8_t* out, int bytes);
+int nbbgpu_comm_init(nbbgpu_t h, const uint8_t* unique_id, int bytes);
+
 /* Raw device pointer of the front buffer (for peer-to-peer transports). */
 int nbbgpu_front_device_ptr(nbbgpu_t h, void** out);
 

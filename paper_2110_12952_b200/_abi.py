@@ -49,6 +49,8 @@ SIGNATURES = {
     "nbbgpu_halo_unpack": (C.c_int, [_H, C.c_int, C.c_void_p]),
     "nbbgpu_state_hash_owned": (C.c_int, [_H, _P(C.c_uint64)]),
     "nbbgpu_front_device_ptr": (C.c_int, [_H, _P(C.c_void_p)]),
+    "nbbgpu_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int]),
+    "nbbgpu_comm_init": (C.c_int, [_H, C.c_void_p, C.c_int]),
     "nbbgpu_plan_tile_level": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, _P(C.c_int)]),
     "nbbgpu_plan_partition": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         C.c_int, _P(C.c_uint64), _P(C.c_uint64)]),

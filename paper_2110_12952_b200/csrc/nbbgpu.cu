@@ -4,6 +4,8 @@
 // the CPU, done here with device buffers and the kernels of naive.cuh, tiled.cuh
 // and maps.cuh.  No CPU fallback exists: every state transition runs on the GPU.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -332,6 +334,13 @@ struct nbbgpu_sim {
     std::vector<uint64_t> n_sends;
     std::vector<uint64_t*> d_recvs;             // per peer: offsets I receive from peer
     std::vector<uint64_t> n_recvs;
+    // in-library NCCL transport (nbbgpu_comm_init)
+    ncclComm_t comm = nullptr;
+    uint64_t* d_send_all = nullptr;             // concatenated per-peer send offsets
+    uint64_t* d_recv_all = nullptr;
+    uint8_t* d_sendbuf = nullptr;
+    uint8_t* d_recvbuf = nullptr;
+    uint64_t n_send_all = 0, n_recv_all = 0;
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -513,6 +522,9 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     else launch_tiled_w<false>(h, P.wq, p, src, dst);
 }
 
+void free_comm(nbbgpu_t h);           // partition.inc
+void exchange_on_stream(nbbgpu_t h);  // partition.inc
+
 void free_all(nbbgpu_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
@@ -529,6 +541,11 @@ void free_all(nbbgpu_t h) {
     }
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
+    if (h->d_send_all) cudaFree(h->d_send_all);
+    if (h->d_recv_all) cudaFree(h->d_recv_all);
+    if (h->d_sendbuf) cudaFree(h->d_sendbuf);
+    if (h->d_recvbuf) cudaFree(h->d_recvbuf);
+    free_comm(h);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -736,6 +753,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
         launch_step(h, birth, survive, moore);
         h->cur ^= 1;
         ++h->iteration;
+        if (h->comm) exchange_on_stream(h);  // halo bytes of the new front, on-stream
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));

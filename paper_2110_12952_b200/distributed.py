@@ -102,14 +102,22 @@ def wrap_u64_sum(values) -> int:
 
 class DistributedSimulation:
     """A GPU Simulation that owns one partition of the compact array and exchanges
-    halos with its peers over torch.distributed (NCCL) after every step."""
+    halos with its peers after every step.
 
-    def __init__(self, sim, dist, rank: int, nranks: int, host_transport: bool = False):
-        """host_transport=True stages the halo through host tensors (gloo: used to
-        exercise this path with several ranks on a single test GPU)."""
+    transport="nccl" (production): the library's own NCCL communicator (unique id
+      broadcast over torch.distributed); pack kernel -> grouped ncclSend/ncclRecv
+      -> unpack kernel are enqueued on the engine stream after each step kernel,
+      so K steps run without any host synchronisation.
+    transport="torch": torch.distributed point-to-point on device tensors
+      (host_staging=True: through host tensors, so gloo can drive several ranks
+      that share one test GPU)."""
+
+    def __init__(self, sim, dist, rank: int, nranks: int, transport: str = "nccl",
+                 host_staging: bool = False):
         import torch
         self.sim, self.dist, self.rank, self.nranks = sim, dist, rank, nranks
-        self.host = host_transport
+        self.transport = transport
+        self.host = host_staging
         h = sim.handle()
         L = _abi.lib()
         _abi.check(L.nbbgpu_partition(h, rank, nranks))
@@ -117,6 +125,17 @@ class DistributedSimulation:
         lo, hi = C.c_uint64(), C.c_uint64()
         _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
         assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"
+        self.launches_per_exchange = (int(any(self.plan.send[p].size for p in self.plan.peers)) +
+                                      int(any(self.plan.recv[p].size for p in self.plan.peers)))
+        if transport == "nccl":
+            uid = (C.c_uint8 * 128)()
+            if rank == 0:
+                _abi.check(L.nbbgpu_nccl_unique_id(uid, 128))
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            _abi.check(L.nbbgpu_comm_init(h, uid, 128))
+            return
         dev = torch.device("cuda", sim.options.device)
         self._send_bufs, self._recv_bufs = {}, {}
         for p in self.plan.peers:
@@ -129,7 +148,10 @@ class DistributedSimulation:
                                          for p in self.plan.peers)
 
     def exchange(self) -> None:
+        """torch transport only (the nccl transport exchanges inside every step)."""
         import torch
+        if self.transport == "nccl":
+            return
         L, h = _abi.lib(), self.sim.handle()
 
         def pack(p):
@@ -149,16 +171,30 @@ class DistributedSimulation:
         exchange(self.plan, self.dist, pack, recv_buffer, unpack)
 
     def step(self, rule, nsteps: int = 1) -> None:
+        if self.transport == "nccl":
+            self.sim.step(rule, nsteps)
+            return
         for _ in range(nsteps):
             self.sim.step(rule)
             self.exchange()
+
+    def step_timed(self, rule, nsteps: int) -> float:
+        """Device ms of nsteps steps (step kernels + halo exchanges, one event pair)."""
+        if self.transport == "nccl":
+            return self.sim.step_timed(rule, nsteps)
+        ms = 0.0
+        for _ in range(nsteps):
+            ms += self.sim.step_timed(rule, 1)
+            self.exchange()
+        return ms
 
     def state_hash(self) -> int:
         import torch
         v = C.c_uint64()
         _abi.check(_abi.lib().nbbgpu_state_hash_owned(self.sim.handle(), C.byref(v)))
+        on_host = self.host or self.dist.get_backend() == "gloo"
         t = torch.tensor([v.value & 0xFFFFFFFF, v.value >> 32], dtype=torch.int64,
-                         device="cpu" if self.host else torch.device("cuda", self.sim.options.device))
+                         device="cpu" if on_host else torch.device("cuda", self.sim.options.device))
         parts = [torch.zeros_like(t) for _ in range(self.nranks)]
         self.dist.all_gather(parts, t)
         return wrap_u64_sum(int(q[0]) | (int(q[1]) << 32) for q in parts)
