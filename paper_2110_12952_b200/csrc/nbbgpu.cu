@@ -19,6 +19,7 @@
 #include "../../include/nbbgpu.h"
 #include "common.cuh"
 #include "maps.cuh"
+#include "bb.cuh"
 #include "naive.cuh"
 #include "tiled.cuh"
 
@@ -472,6 +473,40 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     uint8_t* dst = h->back();
     if (h->mode == NBBGPU_MODE_BB) {
         const uint64_t n = (uint64_t)h->hf.side * h->hf.side;
+        const int s = h->hf.s;
+        if ((s == 2 || s == 4) && h->hf.side % 16 == 0 && h->kernel != NBBGPU_KERNEL_NAIVE) {
+            // vectorised BB baseline (bb.cuh)
+            BBParams p{};
+            p.f = h->frac;
+            p.n = (uint32_t)h->hf.side;
+            p.mlow = s == 2 ? 4 : 2;
+            p.triangle = (h->hf.k == 3 && s == 2 && h->hf.gx[0] == 0 && h->hf.gy[0] == 0 &&
+                          h->hf.gx[1] == 1 && h->hf.gy[1] == 0 && h->hf.gx[2] == 0 && h->hf.gy[2] == 1);
+            for (int yl = 0; yl < 16; ++yl) {
+                uint32_t m = 0;
+                for (int i = 0; i < 16; ++i) {
+                    bool ok = true;
+                    int xx = i, yy = yl;
+                    for (int mu = 0; mu < p.mlow && mu < h->hf.r; ++mu) {
+                        if (h->hf.id[(yy % s) * s + (xx % s)] < 0) ok = false;
+                        xx /= s;
+                        yy /= s;
+                    }
+                    if (ok) m |= 1u << i;
+                }
+                p.low[yl] = (uint16_t)m;
+            }
+            p.birth = birth;
+            p.survive = survive;
+            p.moore = moore;
+            const uint64_t vecs = n / 16;
+            const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((vecs + 255) / 256, 148ull * 16));
+            if ((birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore)
+                step_bb_vec_kernel<true><<<blocks, 256, 0, h->stream>>>(p, src, dst);
+            else
+                step_bb_vec_kernel<false><<<blocks, 256, 0, h->stream>>>(p, src, dst);
+            return;
+        }
 #define NBB_CALL(K, S, ...) step_bb_naive_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, src, dst, birth, survive, deg)
         NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL

@@ -241,3 +241,24 @@ def test_run_simulation_determinism():
     assert zero.state_hash == o.state_hash()
     with pytest.raises(OutOfDomain):
         run_simulation(T, 3, Backend.GpuCompact, conway_rule(), -1, 0, 0.5)
+
+
+def test_bb_vectorised_kernel_vs_oracle():
+    # the vectorised BB baseline (s = 2, 4) against the oracle's step_bounding_box,
+    # including B0 rules (holes must stay 0) and von Neumann neighbourhoods
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    rng = np.random.default_rng(99)
+    for desc, r in [(T, 5), (T, 7), (SOLID, 6), (Y, 3)]:
+        for trial in range(4):
+            rule = conway_rule() if trial == 0 else StencilRule(
+                int(rng.integers(0, 512)) | (1 if trial == 3 else 0), int(rng.integers(0, 512)),
+                Neighborhood.Moore if trial != 2 else Neighborhood.VonNeumann)
+            o = oracle.Oracle(desc.replicas, desc.k, desc.s, r, mode="bb")
+            o.seed(trial + 3, 0.5)
+            sim = Simulation(desc, r, Backend.GpuBoundingBox)
+            sim.seed_random(trial + 3, 0.5)
+            for i in range(5):
+                o.step(rule.birth, rule.survive, rule.moore)
+                sim.step(rule)
+                assert np.array_equal(sim.front().data, o.front), (desc.name, r, rule.to_string(), i)
