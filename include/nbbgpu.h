@@ -125,7 +125,8 @@ int nbbgpu_stream(nbbgpu_t h, void** stream);
  *   nu:     in = count (x, y) pairs -> out = count (cx, cy) pairs, (-1, -1) for a
  *           hole or an out-of-box coordinate.
  * variant = NBBGPU_MAP_DIGIT or NBBGPU_MAP_MMA.  device_ms (optional) receives
- * the kernel time. */
+ * the kernel time.  The engine runs on its own stream: device buffers must be
+ * complete (caller-side synchronisation) before the call. */
 int nbbgpu_lambda_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,
                         float* device_ms);
 int nbbgpu_nu_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,

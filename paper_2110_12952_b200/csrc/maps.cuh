@@ -216,3 +216,110 @@ __global__ void lambda_mma_kernel(Frac f, MmaTables T, const int2* __restrict__ 
 }
 
 }  // namespace nbbgpu
+
+namespace nbbgpu {
+
+// The paper's per-cell compact step (lambda of the own cell, nu of its 8
+// neighbours, stencil.cpp:354-367) with the 8 nu maps evaluated on
+// the tensor cores: a warp stages its 32 cells x 8 neighbour coordinates in smem,
+// 16 mma.sync.m16n8k32 (u8 x u8 -> s32, the nu_mma_kernel formulation) turn them
+// into compact coordinates, and every lane gathers its own 8 results.
+// Used for the "lambda/nu tensor-core vs CUDA-core maps" comparison (config 2).
+template <int S>
+__global__ void __launch_bounds__(128) step_compact_naive_mma_kernel(Frac f, MmaTables T,
+                                                                    const uint8_t* __restrict__ src,
+                                                                    uint8_t* __restrict__ dst,
+                                                                    uint64_t i0, uint64_t i1,
+                                                                    uint32_t birth, uint32_t survive,
+                                                                    int deg) {
+    __shared__ int2 q[4][256];    // per warp: (x, y) of neighbour queries, (-1,-1) = none
+    __shared__ int2 res[4][256];  // per warp: (cx, cy) results, (-1, -1) = absent
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    const uint32_t s = S ? S : f.s;
+    uint32_t b[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int kk = 16 * h + 4 * t + i;
+            uint32_t e = 0;
+            if (kk < f.r && ((g < 4) == ((kk & 1) == 0))) e = limb(T.tau[kk], g & 3);
+            v |= e << (8 * i);
+        }
+        b[h] = v;
+    }
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = i0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; base < i1;
+         base += nwarps * 32) {
+        const uint64_t i = base + lane;
+        const bool valid = i < i1;
+        uint32_t ex = 0, ey = 0;
+        if (valid) lambda_map<0, S>(f, (uint32_t)(i % f.w), (uint32_t)(i / f.w), ex, ey);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int nx = (int)ex + kOffX[j], ny = (int)ey + kOffY[j];
+            const bool in = valid && j < deg && nx >= 0 && ny >= 0 && nx < (int)f.side && ny < (int)f.side;
+            q[wid][lane * 8 + j] = in ? make_int2(nx, ny) : make_int2(-1, -1);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int tile = 0; tile < 16; ++tile) {
+            uint32_t a[4];
+            bool bad[2];
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int2 e = q[wid][tile * 16 + g + 8 * rr];
+                const bool oob = e.x < 0;
+                bool hole = false;
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int mu = 16 * h + 4 * t + ii;
+                        uint32_t id = 0;
+                        if (mu < f.r && !oob) {
+                            const uint32_t sc = T.spow[mu];
+                            const uint32_t gx = ((uint32_t)e.x / sc) % s, gy = ((uint32_t)e.y / sc) % s;
+                            const int r = f.id_of_subbox[gy * s + gx];
+                            if (r < 0) hole = true; else id = (uint32_t)r;
+                        }
+                        v |= id << (8 * ii);
+                    }
+                    if (h == 0) lo = v; else hi = v;
+                }
+                const uint32_t hb = __ballot_sync(0xffffffffu, hole || oob);
+                bad[rr] = ((hb >> (lane & ~3)) & 0xFu) != 0;
+                a[rr] = lo;
+                a[2 + rr] = hi;
+            }
+            int d[4] = {0, 0, 0, 0};
+            mma_u8_16832(d, a, b);
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const uint32_t c0 = (uint32_t)d[2 * rr], c1 = (uint32_t)d[2 * rr + 1];
+                uint32_t part = (c0 << (8 * ((2 * t) & 3))) + (c1 << (8 * ((2 * t + 1) & 3)));
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, part, 2);
+                if (t == 0)
+                    res[wid][tile * 16 + g + 8 * rr] = bad[rr] ? make_int2(-1, -1)
+                                                               : make_int2((int)part, (int)other);
+            }
+        }
+        __syncwarp();
+        if (valid) {
+            uint32_t count = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int2 c = res[wid][lane * 8 + j];
+                if (c.x >= 0) count += src[(uint64_t)c.y * f.w + c.x];
+            }
+            dst[i] = apply_rule(birth, survive, src[i], count);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace nbbgpu

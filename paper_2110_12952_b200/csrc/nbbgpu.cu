@@ -411,10 +411,16 @@ void ensure_plan(nbbgpu_t h, int moore) {
     h->plan_built[moore] = true;
 }
 
+// Below this many compact cells the one-thread-per-cell kernel wins: the tiled
+// kernel's per-group chain (~16 us) dominates tiny levels (measured on B200:
+// T r=10 naive 12 us vs tiled 17 us; r=11 equal; r=12 naive 43 us vs tiled 19 us).
+constexpr uint64_t kTiledMinCells = 1ull << 17;
+
 int resolve_kernel(nbbgpu_t h) {
     if (h->mode == NBBGPU_MODE_BB) return NBBGPU_KERNEL_NAIVE;
     if (h->kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
-    if (h->q > 0) return NBBGPU_KERNEL_TILED;
+    if (h->q > 0 && (h->kernel == NBBGPU_KERNEL_TILED || h->cells >= kTiledMinCells))
+        return NBBGPU_KERNEL_TILED;
     if (h->kernel == NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
     return NBBGPU_KERNEL_NAIVE;
 }
@@ -516,6 +522,13 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     if (kern == NBBGPU_KERNEL_NAIVE) {
         uint64_t lo, hi;
         owned_range(h, lo, hi);
+        if (h->map_variant == NBBGPU_MAP_MMA && h->hf.r <= 32) {
+            const int blocks = grid_for((hi - lo + 31) / 32 * 32, 128);
+#define NBB_CALL(K, S, ...) step_compact_naive_mma_kernel<S><<<blocks, 128, 0, h->stream>>>(h->frac, h->mt, src, dst, lo, hi, birth, survive, deg)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+            return;
+        }
 #define NBB_CALL(K, S, ...) step_compact_naive_kernel<K, S><<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(h->frac, src, dst, lo, hi, birth, survive, deg)
         NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL
@@ -608,7 +621,7 @@ bool is_device_ptr(const void* p) {
         cudaGetLastError();
         return false;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.devicePointer == p;
 }
 
 // storage index of an embedded coordinate (Grid::storage_index, grid.cpp:38-66)
@@ -629,7 +642,9 @@ void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, i
     const bool din = is_device_ptr(in), dout = is_device_ptr(out);
     int2* dI = nullptr;
     int2* dO = nullptr;
-    if (din) dI = (int2*)in; else { CK(cudaMalloc(&dI, bytes)); CK(cudaMemcpyAsync(dI, in, bytes, cudaMemcpyHostToDevice, h->stream)); }
+    // pointers the runtime does not classify as device memory (host memory, or
+    // allocator pools it does not report) are staged with UVA-aware copies
+    if (din) dI = (int2*)in; else { CK(cudaMalloc(&dI, bytes)); CK(cudaMemcpyAsync(dI, in, bytes, cudaMemcpyDefault, h->stream)); }
     if (dout) dO = (int2*)out; else CK(cudaMalloc(&dO, bytes));
     CK(cudaEventRecord(h->ev0, h->stream));
     const uint64_t n = (uint64_t)count;
@@ -657,7 +672,7 @@ void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, i
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));
-    if (!dout) CK(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (!dout) CK(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDefault, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
     if (!din) cudaFree(dI);

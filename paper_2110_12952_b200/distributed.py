@@ -121,7 +121,8 @@ class DistributedSimulation:
         h = sim.handle()
         L = _abi.lib()
         _abi.check(L.nbbgpu_partition(h, rank, nranks))
-        self.plan = PartitionPlan(sim.desc, sim.level(), rank, nranks)
+        _, q = sim.active_kernel()  # partition rows are tile rows of the kernel in use
+        self.plan = PartitionPlan(sim.desc, sim.level(), rank, nranks, tile_level=q)
         lo, hi = C.c_uint64(), C.c_uint64()
         _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
         assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"

@@ -30,8 +30,18 @@ def fnv(buf):
     return f"{oracle.fnv1a64(buf):016x}"
 
 
+def tiled_or_auto(desc, level, kernel):
+    # "tiled" forces the tile-parallel kernel wherever a tile level exists
+    from paper_2110_12952_b200.distributed import plan_tile_level
+    if kernel == "tiled" and plan_tile_level(desc, level) == 0:
+        return "auto"
+    return kernel
+
+
 def run_trace(t, backend, kernel="auto"):
     d = desc_from_trace(t)
+    if backend == Backend.GpuCompact:
+        kernel = tiled_or_auto(d, t["level"], kernel)
     sim = Simulation(d, t["level"], backend, SimOptions(kernel=kernel, memory_cap=1 << 40))
     sim.seed_random(t["seed"], t["density"])
     rule = rule_of(t)
@@ -51,7 +61,7 @@ def run_trace(t, backend, kernel="auto"):
     sim.close()
 
 
-@pytest.mark.parametrize("kernel", ["auto", "naive"])
+@pytest.mark.parametrize("kernel", ["tiled", "naive", "auto"])
 def test_golden_traces_compact(golden, kernel):
     for t in golden["traces"]:
         run_trace(t, Backend.GpuCompact, kernel)
@@ -63,12 +73,12 @@ def test_golden_traces_bb(golden):
             run_trace(t, Backend.GpuBoundingBox)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "naive"])
+@pytest.mark.parametrize("kernel", ["tiled", "naive"])
 def test_golden_random_trials(golden, kernel):
     # acceptance.cpp:202-219 (C5, 50 trials) and test_stencil.cpp:155-182
     for t in golden["random_c5"] + golden["random_xbackend"]:
         run_trace(t, Backend.GpuCompact, kernel)
-        if kernel == "auto":
+        if kernel == "tiled":
             run_trace(t, Backend.GpuBoundingBox)
 
 
@@ -79,10 +89,11 @@ def test_tiled_kernel_is_used_at_scale():
     assert sim2.active_kernel() == ("naive", 0)
 
 
-def _lockstep_vs_oracle(desc, r, rule, seed, density, steps, kernel="auto"):
+def _lockstep_vs_oracle(desc, r, rule, seed, density, steps, kernel="auto", map_variant="digit"):
     o = oracle.Oracle(desc.replicas, desc.k, desc.s, r)
     o.seed(seed, density)
-    sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 40))
+    sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 40,
+                                                             map_variant=map_variant))
     sim.seed_random(seed, density)
     assert np.array_equal(sim.front().data, o.front)
     for i in range(steps):
@@ -111,7 +122,7 @@ def test_tiled_randomized_lockstep():
             if trial == 0:
                 rule = conway_rule()
             _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)),
-                                float(rng.uniform(0.1, 0.9)), 4)
+                                float(rng.uniform(0.1, 0.9)), 4, kernel=tiled_or_auto(desc, r, "tiled"))
 
 
 def test_large_levels_hash(golden, golden_long):
@@ -159,8 +170,8 @@ def test_trivial_steps():
 def test_blinker_on_solid_grid():
     # test_stencil.cpp:69-95
     for backend in (Backend.GpuBoundingBox, Backend.GpuCompact):
-        for kernel in ("auto", "naive"):
-            if backend == Backend.GpuBoundingBox and kernel != "auto":
+        for kernel in ("tiled", "naive"):
+            if backend == Backend.GpuBoundingBox and kernel != "naive":
                 continue
             sim = Simulation(SOLID, 2, backend, SimOptions(kernel=kernel))
             sim.seed_random(0, 0.0)
@@ -262,3 +273,16 @@ def test_bb_vectorised_kernel_vs_oracle():
                 o.step(rule.birth, rule.survive, rule.moore)
                 sim.step(rule)
                 assert np.array_equal(sim.front().data, o.front), (desc.name, r, rule.to_string(), i)
+
+
+def test_naive_kernel_with_tensor_core_maps():
+    # the paper's per-cell kernel with its 8 nu maps on the tensor cores (config 2's
+    # "lambda/nu tensor-core vs CUDA-core maps")
+    rng = np.random.default_rng(7)
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    for desc, r in [(T, 3), (T, 8), (T, 11), (CARPET, 3), (VICSEK, 4), (H, 3), (SOLID, 5)]:
+        for trial in range(2):
+            rule = conway_rule() if trial == 0 else StencilRule(
+                int(rng.integers(0, 512)), int(rng.integers(0, 512)), Neighborhood.VonNeumann)
+            _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)), 0.5, 3,
+                                kernel="naive", map_variant="mma")

@@ -25,7 +25,7 @@ def _run(desc, level, nranks, rule, steps, kernel="auto"):
         sim = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 40))
         sim.seed_random(5, 0.5)
         _abi.check(L.nbbgpu_partition(sim.handle(), r, nranks))
-        plan = PartitionPlan(desc, level, r, nranks, tile_level=-1 if kernel != "naive" else 0)
+        plan = PartitionPlan(desc, level, r, nranks, tile_level=-1 if kernel == "tiled" else 0)
         for p in plan.peers:
             s = plan.send[p]
             _abi.check(L.nbbgpu_halo_set_sends(sim.handle(), p, s.ctypes.data if s.size else None, s.size))
@@ -61,15 +61,15 @@ def _run(desc, level, nranks, rule, steps, kernel="auto"):
 @pytest.mark.parametrize("nranks", [2, 3, 8])
 def test_partitioned_triangle(nranks):
     T = builtin_descriptor("sierpinski-triangle")
-    _run(T, 12, nranks, StencilRule(8, 12, Neighborhood.Moore), 5)
-    _run(T, 9, nranks, StencilRule(0x1C8, 0x6, Neighborhood.VonNeumann), 4)
+    _run(T, 12, nranks, StencilRule(8, 12, Neighborhood.Moore), 5, kernel="tiled")
+    _run(T, 9, nranks, StencilRule(0x1C8, 0x6, Neighborhood.VonNeumann), 4, kernel="tiled")
 
 
 def test_partitioned_other_fractals():
     C8 = builtin_descriptor("sierpinski-carpet")
     V = builtin_descriptor("vicsek")
-    _run(C8, 5, 3, StencilRule(8, 12, Neighborhood.Moore), 4)
-    _run(V, 6, 2, StencilRule(0x6, 0x9, Neighborhood.Moore), 4)
+    _run(C8, 5, 3, StencilRule(8, 12, Neighborhood.Moore), 4, kernel="tiled")
+    _run(V, 6, 2, StencilRule(0x6, 0x9, Neighborhood.Moore), 4, kernel="tiled")
 
 
 def test_partitioned_naive_kernel():
