@@ -48,11 +48,16 @@ typedef enum {
  * (proj/src/stencil.cpp:108-112). */
 enum { NBBGPU_MODE_COMPACT = 0, NBBGPU_MODE_BB = 1 };
 
-/* Step kernels (nbbgpu_set_kernel).  AUTO picks TILED when the level admits a
- * tile level, else NAIVE.  NAIVE is the paper's per-cell kernel: lambda of the
- * own cell plus nu of each neighbour (proj/src/stencil.cpp:354-367); its map
- * variant is chosen by nbbgpu_set_map_variant. */
-enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2 };
+/* Step kernels (nbbgpu_set_kernel).  AUTO picks PACKED when the level admits a
+ * packed tile level (even q >= 2), else TILED / NAIVE.  NAIVE is the paper's
+ * per-cell kernel: lambda of the own cell plus nu of each neighbour
+ * (proj/src/stencil.cpp:354-367); its map variant is chosen by
+ * nbbgpu_set_map_variant.  NAIVE and TILED keep the state in the reference's byte
+ * layout on the device; PACKED keeps it bit-sliced (1 bit per cell, groups of 32
+ * level-q tiles, csrc/packed.cuh) and converts to / from the reference bytes on
+ * download / upload.  Switching between the two families converts the state on
+ * the device.  Results are identical for every kernel. */
+enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2, NBBGPU_KERNEL_PACKED = 3 };
 
 /* lambda / nu map variants: CUDA-core digit loop, or the paper's matrix form on
  * the tensor cores (exact integer MMA, u8 x u8 -> s32). */
@@ -133,6 +138,11 @@ int nbbgpu_nu_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, in
                     float* device_ms);
 
 /* ---- multi-GPU partitioning (one process per GPU) ---------------------------
+ * Byte layouts (NAIVE / TILED): the unit is a tile row, halo elements are state
+ * bytes at compact byte offsets.  PACKED: the unit is a group of 32 tiles (rank r
+ * owns groups [NG r/n, NG (r+1)/n)), owned_range is in packed 32-bit words, and
+ * halo elements are 32-bit boundary-plane words (element index g * nSrc + m);
+ * nbbgpu_halo_elem_bytes tells which (1 or 4).
  * A handle may own a contiguous range of tile rows [row0, row1) of the compact
  * array (tile rows of h_q compact rows each; the whole array when nranks == 1).
  * It keeps a full-size copy of the state, updates only its rows, and exchanges
@@ -159,7 +169,12 @@ int nbbgpu_state_hash_owned(nbbgpu_t h, uint64_t* out);
 int nbbgpu_nccl_unique_id(uint8_t* out, int bytes);
 int nbbgpu_comm_init(nbbgpu_t h, const uint8_t* unique_id, int bytes);
 
-/* Raw device pointer of the front buffer (for peer-to-peer transports). */
+/* Bytes per halo element of the handle's partition (1 = state byte, 4 = packed
+ * boundary-plane word). */
+int nbbgpu_halo_elem_bytes(nbbgpu_t h, int* out);
+
+/* Raw device pointer of the front buffer (reference bytes, or packed words for
+ * the PACKED kernel; for peer-to-peer transports). */
 int nbbgpu_front_device_ptr(nbbgpu_t h, void** out);
 
 /* ---- host-only planning (no GPU needed; same geometry as above) ------------
@@ -173,6 +188,20 @@ int nbbgpu_plan_needs(const int32_t* replicas_xy, int k, int s, int level, int t
 /* info = [q, wq, C, nH, L, Wc, Hc, dmask] of the tile plan. */
 int nbbgpu_plan_tiles(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
                       int moore, int32_t* info);
+
+/* ---- host-only planning of the packed layout --------------------------------
+ * tile_level < 0 selects the level nbbgpu_create would choose (-1 = none).
+ * info = [q, wq, C, Cp, nH, nSrc, T, NG, Wc, Hc, nD, wide]. */
+int nbbgpu_plan_packed_level(const int32_t* replicas_xy, int k, int s, int level, int* tile_level);
+int nbbgpu_plan_packed(const int32_t* replicas_xy, int k, int s, int level, int tile_level, int64_t* info);
+int nbbgpu_plan_packed_partition(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                                 int rank, int nranks, int64_t* group0, int64_t* group1);
+/* Boundary-plane elements rank needs from peer (sorted, unique; elems == NULL -> count). */
+int nbbgpu_plan_packed_needs(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                             int rank, int nranks, int peer, uint64_t* elems, uint64_t* count);
+/* Compact byte offsets of the cells a boundary-plane element holds (<= 32 per element). */
+int nbbgpu_plan_packed_elem_cells(const int32_t* replicas_xy, int k, int s, int level, int tile_level,
+                                  const uint64_t* elems, uint64_t n, uint64_t* out, uint64_t* count);
 
 #ifdef __cplusplus
 }

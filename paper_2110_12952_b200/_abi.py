@@ -58,6 +58,15 @@ SIGNATURES = {
                                     C.c_int, C.c_int, C.c_void_p, _P(C.c_uint64)]),
     "nbbgpu_plan_tiles": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     _P(C.c_int32)]),
+    "nbbgpu_halo_elem_bytes": (C.c_int, [_H, _P(C.c_int)]),
+    "nbbgpu_plan_packed_level": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, _P(C.c_int)]),
+    "nbbgpu_plan_packed": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, _P(C.c_int64)]),
+    "nbbgpu_plan_packed_partition": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int,
+                                               C.c_int, C.c_int, _P(C.c_int64), _P(C.c_int64)]),
+    "nbbgpu_plan_packed_needs": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_int, C.c_void_p, _P(C.c_uint64)]),
+    "nbbgpu_plan_packed_elem_cells": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int,
+                                                C.c_void_p, C.c_uint64, C.c_void_p, _P(C.c_uint64)]),
 }
 
 _lib = None

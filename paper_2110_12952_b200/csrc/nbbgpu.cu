@@ -22,6 +22,7 @@
 #include "bb.cuh"
 #include "naive.cuh"
 #include "tiled.cuh"
+#include "packed.cuh"
 
 using namespace nbbgpu;
 
@@ -293,6 +294,105 @@ int choose_tile_level(const HostFrac& F) {
     return best;
 }
 
+
+// ---------------------------------------------------------------------------
+// Packed plan (packed.cuh): one halo-slot set (Moore; von Neumann's is a subset),
+// boundary sources, [C][8] stage byte offsets for both neighbourhoods.
+// ---------------------------------------------------------------------------
+constexpr int kPackedMaxCells = 24576;  // two smem stages of <= 96 KB
+
+struct PackedPlan {
+    int q = -1, wq = 1, C = 1, Cp = 4, L = 0;
+    int64_t Wc = 0, Hc = 0, T = 0, NG = 0, sq = 1;
+    int nH = 0, nD = 0, nSrc = 0;
+    int8_t dlist[8] = {0};
+    std::vector<uint8_t> slotD;     // per slot: direction D = (dy+1)*3 + dx+1
+    std::vector<uint32_t> slot;     // per slot: (direction slot << 16) | boundary source m
+    std::vector<uint32_t> srcidx;   // per boundary source: local cell
+    std::vector<uint32_t> loc;      // per local cell: (yl << 16) | xl  (level-q lambda)
+    std::vector<uint32_t> nbr[2];   // [moore] C x 8 stage byte offsets
+    bool wide = false;              // offsets do not fit 16 bits
+    uint32_t SW = 0;                // words per smem stage
+    uint32_t lastmask = 0xFFFFFFFFu;
+};
+
+PackedPlan build_packed_plan(const HostFrac& F, int q) {
+    if (q < 2 || (q & 1) || q > F.r) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "packed tile level must be even, 2 <= q <= level");
+    const TilePlan P8 = build_plan(F, q, 8), P4 = build_plan(F, q, 4);
+    PackedPlan PP;
+    PP.q = q; PP.wq = P8.wq; PP.C = P8.C; PP.Cp = (P8.C + 3) & ~3; PP.L = P8.L;
+    PP.Wc = P8.Wc; PP.Hc = P8.Hc; PP.T = P8.Wc * P8.Hc; PP.NG = (PP.T + 31) / 32;
+    PP.sq = F.spow[q];
+    PP.nH = P8.nH; PP.nD = P8.nD;
+    for (int i = 0; i < 8; ++i) PP.dlist[i] = P8.dlist[i];
+    std::map<int, int> m_of;
+    std::map<std::tuple<int, int, int>, int> key8;
+    for (int j = 0; j < P8.nH; ++j) {
+        const int cell = P8.ha[j] * P8.wq + P8.hc[j];
+        auto it = m_of.find(cell);
+        int m;
+        if (it == m_of.end()) { m = (int)PP.srcidx.size(); m_of[cell] = m; PP.srcidx.push_back((uint32_t)cell); }
+        else m = it->second;
+        PP.slot.push_back(((uint32_t)P8.hDslot[j] << 16) | (uint32_t)m);
+        PP.slotD.push_back(P8.hD[j]);
+        key8[std::make_tuple((int)P8.hD[j], (int)P8.ha[j], (int)P8.hc[j])] = j;
+    }
+    PP.nSrc = (int)PP.srcidx.size();
+    const uint32_t zero = (uint32_t)(PP.Cp + PP.nH);
+    PP.wide = 4ull * zero > 0xFFFFull;
+    PP.SW = (zero + 1 + 3) & ~3u;
+    PP.nbr[1].resize((size_t)PP.C * 8);
+    PP.nbr[0].resize((size_t)PP.C * 8);
+    for (size_t e = 0; e < PP.nbr[1].size(); ++e) {
+        const uint32_t v = P8.nbr[e] / 4;
+        const uint32_t word = v < (uint32_t)PP.C ? v : (v == (uint32_t)(P8.C + P8.nH) ? zero : (uint32_t)PP.Cp + v - PP.C);
+        PP.nbr[1][e] = 4 * word;
+    }
+    for (size_t e = 0; e < PP.nbr[0].size(); ++e) {
+        const uint32_t v = P4.nbr[e] / 4;
+        uint32_t word;
+        if (v < (uint32_t)PP.C) word = v;
+        else if (v == (uint32_t)(P4.C + P4.nH)) word = zero;
+        else {
+            const int j4 = (int)(v - PP.C);
+            auto it = key8.find(std::make_tuple((int)P4.hD[j4], (int)P4.ha[j4], (int)P4.hc[j4]));
+            if (it == key8.end()) raise(NBBGPU_ERR_CUDA, "internal: von Neumann halo slot missing from the Moore plan");
+            word = (uint32_t)PP.Cp + (uint32_t)it->second;
+        }
+        PP.nbr[0][e] = 4 * word;
+    }
+    if (PP.T % 32) PP.lastmask = (1u << (PP.T % 32)) - 1u;
+    PP.loc.resize(PP.C);
+    for (int i = 0; i < PP.C; ++i) {
+        int64_t xl, yl;
+        F.lambda(i % PP.wq, i / PP.wq, xl, yl, q);
+        PP.loc[i] = ((uint32_t)yl << 16) | (uint32_t)xl;
+    }
+    return PP;
+}
+
+// Tile level of the packed kernel: the largest even q whose group record fits the
+// smem ring and still leaves >= 4 groups per SM; else the smallest feasible q.
+// NBBGPU_PACKED_Q overrides (tuning).
+int choose_packed_level(const HostFrac& F) {
+    if (const char* e = getenv("NBBGPU_PACKED_Q")) {
+        const int q = atoi(e);
+        if (q >= 2 && !(q & 1) && q <= F.r) return q;
+    }
+    int best = -1, fallback = -1;
+    for (int q = 2; q <= F.r; q += 2) {
+        const int64_t wq = HostFrac::ipow(F.k, q / 2);
+        if (wq * wq > kPackedMaxCells) break;
+        if (F.spow[q] > 65535) break;
+        const int64_t T = (F.w / wq) * (F.h / wq);
+        if (T >= ((int64_t)1 << 32) - 64) continue;
+        const int64_t NG = (T + 31) / 32;
+        if (fallback < 0) fallback = q;
+        if (NG >= 4 * 148) best = q;
+    }
+    return best >= 0 ? best : fallback;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -328,6 +428,7 @@ struct nbbgpu_sim {
     // partition (rows of the partition unit: tiles when q > 0, compact rows otherwise)
     int rank = 0, nranks = 1;
     int part_q = 0;           // tile level the partition is expressed in
+    bool part_packed = false; // partition unit = packed groups, halo elements = boundary words
     int64_t unit_rows = 1;    // compact rows per partition row (k^(q/2))
     int64_t prow0 = 0, prow1 = 0;  // owned partition rows
     std::vector<std::vector<uint64_t>> needs;   // per peer: offsets I need from peer
@@ -342,6 +443,21 @@ struct nbbgpu_sim {
     uint8_t* d_sendbuf = nullptr;
     uint8_t* d_recvbuf = nullptr;
     uint64_t n_send_all = 0, n_recv_all = 0;
+
+    // packed layout (packed.cuh): state bit-sliced over groups of 32 tiles
+    int layout = 0;                 // 0 = reference bytes (buf), 1 = packed (pk, bnd)
+    int pq = -1;                    // packed tile level (-1: unavailable)
+    PackedPlan pp;
+    bool pp_built = false;
+    uint32_t* pk[2] = {nullptr, nullptr};   // packed state, NG * Cp words
+    uint32_t* bnd[2] = {nullptr, nullptr};  // boundary planes, NG * nSrc words
+    void* d_pnbr[2] = {nullptr, nullptr};   // [moore] neighbour offsets
+    uint32_t* d_pslot = nullptr;
+    uint32_t* d_pntab = nullptr;            // [nD][T] linear neighbour tiles
+    uint32_t* d_psrc = nullptr;
+    uint32_t* d_ploc = nullptr;
+    uint64_t packed_table_bytes = 0;
+    int64_t pg0 = 0, pg1 = 0;               // owned groups
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -416,13 +532,277 @@ void ensure_plan(nbbgpu_t h, int moore) {
 // T r=10 naive 12 us vs tiled 17 us; r=11 equal; r=12 naive 43 us vs tiled 19 us).
 constexpr uint64_t kTiledMinCells = 1ull << 17;
 
-int resolve_kernel(nbbgpu_t h) {
+bool is_device_ptr(const void* p);
+
+int resolve_kernel_for(nbbgpu_t h, int kernel) {
     if (h->mode == NBBGPU_MODE_BB) return NBBGPU_KERNEL_NAIVE;
-    if (h->kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
-    if (h->q > 0 && (h->kernel == NBBGPU_KERNEL_TILED || h->cells >= kTiledMinCells))
+    if (kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
+    if (kernel == NBBGPU_KERNEL_PACKED) {
+        if (h->pq < 2) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
+        return NBBGPU_KERNEL_PACKED;
+    }
+    if (kernel == NBBGPU_KERNEL_AUTO && h->pq >= 2) return NBBGPU_KERNEL_PACKED;
+    if (h->q > 0 && (kernel == NBBGPU_KERNEL_TILED || h->cells >= kTiledMinCells))
         return NBBGPU_KERNEL_TILED;
-    if (h->kernel == NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
+    if (kernel == NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
     return NBBGPU_KERNEL_NAIVE;
+}
+int resolve_kernel(nbbgpu_t h) { return resolve_kernel_for(h, h->kernel); }
+int layout_of_kernel(int k) { return k == NBBGPU_KERNEL_PACKED ? 1 : 0; }
+
+// ---------------------------------------------------------------------------
+// packed layout: tables, buffers, conversions (packed.cuh)
+// ---------------------------------------------------------------------------
+PackedGeom packed_geom(nbbgpu_t h) {
+    const PackedPlan& P = h->pp;
+    PackedGeom G{};
+    G.f = h->frac;
+    G.q = (uint32_t)P.q; G.WQ = (uint32_t)P.wq; G.C = (uint32_t)P.C; G.Cp = (uint32_t)P.Cp;
+    G.Wc = (uint32_t)P.Wc; G.Hc = (uint32_t)P.Hc; G.L = (uint32_t)P.L;
+    G.T = (uint32_t)P.T; G.NG = (uint32_t)P.NG; G.sq = (uint32_t)P.sq;
+    G.w = (uint64_t)h->hf.w;
+    return G;
+}
+
+uint64_t packed_words(const PackedPlan& P) { return (uint64_t)P.NG * P.Cp; }
+uint64_t bnd_words(const PackedPlan& P) { return std::max<uint64_t>(1, (uint64_t)P.NG * P.nSrc); }
+
+template <class T>
+void dmalloc_cap(T*& p, size_t bytes, const char* what) {
+    if (cudaMalloc((void**)&p, std::max<size_t>(bytes, 4)) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        raise(NBBGPU_ERR_CAPACITY, std::string(what) + " exceeds the device memory (memory cap)");
+    }
+}
+
+// plan tables on the device (once per handle)
+void ensure_packed_tables(nbbgpu_t h) {
+    if (h->pp_built) return;
+    if (h->pq < 2) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
+    PackedPlan P = build_packed_plan(h->hf, h->pq);
+    uint64_t tb = 0;
+    for (int m = 0; m < 2; ++m) {
+        if (P.wide) {
+            dmalloc_cap(h->d_pnbr[m], P.nbr[m].size() * 4, "neighbour table");
+            CK(cudaMemcpy(h->d_pnbr[m], P.nbr[m].data(), P.nbr[m].size() * 4, cudaMemcpyHostToDevice));
+            tb += P.nbr[m].size() * 4;
+        } else {
+            std::vector<uint16_t> n16(P.nbr[m].begin(), P.nbr[m].end());
+            dmalloc_cap(h->d_pnbr[m], n16.size() * 2, "neighbour table");
+            CK(cudaMemcpy(h->d_pnbr[m], n16.data(), n16.size() * 2, cudaMemcpyHostToDevice));
+            tb += n16.size() * 2;
+        }
+    }
+    dmalloc_cap(h->d_pslot, P.slot.size() * 4, "halo table");
+    if (!P.slot.empty()) CK(cudaMemcpy(h->d_pslot, P.slot.data(), P.slot.size() * 4, cudaMemcpyHostToDevice));
+    dmalloc_cap(h->d_psrc, P.srcidx.size() * 4, "halo table");
+    if (!P.srcidx.empty()) CK(cudaMemcpy(h->d_psrc, P.srcidx.data(), P.srcidx.size() * 4, cudaMemcpyHostToDevice));
+    dmalloc_cap(h->d_ploc, P.loc.size() * 4, "lambda table");
+    CK(cudaMemcpy(h->d_ploc, P.loc.data(), P.loc.size() * 4, cudaMemcpyHostToDevice));
+    const uint64_t nt = (uint64_t)P.nD * P.T;
+    dmalloc_cap(h->d_pntab, nt * 4, "coarse neighbour table");
+    tb += (P.slot.size() + P.srcidx.size() + P.loc.size() + nt) * 4;
+    if (P.nD > 0) {
+        const int8_t* d = P.dlist;
+#define NBB_CALL(K, S, ...) build_ntab_linear_kernel<K, S><<<grid_for(P.T, 256), 256, 0, h->stream>>>(h->frac, P.L, (uint32_t)P.Wc, (uint32_t)P.Hc, P.nD, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], h->d_pntab)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->pp = std::move(P);
+    h->pp_built = true;
+    h->packed_table_bytes = tb;
+    h->bytes_held += tb;
+    h->pg0 = 0;
+    h->pg1 = h->pp.NG;
+}
+
+void free_packed_state(nbbgpu_t h) {
+    for (int b = 0; b < 2; ++b) {
+        if (h->pk[b]) { cudaFree(h->pk[b]); h->pk[b] = nullptr; h->bytes_held -= packed_words(h->pp) * 4; }
+        if (h->bnd[b]) { cudaFree(h->bnd[b]); h->bnd[b] = nullptr; h->bytes_held -= bnd_words(h->pp) * 4; }
+    }
+}
+
+void free_byte_state(nbbgpu_t h) {
+    for (int b = 0; b < 2; ++b)
+        if (h->buf[b]) { cudaFree(h->buf[b]); h->buf[b] = nullptr; h->bytes_held -= h->cells + 64; }
+}
+
+void alloc_byte_state(nbbgpu_t h) {
+    for (int b = 0; b < 2; ++b) {
+        if (h->buf[b]) continue;
+        if (cudaMalloc(&h->buf[b], h->cells + 64) != cudaSuccess) {
+            cudaGetLastError();
+            raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(h->cells) + " cells exceeds the device memory (memory cap)");
+        }
+        h->bytes_held += h->cells + 64;
+        CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
+    }
+}
+
+void alloc_packed_state(nbbgpu_t h) {
+    ensure_packed_tables(h);
+    for (int b = 0; b < 2; ++b) {
+        if (!h->pk[b]) {
+            dmalloc_cap(h->pk[b], packed_words(h->pp) * 4, "packed grid");
+            h->bytes_held += packed_words(h->pp) * 4;
+            CK(cudaMemsetAsync(h->pk[b], 0, packed_words(h->pp) * 4, h->stream));
+        }
+        if (!h->bnd[b]) {
+            dmalloc_cap(h->bnd[b], bnd_words(h->pp) * 4, "boundary plane");
+            h->bytes_held += bnd_words(h->pp) * 4;
+            CK(cudaMemsetAsync(h->bnd[b], 0, bnd_words(h->pp) * 4, h->stream));
+        }
+    }
+}
+
+void bnd_refresh(nbbgpu_t h) {
+    const PackedPlan& P = h->pp;
+    if (P.nSrc == 0) return;
+    bnd_refresh_kernel<<<grid_for((uint64_t)P.NG * P.nSrc, 256), 256, 0, h->stream>>>(
+        h->pk[h->cur], (uint32_t)P.Cp, (uint32_t)P.NG, (uint32_t)P.nSrc, h->d_psrc, h->bnd[h->cur]);
+    CK(cudaGetLastError());
+}
+
+// coarse rows per staging chunk for byte <-> packed conversions (bounded device memory)
+// (NBBGPU_STAGE_BYTES overrides the 256 MB default; the tests force many chunks)
+int64_t chunk_rows(nbbgpu_t h) {
+    uint64_t stage = 256ull << 20;
+    if (const char* e = getenv("NBBGPU_STAGE_BYTES")) stage = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    const uint64_t row_bytes = (uint64_t)h->pp.wq * (uint64_t)h->hf.w;
+    return (int64_t)std::max<uint64_t>(1, stage / std::max<uint64_t>(1, row_bytes));
+}
+
+// bytes (host or device, reference layout) -> packed buffer dstP.  Returns false if
+// a byte > 1 was seen (dstP then holds garbage; callers restore).
+bool packed_from_bytes(nbbgpu_t h, const uint8_t* src, uint32_t* dstP) {
+    const PackedPlan& P = h->pp;
+    const PackedGeom G = packed_geom(h);
+    CK(cudaMemsetAsync(dstP, 0, packed_words(P) * 4, h->stream));
+    CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+    const int64_t cr = chunk_rows(h);
+    const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
+    const bool dev = is_device_ptr(src);
+    uint8_t* stage = nullptr;
+    if (!dev) dmalloc_cap(stage, std::min<uint64_t>(h->cells, cr * row_bytes), "staging buffer");
+    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr) {
+        const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
+        const uint64_t nb = (uint64_t)(Y1 - Y0) * row_bytes;
+        const uint8_t* chunk = src + (uint64_t)Y0 * row_bytes;
+        if (!dev) {
+            CK(cudaMemcpyAsync(stage, chunk, nb, cudaMemcpyDefault, h->stream));
+            chunk = stage;
+        }
+        check_binary_kernel<<<grid_for(nb, 256), 256, 0, h->stream>>>(chunk, nb, h->d_flag);
+        const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
+        pack_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, chunk, (uint32_t)Y0, (uint32_t)Y1, dstP);
+        CK(cudaGetLastError());
+        if (!dev) CK(cudaStreamSynchronize(h->stream));  // stage reuse
+    }
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (stage) cudaFree(stage);
+    return flag == 0;
+}
+
+// packed buffer srcP -> bytes (host or device, reference layout)
+void packed_to_bytes(nbbgpu_t h, const uint32_t* srcP, uint8_t* dst) {
+    const PackedPlan& P = h->pp;
+    const PackedGeom G = packed_geom(h);
+    const int64_t cr = chunk_rows(h);
+    const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
+    const bool dev = is_device_ptr(dst);
+    uint8_t* stage = nullptr;
+    if (!dev) dmalloc_cap(stage, std::min<uint64_t>(h->cells, cr * row_bytes), "staging buffer");
+    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr) {
+        const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
+        const uint64_t nb = (uint64_t)(Y1 - Y0) * row_bytes;
+        uint8_t* chunk = dev ? dst + (uint64_t)Y0 * row_bytes : stage;
+        const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
+        unpack_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, srcP, (uint32_t)Y0, (uint32_t)Y1, chunk);
+        CK(cudaGetLastError());
+        if (!dev) {
+            CK(cudaMemcpyAsync(dst + (uint64_t)Y0 * row_bytes, stage, nb, cudaMemcpyDefault, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    if (stage) cudaFree(stage);
+}
+
+// switch the state layout, converting the front state on the device
+void set_layout(nbbgpu_t h, int want) {
+    if (h->layout == want && (want == 1 ? h->pk[0] != nullptr : h->buf[0] != nullptr)) return;
+    if (want == 1) {
+        alloc_packed_state(h);
+        if (h->buf[h->cur]) {
+            if (!packed_from_bytes(h, h->buf[h->cur], h->pk[0])) raise(NBBGPU_ERR_CUDA, "internal: non-binary state");
+        }
+        CK(cudaMemsetAsync(h->pk[1], 0, packed_words(h->pp) * 4, h->stream));
+        h->cur = 0;
+        bnd_refresh(h);
+        CK(cudaStreamSynchronize(h->stream));
+        free_byte_state(h);
+        h->layout = 1;
+    } else {
+        alloc_byte_state(h);
+        if (h->pk[h->cur]) packed_to_bytes(h, h->pk[h->cur], h->buf[0]);
+        CK(cudaMemsetAsync(h->buf[1], 0, h->cells + 64, h->stream));
+        h->cur = 0;
+        CK(cudaStreamSynchronize(h->stream));
+        free_packed_state(h);
+        h->layout = 0;
+    }
+}
+
+// packed word index + bit of the compact cell (cx, cy)
+void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t& bit) {
+    const PackedPlan& P = h->pp;
+    const int64_t X = cx / P.wq, c = cx % P.wq, Y = cy / P.wq, a = cy % P.wq;
+    const uint64_t t = (uint64_t)(Y * P.Wc + X);
+    word = (t / 32) * (uint64_t)P.Cp + (uint64_t)(a * P.wq + c);
+    bit = (uint32_t)(t % 32);
+}
+
+template <bool CONWAY, int DEG, bool WIDE>
+void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
+    auto kern = step_packed_kernel<CONWAY, DEG, WIDE>;
+    const size_t smem = 16 + 2 * (size_t)p.SW * 4;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr_set = true;
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPackedThreads, smem));
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const uint64_t groups = p.g1 - p.g0;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
+    kern<<<(unsigned)blocks, kPackedThreads, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
+}
+
+void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
+    const PackedPlan& P = h->pp;
+    PackedStepParams p{};
+    p.C = (uint32_t)P.C; p.Cp = (uint32_t)P.Cp; p.SW = P.SW;
+    p.nH = (uint32_t)P.nH; p.nSrc = (uint32_t)P.nSrc;
+    p.T = (uint32_t)P.T; p.NG = (uint32_t)P.NG;
+    p.g0 = (uint32_t)h->pg0; p.g1 = (uint32_t)h->pg1;
+    p.lastmask = P.lastmask;
+    p.birth = birth; p.survive = survive;
+    p.nbr = h->d_pnbr[moore];
+    p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc;
+    if (p.g1 <= p.g0) return;
+    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
+#define NBB_PK(CW, DG, WD) if (conway == CW && (moore ? 8 : 4) == DG && P.wide == WD) return launch_packed_t<CW, DG, WD>(h, p)
+    NBB_PK(true, 8, false); NBB_PK(false, 8, false); NBB_PK(true, 4, false); NBB_PK(false, 4, false);
+    NBB_PK(true, 8, true); NBB_PK(false, 8, true); NBB_PK(true, 4, true); NBB_PK(false, 4, true);
+#undef NBB_PK
 }
 
 template <int WQ, int K, int S, bool CONWAY>
@@ -464,6 +844,11 @@ void launch_tiled_w(nbbgpu_t h, int wq, const TiledParams& p, const uint8_t* src
 
 // owned compact-index range
 void owned_range(nbbgpu_t h, uint64_t& lo, uint64_t& hi) {
+    if (h->layout == 1) {  // packed words of the owned groups
+        lo = (uint64_t)h->pg0 * h->pp.Cp;
+        hi = (uint64_t)h->pg1 * h->pp.Cp;
+        return;
+    }
     if (h->mode == NBBGPU_MODE_BB || h->nranks == 1) {
         lo = 0;
         hi = h->cells;
@@ -519,6 +904,10 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
         return;
     }
     const int kern = resolve_kernel(h);
+    if (kern == NBBGPU_KERNEL_PACKED) {
+        launch_step_packed(h, birth, survive, moore);
+        return;
+    }
     if (kern == NBBGPU_KERNEL_NAIVE) {
         uint64_t lo, hi;
         owned_range(h, lo, hi);
@@ -587,6 +976,13 @@ void free_all(nbbgpu_t h) {
         if (h->d_hc[m]) cudaFree(h->d_hc[m]);
         if (h->d_hoff[m]) cudaFree(h->d_hoff[m]);
     }
+    for (auto*& p : h->pk) if (p) { cudaFree(p); p = nullptr; }
+    for (auto*& p : h->bnd) if (p) { cudaFree(p); p = nullptr; }
+    for (auto*& p : h->d_pnbr) if (p) { cudaFree(p); p = nullptr; }
+    if (h->d_pslot) cudaFree(h->d_pslot);
+    if (h->d_pntab) cudaFree(h->d_pntab);
+    if (h->d_psrc) cudaFree(h->d_psrc);
+    if (h->d_ploc) cudaFree(h->d_ploc);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
     if (h->d_send_all) cudaFree(h->d_send_all);
@@ -599,9 +995,21 @@ void free_all(nbbgpu_t h) {
     if (h->stream) cudaStreamDestroy(h->stream);
 }
 
-uint64_t device_hash(nbbgpu_t h, uint64_t lo, uint64_t hi) {
+uint64_t device_hash(nbbgpu_t h, bool owned) {
+    uint64_t lo = 0, hi = h->cells;
+    if (owned) owned_range(h, lo, hi);
+    if (h->layout == 1) { lo = owned ? h->pg0 : 0; hi = owned ? h->pg1 : h->pp.NG; }
     CK(cudaMemsetAsync(h->d_acc, 0, sizeof(unsigned long long), h->stream));
-    if (h->mode == NBBGPU_MODE_BB) {
+    if (h->layout == 1) {
+        const PackedGeom G = packed_geom(h);
+        const uint64_t g0 = lo, g1 = hi;  // group range for the packed layout
+        const uint64_t warps = (g1 - g0) * ((h->pp.C + 31) / 32);
+        if (warps) {
+#define NBB_CALL(K, S, ...) hash_packed_kernel<K, S><<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, h->d_ploc, h->pk[h->cur], (uint32_t)g0, (uint32_t)g1, h->d_acc)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+    } else if (h->mode == NBBGPU_MODE_BB) {
         hash_bb_kernel<<<grid_for((uint64_t)h->hf.side * h->hf.side, 256), 256, 0, h->stream>>>((uint32_t)h->hf.side, h->front(), h->d_acc);
     } else if (hi > lo) {
 #define NBB_CALL(K, S, ...) hash_compact_kernel<K, S><<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(h->frac, h->front(), lo, hi, h->d_acc)
@@ -733,20 +1141,21 @@ int nbbgpu_create(const int32_t* rep, int k, int s, int level, int mode, int dev
             for (int j = 0; j < mu / 2; ++j) t *= k;
             h->mt.tau[mu] = (uint32_t)t;
         }
-        // double buffer + 64 B slack for the tiled kernel's aligned 16-B accesses
-        const size_t bytes = (size_t)cells + 64;
-        for (int b = 0; b < 2; ++b) {
-            cudaError_t e = cudaMalloc(&h->buf[b], bytes);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(cells) + " cells exceeds the device memory (memory cap)");
-            }
-            CK(cudaMemsetAsync(h->buf[b], 0, bytes, h->stream));
-        }
         CK(cudaMalloc(&h->d_acc, sizeof(unsigned long long)));
         CK(cudaMalloc(&h->d_flag, sizeof(int)));
-        h->bytes_held = 2 * bytes + 16;
+        h->bytes_held = 16;
         h->q = mode == NBBGPU_MODE_COMPACT ? choose_tile_level(h->hf) : 0;
+        h->pq = mode == NBBGPU_MODE_COMPACT ? choose_packed_level(h->hf) : -1;
+        // state buffers of the default kernel's layout: packed (bit-sliced, 1/8 of the
+        // bytes) when a packed tile level exists, else the reference bytes (double
+        // buffer + 64 B slack for the tiled kernel's aligned 16-B accesses)
+        if (resolve_kernel(h) == NBBGPU_KERNEL_PACKED) {
+            alloc_packed_state(h);
+            h->layout = 1;
+        } else {
+            alloc_byte_state(h);
+            h->layout = 0;
+        }
         h->part_q = 0;
         h->unit_rows = 1;
         h->prow0 = 0;
@@ -773,9 +1182,21 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
     return guarded([&] {
         check_handle(h);
         if (!(density >= 0.0 && density <= 1.0)) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "density must be in [0,1]");
-        for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
         h->iteration = 0;
         const uint64_t mix = splitmix64(seed);
+        if (h->layout == 1) {
+            for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(h->pk[b], 0, packed_words(h->pp) * 4, h->stream));
+            const PackedGeom G = packed_geom(h);
+            const uint64_t warps = (uint64_t)G.NG * ((G.C + 31) / 32);
+#define NBB_CALL(K, S, ...) seed_packed_kernel<K, S><<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, h->d_ploc, h->pk[h->cur], mix, density)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+            CK(cudaGetLastError());
+            bnd_refresh(h);
+            CK(cudaStreamSynchronize(h->stream));
+            return;
+        }
+        for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
         if (h->mode == NBBGPU_MODE_BB) {
             const uint64_t n = h->cells;
 #define NBB_CALL(K, S, ...) seed_bb_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, h->front(), mix, density)
@@ -797,7 +1218,9 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     check_handle(h);
     if (nsteps < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "steps must be >= 0");
     moore = moore ? 1 : 0;
-    if (resolve_kernel(h) == NBBGPU_KERNEL_TILED) ensure_plan(h, moore);
+    const int rk = resolve_kernel(h);
+    if (layout_of_kernel(rk) != h->layout) raise(NBBGPU_ERR_CUDA, "internal: state layout does not match the kernel");
+    if (rk == NBBGPU_KERNEL_TILED) ensure_plan(h, moore);
     CK(cudaEventRecord(h->ev0, h->stream));
     for (int64_t i = 0; i < nsteps; ++i) {
         launch_step(h, birth, survive, moore);
@@ -824,7 +1247,7 @@ int nbbgpu_state_hash(nbbgpu_t h, uint64_t* out) {
     return guarded([&] {
         check_handle(h);
         if (!out) raise(NBBGPU_ERR_INVALID, "null output");
-        *out = device_hash(h, 0, h->cells);
+        *out = device_hash(h, false);
     });
 }
 
@@ -832,9 +1255,7 @@ int nbbgpu_state_hash_owned(nbbgpu_t h, uint64_t* out) {
     return guarded([&] {
         check_handle(h);
         if (!out) raise(NBBGPU_ERR_INVALID, "null output");
-        uint64_t lo, hi;
-        owned_range(h, lo, hi);
-        *out = device_hash(h, lo, hi);
+        *out = device_hash(h, true);
     });
 }
 
@@ -866,6 +1287,10 @@ int nbbgpu_download(nbbgpu_t h, uint8_t* dst, uint64_t bytes) {
         check_handle(h);
         if (bytes != h->cells) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "download size " + std::to_string(bytes) + " != stored cells " + std::to_string(h->cells));
         if (!dst) raise(NBBGPU_ERR_INVALID, "null destination");
+        if (h->layout == 1) {
+            packed_to_bytes(h, h->pk[h->cur], dst);
+            return;
+        }
         CK(cudaMemcpyAsync(dst, h->front(), bytes, cudaMemcpyDefault, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
@@ -876,6 +1301,19 @@ int nbbgpu_upload(nbbgpu_t h, const uint8_t* src, uint64_t bytes) {
         check_handle(h);
         if (bytes != h->cells) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "upload size " + std::to_string(bytes) + " != stored cells " + std::to_string(h->cells));
         if (!src) raise(NBBGPU_ERR_INVALID, "null source");
+        if (h->layout == 1) {
+            // pack into the back buffer (validating), then publish
+            if (!packed_from_bytes(h, src, h->pk[h->cur ^ 1])) {
+                CK(cudaMemsetAsync(h->pk[h->cur ^ 1], 0, packed_words(h->pp) * 4, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+                raise(NBBGPU_ERR_OUT_OF_DOMAIN, "GPU backends store binary cell states (bytes 0/1)");
+            }
+            h->cur ^= 1;
+            CK(cudaMemsetAsync(h->pk[h->cur ^ 1], 0, packed_words(h->pp) * 4, h->stream));
+            bnd_refresh(h);
+            CK(cudaStreamSynchronize(h->stream));
+            return;
+        }
         // stage into the back buffer, validate binary states, then publish
         CK(cudaMemcpyAsync(h->back(), src, bytes, cudaMemcpyDefault, h->stream));
         CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
@@ -900,6 +1338,17 @@ int nbbgpu_get_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t* out) {
         if (!out) raise(NBBGPU_ERR_INVALID, "null output");
         // Simulation::cell (stencil.cpp:182-188)
         if (x < 0 || y < 0 || x >= h->hf.side || y >= h->hf.side) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "embedded coordinate outside the bounding box");
+        if (h->layout == 1) {
+            int64_t cx, cy;
+            if (!h->hf.nu(x, y, cx, cy, h->hf.r)) { *out = 0; return; }
+            uint64_t wi;
+            uint32_t bit, word = 0;
+            packed_locate(h, cx, cy, wi, bit);
+            CK(cudaMemcpyAsync(&word, h->pk[h->cur] + wi, 4, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            *out = (uint8_t)((word >> bit) & 1u);
+            return;
+        }
         uint64_t idx;
         if (!storage_index(h, x, y, idx)) { *out = 0; return; }
         CK(cudaMemcpyAsync(out, h->front() + idx, 1, cudaMemcpyDeviceToHost, h->stream));
@@ -915,6 +1364,20 @@ int nbbgpu_set_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t state) {
         uint64_t idx;
         if (!storage_index(h, x, y, idx)) raise(NBBGPU_ERR_NOT_IN_FRACTAL, "set_cell requires a fractal cell");
         if (state > 1) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "GPU backends store binary cell states (bytes 0/1)");
+        if (h->layout == 1) {
+            int64_t cx, cy;
+            h->hf.nu(x, y, cx, cy, h->hf.r);
+            uint64_t wi;
+            uint32_t bit, word = 0;
+            packed_locate(h, cx, cy, wi, bit);
+            CK(cudaMemcpyAsync(&word, h->pk[h->cur] + wi, 4, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            word = (word & ~(1u << bit)) | ((uint32_t)state << bit);
+            CK(cudaMemcpyAsync(h->pk[h->cur] + wi, &word, 4, cudaMemcpyHostToDevice, h->stream));
+            bnd_refresh(h);
+            CK(cudaStreamSynchronize(h->stream));
+            return;
+        }
         CK(cudaMemcpyAsync(h->front() + idx, &state, 1, cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
@@ -930,10 +1393,14 @@ int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out) {
 int nbbgpu_set_kernel(nbbgpu_t h, int kernel) {
     return guarded([&] {
         if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
-        if (kernel < NBBGPU_KERNEL_AUTO || kernel > NBBGPU_KERNEL_TILED) raise(NBBGPU_ERR_INVALID, "unknown kernel");
+        if (kernel < NBBGPU_KERNEL_AUTO || kernel > NBBGPU_KERNEL_PACKED) raise(NBBGPU_ERR_INVALID, "unknown kernel");
         if (kernel == NBBGPU_KERNEL_TILED && (h->mode != NBBGPU_MODE_COMPACT || h->q == 0))
             raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
+        if (kernel == NBBGPU_KERNEL_PACKED && (h->mode != NBBGPU_MODE_COMPACT || h->pq < 2))
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
         if (h->nranks > 1 && kernel != h->kernel) raise(NBBGPU_ERR_INVALID, "kernel is fixed once partitioned");
+        CK(cudaSetDevice(h->device));
+        set_layout(h, layout_of_kernel(resolve_kernel_for(h, kernel)));
         h->kernel = kernel;
     });
 }
@@ -951,7 +1418,7 @@ int nbbgpu_active_kernel(nbbgpu_t h, int* kernel, int* tile_level) {
         if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
         const int k = resolve_kernel(h);
         if (kernel) *kernel = k;
-        if (tile_level) *tile_level = k == NBBGPU_KERNEL_TILED ? h->q : 0;
+        if (tile_level) *tile_level = k == NBBGPU_KERNEL_TILED ? h->q : (k == NBBGPU_KERNEL_PACKED ? h->pq : 0);
     });
 }
 
@@ -981,7 +1448,7 @@ int nbbgpu_nu_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, in
 int nbbgpu_front_device_ptr(nbbgpu_t h, void** out) {
     return guarded([&] {
         if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
-        *out = h->front();
+        *out = h->layout == 1 ? (void*)h->pk[h->cur] : (void*)h->front();
     });
 }
 

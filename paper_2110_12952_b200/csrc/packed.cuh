@@ -1,0 +1,379 @@
+// packed.cuh -- the throughput path: compact state kept BIT-SLICED in HBM.
+//
+// Layout ("packed", SURVEY.md 8(d) allows an internal bit-packing as long as the
+// roofline is quoted against the 2 B/cell model AND the packed model):
+//   * tile level q (even): a tile is a level-q sub-fractal, i.e. a WQ x WQ
+//     (WQ = k^(q/2)) sub-rectangle of the compact array laid out like the level-q
+//     compact array.  Tiles are numbered linearly over the coarse
+//     compact array: t = Y * Wc + X.
+//   * a group is 32 consecutive tiles; its record is Cp = round_up(C, 4) words of
+//     32 bits, word i = local cell i (i = a * WQ + c), bit b = tile 32 g + b.
+//     P[g * Cp + i].  k^r cells -> k^r / 8 bytes (+ < 1 group of padding).
+//   * the boundary plane B[g * nSrc + m] duplicates the words of the nSrc local
+//     cells that any neighbour tile reads (the halo sources).  It is tiny
+//     (T r=20, q=8: 0.4 MB), written by the step that produces the state and read
+//     by the next one -> halo gathers hit L2, never DRAM.
+// The reference semantics (stencil.cpp:334-368) hold bit for bit: out-of-box and
+// hole neighbours count 0 (the "zero word"), states are read from the front and
+// written to the back buffer only.  Bytes <-> packed conversion kernels below
+// give the reference's byte layout (cy*w + cx) back on download.
+#pragma once
+
+#include "naive.cuh"
+#include "tiled.cuh"
+
+namespace nbbgpu {
+
+constexpr int kPackedThreads = 256;
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
+struct PackedGeom {
+    Frac f;
+    uint32_t q, WQ, C, Cp;   // tile level, tile width, local cells, padded words per group
+    uint32_t Wc, Hc, L;      // coarse dims, coarse level r - q
+    uint32_t T, NG;          // tiles, groups
+    uint32_t sq;             // s^q (embedded tile side)
+    uint64_t w;              // compact row stride (bytes of the reference layout)
+};
+
+struct PackedStepParams {
+    uint32_t C, Cp, SW;      // local cells, words per group record, words per smem stage
+    uint32_t nH, nSrc;       // halo slots, boundary sources
+    uint32_t T, NG, g0, g1;  // tiles, groups, owned groups [g0, g1)
+    uint32_t lastmask;       // valid tile bits of group NG - 1
+    uint32_t birth, survive;
+    const void* nbr;         // [C][8] u16 (u32 when WIDE) byte offsets into the stage
+    const uint32_t* slot;    // per halo slot: (direction slot << 16) | boundary source m
+    const uint32_t* ntab;    // [nD][T] linear neighbour tile or kNoTile
+    const uint32_t* srcidx;  // per boundary source m: its local cell
+};
+
+// ---- mbarrier + 1-D bulk copy (TMA engine) -----------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+// The bit-sliced Life step of local cell i of a group staged at Sb (bytes):
+// 8 (or 4) neighbour words through the tile's neighbour table, a 14-LOP adder and
+// the rule (tiled.cuh).  Bit b of the result = next state of tile b's cell i.
+template <bool CONWAY, int DEG, bool WIDE>
+__device__ __forceinline__ uint32_t cell_word(const uint8_t* Sb, const void* nbr, uint32_t i,
+                                              const uint32_t (&KB)[9], const uint32_t (&KS)[9]) {
+    uint32_t o[8];
+    if (!WIDE) {
+        const uint4 e = __ldg(reinterpret_cast<const uint4*>(nbr) + i);
+        o[0] = e.x & 0xFFFFu; o[1] = e.x >> 16; o[2] = e.y & 0xFFFFu; o[3] = e.y >> 16;
+        o[4] = e.z & 0xFFFFu; o[5] = e.z >> 16; o[6] = e.w & 0xFFFFu; o[7] = e.w >> 16;
+    } else {
+        const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(nbr) + 2 * i);
+        o[0] = e0.x; o[1] = e0.y; o[2] = e0.z; o[3] = e0.w;
+        if (DEG == 8) {
+            const uint4 e1 = __ldg(reinterpret_cast<const uint4*>(nbr) + 2 * i + 1);
+            o[4] = e1.x; o[5] = e1.y; o[6] = e1.z; o[7] = e1.w;
+        } else {
+            o[4] = o[5] = o[6] = o[7] = 0;
+        }
+    }
+    uint32_t x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = j < DEG ? *reinterpret_cast<const uint32_t*>(Sb + o[j]) : 0u;
+    const uint32_t own = *reinterpret_cast<const uint32_t*>(Sb + 4 * i);
+    const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+    return apply_rule_bits<CONWAY>(cnt, own, KB, KS);
+}
+
+// One step over the owned groups.  Per CTA a 2-stage ring: the record of the next
+// group is in flight (one cp.async.bulk, mbarrier completion) while the halo words
+// of the current one are gathered from the boundary plane and its C words are
+// computed; results go straight to HBM with coalesced 32-bit stores.
+template <bool CONWAY, int DEG, bool WIDE>
+__global__ void __launch_bounds__(kPackedThreads)
+step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                   const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t mb = smem_u32(sm);  // two mbarriers at [0, 16)
+    uint8_t* st = sm + 16;
+    const uint32_t stage_bytes = p.SW * 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NWARPS = kPackedThreads / 32;
+
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    if (tid == 0) {
+        mbar_init(mb, 1);
+        mbar_init(mb + 8, 1);
+        mbar_fence_init();
+    }
+    if (tid < 2) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nH] = 0u;  // absent
+    __syncthreads();
+
+    const uint32_t rec_bytes = p.Cp * 4;
+    uint32_t g = p.g0 + blockIdx.x;
+    if (tid == 0 && g < p.g1) {
+        mbar_expect_tx(mb, rec_bytes);
+        bulk_g2s(smem_u32(st), src + (uint64_t)g * p.Cp, rec_bytes, mb);
+    }
+    uint32_t phase = 0;
+    for (int s = 0; g < p.g1; g += gridDim.x, s ^= 1) {
+        const uint32_t gn = g + gridDim.x;
+        if (tid == 0 && gn < p.g1) {  // stage s^1 was released by the last __syncthreads
+            mbar_expect_tx(mb + 8 * (s ^ 1), rec_bytes);
+            bulk_g2s(smem_u32(st + (s ^ 1) * stage_bytes), src + (uint64_t)gn * p.Cp, rec_bytes, mb + 8 * (s ^ 1));
+        }
+        uint8_t* Sb = st + s * stage_bytes;
+        uint32_t* S = reinterpret_cast<uint32_t*>(Sb);
+        // ---- halo words: warp w gathers slots w, w + 8, ... from the boundary plane
+        const uint32_t t = g * 32 + lane;
+        for (uint32_t jb = warp; jb < p.nH; jb += NWARPS * 4) {
+            uint32_t t2[4], sl[4], v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = jb + NWARPS * u;
+                t2[u] = kNoTile;
+                sl[u] = 0;
+                if (j < p.nH) {
+                    sl[u] = __ldg(p.slot + j);
+                    if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                v[u] = t2[u] != kNoTile
+                           ? (__ldg(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
+                           : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = jb + NWARPS * u;
+                const uint32_t word = __ballot_sync(0xFFFFFFFFu, v[u] != 0);
+                if (lane == 0 && j < p.nH) S[p.Cp + j] = word;
+            }
+        }
+        mbar_wait(mb + 8 * s, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        __syncthreads();
+        // ---- program: every local cell, straight to HBM -------------------------------
+        const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+        uint32_t* D = dst + (uint64_t)g * p.Cp;
+#pragma unroll 2
+        for (uint32_t i = tid; i < p.C; i += kPackedThreads)
+            D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
+        // boundary plane of the new state (a few words per group: recomputed)
+        for (uint32_t m = tid; m < p.nSrc; m += kPackedThreads)
+            bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+        __syncthreads();
+    }
+}
+
+// Static coarse-neighbour table over LINEAR tile indices (setup, once per plan):
+// out[ds * T + t] = linear index of the neighbour tile of t in direction dlist[ds]
+// (the carry walk of tiled.cuh, exactly nu(lambda(tile) + offset) at level L), or
+// kNoTile for a hole / outside the box.
+template <int K, int S>
+__global__ void build_ntab_linear_kernel(Frac f, int L, uint32_t Wc, uint32_t Hc, int nD, int8_t d0, int8_t d1,
+                                         int8_t d2, int8_t d3, int8_t d4, int8_t d5, int8_t d6, int8_t d7,
+                                         uint32_t* __restrict__ out) {
+    const int8_t dl[8] = {d0, d1, d2, d3, d4, d5, d6, d7};
+    const uint64_t n = (uint64_t)Wc * Hc;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t X = (uint32_t)(i % Wc), Y = (uint32_t)(i / Wc);
+        for (int ds = 0; ds < nD; ++ds) {
+            const int D = dl[ds];
+            uint32_t X2, Y2, v = kNoTile;
+            if (coarse_neighbor<K, S>(f, L, X, Y, D % 3 - 1, D / 3 - 1, X2, Y2)) v = Y2 * Wc + X2;
+            out[(uint64_t)ds * n + i] = v;
+        }
+    }
+}
+
+// ---- boundary plane from a packed state ---------------------------------------
+__global__ void bnd_refresh_kernel(const uint32_t* __restrict__ P, uint32_t Cp, uint32_t NG, uint32_t nSrc,
+                                   const uint32_t* __restrict__ srcidx, uint32_t* __restrict__ B) {
+    const uint64_t n = (uint64_t)NG * nSrc;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = i / nSrc;
+        const uint32_t m = (uint32_t)(i - g * nSrc);
+        B[i] = P[g * Cp + srcidx[m]];
+    }
+}
+
+// lambda at `levels` levels (CoordMapper::to_embedded restricted, maps.cpp:123-146)
+template <int K, int S>
+__device__ __forceinline__ void lambda_levels(const Frac& f, uint32_t cx, uint32_t cy, int levels, uint32_t& x,
+                                              uint32_t& y) {
+    const uint32_t k = kval<K>(f), s = sval<S>(f);
+    uint32_t ex = 0, ey = 0, sp = 1;
+    for (int mu = 0; mu < levels; ++mu) {
+        uint32_t d;
+        if ((mu & 1) == 0) { d = cx % k; cx /= k; }
+        else               { d = cy % k; cy /= k; }
+        ex += f.gx[d] * sp;
+        ey += f.gy[d] * sp;
+        sp *= s;
+    }
+    x = ex;
+    y = ey;
+}
+
+// Embedded origin of tile t: lambda of (cx, cy) splits into the tile's digits
+// (levels q..r-1, the coarse coordinates) and the local ones (levels 0..q-1):
+// lambda(X*WQ + c, Y*WQ + a) = s^q * lambda_L(X, Y) + lambda_q(c, a).
+template <int K, int S>
+__device__ __forceinline__ void tile_origin(const PackedGeom& G, uint32_t t, uint32_t& x0, uint32_t& y0) {
+    const uint32_t X = t % G.Wc, Y = t / G.Wc;
+    uint32_t xt, yt;
+    lambda_levels<K, S>(G.f, X, Y, (int)G.L, xt, yt);
+    x0 = xt * G.sq;
+    y0 = yt * G.sq;
+}
+
+// Simulation::seed_random (stencil.cpp:138-180) straight into the packed layout:
+// warp per (group, 32 local cells); lane b = tile b; loc[i] = (yl << 16) | xl is
+// the level-q lambda of local cell i.
+template <int K, int S>
+__global__ void seed_packed_kernel(PackedGeom G, const uint32_t* __restrict__ loc, uint32_t* __restrict__ P,
+                                   uint64_t seed_mix, double density) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cpw = (G.C + 31) / 32;  // 32-cell chunks per group
+    const uint64_t nw = (uint64_t)G.NG * cpw;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = (uint32_t)(wi / cpw), i0 = (uint32_t)(wi - (uint64_t)g * cpw) * 32;
+        const uint32_t t = g * 32 + lane;
+        const bool tv = t < G.T;
+        uint32_t x0 = 0, y0 = 0;
+        if (tv) tile_origin<K, S>(G, t, x0, y0);
+        uint32_t mine = 0;
+        for (uint32_t cc = 0; cc < 32; ++cc) {
+            const uint32_t i = i0 + cc;
+            bool alive = false;
+            if (tv && i < G.C) {
+                const uint32_t l = __ldg(loc + i);
+                alive = cell_alive_mixed(seed_mix, x0 + (l & 0xFFFFu), y0 + (l >> 16), density);
+            }
+            const uint32_t word = __ballot_sync(0xFFFFFFFFu, alive);
+            if (lane == cc) mine = word;
+        }
+        if (i0 + lane < G.C) P[(uint64_t)g * G.Cp + i0 + lane] = mine;
+    }
+}
+
+// Simulation::state_hash (stencil.cpp:207-216) over the groups [g0, g1).
+template <int K, int S>
+__global__ void hash_packed_kernel(PackedGeom G, const uint32_t* __restrict__ loc, const uint32_t* __restrict__ P,
+                                   uint32_t g0, uint32_t g1, unsigned long long* out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cpw = (G.C + 31) / 32;
+    const uint64_t nw = (uint64_t)(g1 - g0) * cpw;
+    uint64_t acc = 0;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = g0 + (uint32_t)(wi / cpw), i0 = (uint32_t)(wi % cpw) * 32;
+        const uint32_t t = g * 32 + lane;
+        const bool tv = t < G.T;
+        uint32_t x0 = 0, y0 = 0;
+        if (tv) tile_origin<K, S>(G, t, x0, y0);
+        const uint32_t mine = i0 + lane < G.C ? P[(uint64_t)g * G.Cp + i0 + lane] : 0u;
+        const uint32_t l_mine = i0 + lane < G.C ? __ldg(loc + i0 + lane) : 0u;
+        for (uint32_t cc = 0; cc < 32; ++cc) {
+            const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, cc);
+            const uint32_t l = __shfl_sync(0xFFFFFFFFu, l_mine, cc);
+            if (tv && ((word >> lane) & 1u)) acc += coord_mix(x0 + (l & 0xFFFFu), y0 + (l >> 16));
+        }
+    }
+    block_sum_atomic(acc, out);
+}
+
+// Reference bytes -> packed, for the tiles [tlo, thi) (coarse rows [Y0, Y1)).
+// `bytes` holds compact rows starting at compact row Y0 * WQ.  Warp per (group,
+// local row a): lane b reads tile b's row bytes, ballots give the words.
+__global__ void pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32_t Y1,
+                            uint32_t* __restrict__ P) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t tlo = Y0 * G.Wc, thi = Y1 * G.Wc;
+    const uint32_t glo = tlo / 32, ghi = (thi + 31) / 32;
+    const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
+        const uint32_t t = g * 32 + lane;
+        const bool tv = t >= tlo && t < thi && t < G.T;
+        const uint32_t lanes = __ballot_sync(0xFFFFFFFFu, tv);
+        uint64_t base = 0;
+        if (tv) {
+            const uint32_t X = t % G.Wc, Y = t / G.Wc;
+            base = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+        }
+        uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        for (uint32_t c0 = 0; c0 < G.WQ; c0 += 32) {
+            uint32_t mine = 0;
+            for (uint32_t cc = 0; cc < 32 && c0 + cc < G.WQ; ++cc) {
+                const bool bit = tv && bytes[base + c0 + cc] != 0;
+                const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
+                if (lane == cc) mine = word;
+            }
+            if (c0 + lane < G.WQ) {
+                // groups shared with a neighbouring row chunk keep the other tiles' bits
+                if (lanes == 0xFFFFFFFFu) R[c0 + lane] = mine;
+                else R[c0 + lane] = (R[c0 + lane] & ~lanes) | mine;
+            }
+        }
+    }
+}
+
+// Packed -> reference bytes for the tiles of coarse rows [Y0, Y1) (inverse of pack_kernel).
+__global__ void unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_t Y1,
+                              uint8_t* __restrict__ bytes) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t tlo = Y0 * G.Wc, thi = Y1 * G.Wc;
+    const uint32_t glo = tlo / 32, ghi = (thi + 31) / 32;
+    const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
+        const uint32_t t = g * 32 + lane;
+        const bool tv = t >= tlo && t < thi && t < G.T;
+        uint64_t base = 0;
+        if (tv) {
+            const uint32_t X = t % G.Wc, Y = t / G.Wc;
+            base = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+        }
+        const uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        for (uint32_t c0 = 0; c0 < G.WQ; c0 += 32) {
+            const uint32_t mine = c0 + lane < G.WQ ? R[c0 + lane] : 0u;
+            for (uint32_t cc = 0; cc < 32 && c0 + cc < G.WQ; ++cc) {
+                const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, cc);
+                if (tv) bytes[base + c0 + cc] = (uint8_t)((word >> lane) & 1u);
+            }
+        }
+    }
+}
+
+}  // namespace nbbgpu

@@ -37,6 +37,46 @@ def _needs(desc: FractalDescriptor, level: int, tile_level: int, rank: int, nran
     return out[:cnt.value]
 
 
+def _packed_needs(desc: FractalDescriptor, level: int, tile_level: int, rank: int, nranks: int,
+                  peer: int) -> np.ndarray:
+    L = _abi.lib()
+    rep = _abi.replica_array(desc.replicas)
+    cnt = C.c_uint64()
+    _abi.check(L.nbbgpu_plan_packed_needs(rep, desc.k, desc.s, level, tile_level, rank, nranks, peer,
+                                          None, C.byref(cnt)))
+    out = np.zeros(max(1, cnt.value), dtype=np.uint64)
+    _abi.check(L.nbbgpu_plan_packed_needs(rep, desc.k, desc.s, level, tile_level, rank, nranks, peer,
+                                          out.ctypes.data, C.byref(cnt)))
+    return out[:cnt.value]
+
+
+def plan_packed_level(desc: FractalDescriptor, level: int) -> int:
+    q = C.c_int()
+    _abi.check(_abi.lib().nbbgpu_plan_packed_level(_abi.replica_array(desc.replicas), desc.k, desc.s,
+                                                   level, C.byref(q)))
+    return q.value
+
+
+def packed_info(desc: FractalDescriptor, level: int, tile_level: int = -1) -> dict:
+    """Packed plan geometry (nbbgpu_plan_packed)."""
+    info = (C.c_int64 * 12)()
+    _abi.check(_abi.lib().nbbgpu_plan_packed(_abi.replica_array(desc.replicas), desc.k, desc.s, level,
+                                             tile_level, info))
+    keys = ["q", "wq", "C", "Cp", "nH", "nSrc", "T", "NG", "Wc", "Hc", "nD", "wide"]
+    return dict(zip(keys, [int(v) for v in info]))
+
+
+def packed_elem_cells(desc: FractalDescriptor, level: int, tile_level: int, elems: np.ndarray) -> np.ndarray:
+    """Compact byte offsets of the cells held by boundary-plane elements."""
+    elems = np.ascontiguousarray(elems, dtype=np.uint64)
+    out = np.zeros(max(1, 32 * elems.size), dtype=np.uint64)
+    cnt = C.c_uint64()
+    _abi.check(_abi.lib().nbbgpu_plan_packed_elem_cells(
+        _abi.replica_array(desc.replicas), desc.k, desc.s, level, tile_level,
+        elems.ctypes.data if elems.size else None, elems.size, out.ctypes.data, C.byref(cnt)))
+    return out[:cnt.value]
+
+
 def plan_tile_level(desc: FractalDescriptor, level: int) -> int:
     q = C.c_int()
     _abi.check(_abi.lib().nbbgpu_plan_tile_level(_abi.replica_array(desc.replicas), desc.k, desc.s,
@@ -46,20 +86,60 @@ def plan_tile_level(desc: FractalDescriptor, level: int) -> int:
 
 @dataclass
 class PartitionPlan:
-    """Owned compact range and halo lists of one rank (host only, no GPU)."""
+    """Owned range and halo lists of one rank (host only, no GPU).
+
+    Byte layouts: lo/hi = owned compact byte range, halo elements = state bytes at
+    compact byte offsets.  packed=True (the PACKED kernel): lo/hi = owned group
+    range [g0, g1), halo elements = 32-bit boundary-plane words (g * nSrc + m)."""
     desc: FractalDescriptor
     level: int
     rank: int
     nranks: int
     tile_level: int = -1
+    packed: bool = False
     lo: int = 0
     hi: int = 0
-    recv: Dict[int, np.ndarray] = field(default_factory=dict)  # offsets I need from peer
-    send: Dict[int, np.ndarray] = field(default_factory=dict)  # offsets peer needs from me
+    recv: Dict[int, np.ndarray] = field(default_factory=dict)  # elements I need from peer
+    send: Dict[int, np.ndarray] = field(default_factory=dict)  # elements peer needs from me
+
+    @property
+    def elem_bytes(self) -> int:
+        return 4 if self.packed else 1
+
+    def owned_cell_mask(self) -> np.ndarray:
+        """Boolean mask over the compact byte layout of the cells this rank owns."""
+        L = _abi.lib()
+        rep = _abi.replica_array(self.desc.replicas)
+        w = self.desc.k ** ((self.level + 1) // 2)
+        h = self.desc.k ** (self.level // 2)
+        mask = np.zeros(w * h, dtype=bool)
+        if not self.packed:
+            mask[self.lo:self.hi] = True
+            return mask
+        info = packed_info(self.desc, self.level, self.tile_level)
+        wq, Wc, Hc, T = info["wq"], info["Wc"], info["Hc"], info["T"]
+        tiles = np.zeros(Wc * Hc, dtype=bool)
+        tiles[self.lo * 32:min(self.hi * 32, T)] = True
+        m = np.repeat(np.repeat(tiles.reshape(Hc, Wc), wq, axis=0), wq, axis=1)
+        return m.reshape(-1)
 
     def __post_init__(self):
         L = _abi.lib()
         rep = _abi.replica_array(self.desc.replicas)
+        if self.packed:
+            g0, g1 = C.c_int64(), C.c_int64()
+            _abi.check(L.nbbgpu_plan_packed_partition(rep, self.desc.k, self.desc.s, self.level,
+                                                      self.tile_level, self.rank, self.nranks,
+                                                      C.byref(g0), C.byref(g1)))
+            self.lo, self.hi = g0.value, g1.value
+            for p in range(self.nranks):
+                if p == self.rank:
+                    continue
+                self.recv[p] = _packed_needs(self.desc, self.level, self.tile_level, self.rank,
+                                             self.nranks, p)
+                self.send[p] = _packed_needs(self.desc, self.level, self.tile_level, p, self.nranks,
+                                             self.rank)
+            return
         lo, hi = C.c_uint64(), C.c_uint64()
         _abi.check(L.nbbgpu_plan_partition(rep, self.desc.k, self.desc.s, self.level, self.tile_level,
                                            self.rank, self.nranks, C.byref(lo), C.byref(hi)))
@@ -75,7 +155,7 @@ class PartitionPlan:
         return [p for p in sorted(self.recv) if self.recv[p].size or self.send[p].size]
 
     def halo_bytes(self) -> int:
-        return int(sum(v.size for v in self.recv.values()))
+        return int(sum(v.size for v in self.recv.values())) * self.elem_bytes
 
 
 def exchange(plan: PartitionPlan, dist, pack: Callable[[int], "object"],
@@ -121,11 +201,16 @@ class DistributedSimulation:
         h = sim.handle()
         L = _abi.lib()
         _abi.check(L.nbbgpu_partition(h, rank, nranks))
-        _, q = sim.active_kernel()  # partition rows are tile rows of the kernel in use
-        self.plan = PartitionPlan(sim.desc, sim.level(), rank, nranks, tile_level=q)
+        kern, q = sim.active_kernel()  # partition units of the kernel in use
+        self.plan = PartitionPlan(sim.desc, sim.level(), rank, nranks, tile_level=q,
+                                  packed=kern == "packed")
         lo, hi = C.c_uint64(), C.c_uint64()
         _abi.check(L.nbbgpu_owned_range(h, C.byref(lo), C.byref(hi)))
-        assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"
+        if self.plan.packed:
+            cp = packed_info(sim.desc, sim.level(), q)["Cp"]
+            assert (lo.value, hi.value) == (self.plan.lo * cp, self.plan.hi * cp), "partition geometry mismatch"
+        else:
+            assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"
         self.launches_per_exchange = (int(any(self.plan.send[p].size for p in self.plan.peers)) +
                                       int(any(self.plan.recv[p].size for p in self.plan.peers)))
         if transport == "nccl":
@@ -138,12 +223,13 @@ class DistributedSimulation:
             _abi.check(L.nbbgpu_comm_init(h, uid, 128))
             return
         dev = torch.device("cuda", sim.options.device)
+        self._dtype = torch.int32 if self.plan.packed else torch.uint8
         self._send_bufs, self._recv_bufs = {}, {}
         for p in self.plan.peers:
             s = self.plan.send[p]
             _abi.check(L.nbbgpu_halo_set_sends(h, p, s.ctypes.data if s.size else None, s.size))
-            self._send_bufs[p] = torch.empty(max(1, s.size), dtype=torch.uint8, device=dev)
-            self._recv_bufs[p] = torch.empty(max(1, self.plan.recv[p].size), dtype=torch.uint8,
+            self._send_bufs[p] = torch.empty(max(1, s.size), dtype=self._dtype, device=dev)
+            self._recv_bufs[p] = torch.empty(max(1, self.plan.recv[p].size), dtype=self._dtype,
                                              device=dev)
         self.launches_per_exchange = sum(int(self.plan.send[p].size > 0) + int(self.plan.recv[p].size > 0)
                                          for p in self.plan.peers)
@@ -161,7 +247,7 @@ class DistributedSimulation:
             return self._send_bufs[p][:n].cpu() if self.host else self._send_bufs[p][:n]
 
         def recv_buffer(p, n):
-            return torch.empty(n, dtype=torch.uint8) if self.host else self._recv_bufs[p][:n]
+            return torch.empty(n, dtype=self._dtype) if self.host else self._recv_bufs[p][:n]
 
         def unpack(p, buf):
             if self.host:

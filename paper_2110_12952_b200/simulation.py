@@ -22,7 +22,7 @@ from .stencil import Backend, Neighborhood, StencilRule
 
 DEFAULT_MEMORY_CAP = 2 << 30  # kDefaultMemoryCap, proj/include/nbb/grid.hpp:13
 
-KERNELS = {"auto": 0, "naive": 1, "tiled": 2}
+KERNELS = {"auto": 0, "naive": 1, "tiled": 2, "packed": 3}
 MAP_VARIANTS = {"digit": 0, "mma": 1}
 
 
@@ -137,7 +137,7 @@ class Simulation:
     def active_kernel(self) -> Tuple[str, int]:
         k, q = C.c_int(), C.c_int()
         _abi.check(_abi.lib().nbbgpu_active_kernel(self._h, C.byref(k), C.byref(q)))
-        return {1: "naive", 2: "tiled"}[k.value], q.value
+        return {1: "naive", 2: "tiled", 3: "packed"}[k.value], q.value
 
     def handle(self):
         return self._h

@@ -12,6 +12,7 @@ from paper_2110_12952_b200 import (Backend, SimOptions, Simulation, StencilRule,
                                    Neighborhood, builtin_descriptor, run_simulation)
 from paper_2110_12952_b200.descriptor import FractalDescriptor
 from paper_2110_12952_b200.errors import CapacityError, NotInFractal, OutOfDomain
+from paper_2110_12952_b200 import _abi
 
 pytestmark = pytest.mark.gpu
 
@@ -31,10 +32,12 @@ def fnv(buf):
 
 
 def tiled_or_auto(desc, level, kernel):
-    # "tiled" forces the tile-parallel kernel wherever a tile level exists
-    from paper_2110_12952_b200.distributed import plan_tile_level
+    # "tiled" / "packed" force that kernel wherever its tile level exists
+    from paper_2110_12952_b200.distributed import plan_packed_level, plan_tile_level
     if kernel == "tiled" and plan_tile_level(desc, level) == 0:
-        return "auto"
+        return "naive"
+    if kernel == "packed" and plan_packed_level(desc, level) < 2:
+        return "naive"
     return kernel
 
 
@@ -61,7 +64,7 @@ def run_trace(t, backend, kernel="auto"):
     sim.close()
 
 
-@pytest.mark.parametrize("kernel", ["tiled", "naive", "auto"])
+@pytest.mark.parametrize("kernel", ["packed", "tiled", "naive", "auto"])
 def test_golden_traces_compact(golden, kernel):
     for t in golden["traces"]:
         run_trace(t, Backend.GpuCompact, kernel)
@@ -73,7 +76,7 @@ def test_golden_traces_bb(golden):
             run_trace(t, Backend.GpuBoundingBox)
 
 
-@pytest.mark.parametrize("kernel", ["tiled", "naive"])
+@pytest.mark.parametrize("kernel", ["packed", "tiled", "naive"])
 def test_golden_random_trials(golden, kernel):
     # acceptance.cpp:202-219 (C5, 50 trials) and test_stencil.cpp:155-182
     for t in golden["random_c5"] + golden["random_xbackend"]:
@@ -82,11 +85,16 @@ def test_golden_random_trials(golden, kernel):
             run_trace(t, Backend.GpuBoundingBox)
 
 
-def test_tiled_kernel_is_used_at_scale():
-    sim = Simulation(T, 12, Backend.GpuCompact)
+def test_kernel_selection():
+    sim = Simulation(T, 12, Backend.GpuCompact, SimOptions(kernel="tiled"))
     assert sim.active_kernel() == ("tiled", 6)
     sim2 = Simulation(T, 12, Backend.GpuCompact, SimOptions(kernel="naive"))
     assert sim2.active_kernel() == ("naive", 0)
+    assert Simulation(T, 16, Backend.GpuCompact).active_kernel() == ("packed", 6)
+    assert Simulation(T, 18, Backend.GpuCompact).active_kernel() == ("packed", 8)
+    # the packed state is 1/8 of the reference bytes (+ tables)
+    assert Simulation(T, 18, Backend.GpuCompact).peak_bytes() < 3 ** 18 // 3
+    assert Simulation(T, 1, Backend.GpuCompact).active_kernel() == ("naive", 0)
 
 
 def _lockstep_vs_oracle(desc, r, rule, seed, density, steps, kernel="auto", map_variant="digit"):
@@ -121,8 +129,74 @@ def test_tiled_randomized_lockstep():
                                Neighborhood.Moore if trial != 1 else Neighborhood.VonNeumann)
             if trial == 0:
                 rule = conway_rule()
-            _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)),
-                                float(rng.uniform(0.1, 0.9)), 4, kernel=tiled_or_auto(desc, r, "tiled"))
+            for kernel in ("tiled", "packed"):
+                _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)),
+                                    float(rng.uniform(0.1, 0.9)), 4, kernel=tiled_or_auto(desc, r, kernel))
+
+
+def test_packed_b0_rules_and_partial_groups():
+    # B0 rules wake every dead cell: the bits of the padding tiles of the last group
+    # must stay isolated (masked) and the result bit-exact
+    rng = np.random.default_rng(4321)
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    for desc, r in [(T, 5), (T, 7), (CARPET, 3), (VICSEK, 5), (Y, 3), (SOLID, 6)]:
+        for trial in range(3):
+            rule = StencilRule(int(rng.integers(0, 512)) | 1, int(rng.integers(0, 512)),
+                               Neighborhood.Moore if trial != 2 else Neighborhood.VonNeumann)
+            _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)), 0.5, 5,
+                                kernel=tiled_or_auto(desc, r, "packed"))
+
+
+def test_packed_tile_levels_forced(monkeypatch):
+    # every admissible packed tile level of a few cases gives the same bytes
+    for desc, r, qs in [(T, 9, (2, 4, 6, 8)), (CARPET, 4, (2, 4)), (VICSEK, 5, (2, 4))]:
+        for q in qs:
+            monkeypatch.setenv("NBBGPU_PACKED_Q", str(q))
+            sim = Simulation(desc, r, Backend.GpuCompact)
+            assert sim.active_kernel() == ("packed", q)
+            sim.close()
+            _lockstep_vs_oracle(desc, r, conway_rule(), 11 + q, 0.45, 4, kernel="packed")
+            _lockstep_vs_oracle(desc, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 12 + q,
+                                0.5, 3, kernel="packed")
+
+
+def test_kernel_switch_converts_state():
+    # bytes <-> packed conversions on the device keep the state exact
+    o = oracle.Oracle(T.replicas, 3, 2, 10)
+    o.seed(3, 0.5)
+    sim = Simulation(T, 10, Backend.GpuCompact, SimOptions(kernel="packed"))
+    sim.seed_random(3, 0.5)
+    L = _abi.lib()
+    for kernel in ("packed", "tiled", "naive", "packed", "auto", "tiled", "packed"):
+        _abi.check(L.nbbgpu_set_kernel(sim.handle(), {"auto": 0, "naive": 1, "tiled": 2, "packed": 3}[kernel]))
+        sim._front_cache = None
+        assert np.array_equal(sim.front().data, o.front), kernel
+        for _ in range(2):
+            sim.step(conway_rule())
+            o.step(8, 12, True)
+        assert np.array_equal(sim.front().data, o.front), kernel
+        assert sim.state_hash() == o.state_hash()
+
+
+def test_packed_chunked_conversions(monkeypatch):
+    # upload / download through several bounded staging chunks
+    monkeypatch.setenv("NBBGPU_STAGE_BYTES", "4096")
+    o = oracle.Oracle(CARPET.replicas, 8, 3, 5)
+    o.seed(9, 0.5)
+    sim = Simulation(CARPET, 5, Backend.GpuCompact, SimOptions(kernel="packed"))
+    sim.upload(o.front)
+    assert np.array_equal(sim.front().data, o.front)
+    assert sim.state_hash() == o.state_hash()
+    sim.step(conway_rule(), 3)
+    for _ in range(3):
+        o.step(8, 12, True)
+    assert np.array_equal(sim.front().data, o.front)
+    bad = o.front.copy()
+    bad[5] = 2
+    with pytest.raises(OutOfDomain):
+        sim.upload(bad)
+    assert np.array_equal(sim.front().data, o.front)  # unchanged on error
 
 
 def test_large_levels_hash(golden, golden_long):

@@ -25,7 +25,11 @@ def _run(desc, level, nranks, rule, steps, kernel="auto"):
         sim = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 40))
         sim.seed_random(5, 0.5)
         _abi.check(L.nbbgpu_partition(sim.handle(), r, nranks))
-        plan = PartitionPlan(desc, level, r, nranks, tile_level=-1 if kernel == "tiled" else 0)
+        kern, q = sim.active_kernel()
+        if kern == "packed":
+            plan = PartitionPlan(desc, level, r, nranks, tile_level=q, packed=True)
+        else:
+            plan = PartitionPlan(desc, level, r, nranks, tile_level=-1 if kernel == "tiled" else 0)
         for p in plan.peers:
             s = plan.send[p]
             _abi.check(L.nbbgpu_halo_set_sends(sim.handle(), p, s.ctypes.data if s.size else None, s.size))
@@ -38,7 +42,8 @@ def _run(desc, level, nranks, rule, steps, kernel="auto"):
         for r, (sim, plan) in enumerate(ranks):
             for p in plan.peers:
                 n = int(plan.send[p].size)
-                buf = torch.empty(max(1, n), dtype=torch.uint8, device="cuda")
+                buf = torch.empty(max(1, n), dtype=torch.int32 if plan.packed else torch.uint8,
+                                  device="cuda")
                 _abi.check(L.nbbgpu_halo_pack(sim.handle(), p, C.c_void_p(buf.data_ptr())))
                 packed[(r, p)] = buf
         for r, (sim, plan) in enumerate(ranks):
@@ -54,7 +59,8 @@ def _run(desc, level, nranks, rule, steps, kernel="auto"):
             _abi.check(L.nbbgpu_state_hash_owned(sim.handle(), C.byref(v)))
             parts.append(v.value)
             got = sim.front().data
-            assert np.array_equal(got[plan.lo:plan.hi], ref[plan.lo:plan.hi]), (desc.name, level, step)
+            m = plan.owned_cell_mask()
+            assert np.array_equal(got[m], ref[m]), (desc.name, level, step)
         assert wrap_u64_sum(parts) == full.state_hash(), (desc.name, level, step)
 
 
@@ -75,3 +81,12 @@ def test_partitioned_other_fractals():
 def test_partitioned_naive_kernel():
     T = builtin_descriptor("sierpinski-triangle")
     _run(T, 8, 3, StencilRule(8, 12, Neighborhood.Moore), 4, kernel="naive")
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_partitioned_packed(nranks):
+    T = builtin_descriptor("sierpinski-triangle")
+    C8 = builtin_descriptor("sierpinski-carpet")
+    _run(T, 12, nranks, StencilRule(8, 12, Neighborhood.Moore), 5, kernel="packed")
+    _run(T, 9, nranks, StencilRule(0x1C9, 0x6, Neighborhood.VonNeumann), 4, kernel="packed")
+    _run(C8, 5, nranks, StencilRule(8, 12, Neighborhood.Moore), 4, kernel="packed")
