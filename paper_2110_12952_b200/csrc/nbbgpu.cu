@@ -314,7 +314,77 @@ struct PackedPlan {
     bool wide = false;              // offsets do not fit 16 bits
     uint32_t SW = 0;                // words per smem stage
     uint32_t lastmask = 0xFFFFFFFFu;
+    int tag = 0;                    // micro-block descriptor (kTag*), 0 = generic program
+    std::vector<uint32_t> btab;     // micro-block external offsets (blocks.cuh)
 };
+
+// descriptors with compile-time micro-block wiring (blocks.cuh)
+enum { kTagNone = 0, kTagTriangle = 1, kTagCarpet = 2, kTagVicsek = 3, kTagH = 4, kTagCandy = 5 };
+
+template <class FT>
+bool matches_tag(const HostFrac& F) {
+    if (F.k != FT::K || F.s != FT::S) return false;
+    for (int i = 0; i < FT::K; ++i)
+        if (F.gx[i] != FT::GX[i] || F.gy[i] != FT::GY[i]) return false;
+    return true;
+}
+
+int descriptor_tag(const HostFrac& F) {
+    if (matches_tag<TriangleTag>(F)) return kTagTriangle;
+    if (matches_tag<CarpetTag>(F)) return kTagCarpet;
+    if (matches_tag<VicsekTag>(F)) return kTagVicsek;
+    if (matches_tag<HTag>(F)) return kTagH;
+    if (matches_tag<CandyTag>(F)) return kTagCandy;
+    return kTagNone;
+}
+
+// (tag, tile width) pairs with an instantiated micro-block kernel, and their block level
+int block_level_for(int tag, int wq) {
+    switch (tag) {
+        case kTagTriangle: return (wq == 27 || wq == 81) ? 2 : 0;
+        case kTagCarpet: return wq == 64 ? 1 : 0;
+        case kTagVicsek: return wq == 25 ? 2 : 0;
+        case kTagH: return wq == 49 ? 1 : 0;
+        case kTagCandy: return wq == 144 ? 1 : 0;
+        default: return 0;
+    }
+}
+
+// per micro-block: stage byte offsets of its NE external positions (blocks.cuh)
+template <class FT, int P>
+std::vector<uint32_t> build_block_table(const HostFrac& F, int q, int wq, int Cp, int nH,
+                                        const std::map<std::tuple<int, int, int>, int>& key8) {
+    using W = Wiring<FT, P>;
+    const int bpr = wq / W::BW, bpc = wq / W::BH;
+    const int64_t tside = F.spow[q];
+    const uint32_t zero = 4u * (uint32_t)(Cp + nH);
+    std::vector<uint32_t> t((size_t)bpr * bpc * W::NEP, zero);
+    for (int by = 0; by < bpc; ++by)
+        for (int bx = 0; bx < bpr; ++bx) {
+            // embedded origin of the block's s^P box = lambda(cell 0) - its in-box position
+            int64_t lx0, ly0;
+            F.lambda(bx * W::BW, by * W::BH, lx0, ly0, q);
+            lx0 -= W::d.ex[0];
+            ly0 -= W::d.ey[0];
+            for (int e = 0; e < W::NE; ++e) {
+                const int64_t X = lx0 + W::d.epx[e], Y = ly0 + W::d.epy[e];
+                const int Dx = X < 0 ? -1 : (X >= tside ? 1 : 0), Dy = Y < 0 ? -1 : (Y >= tside ? 1 : 0);
+                int64_t ncx, ncy;
+                uint32_t off = zero;
+                if (F.nu(X - Dx * tside, Y - Dy * tside, ncx, ncy, q)) {
+                    if (Dx == 0 && Dy == 0) {
+                        off = 4u * (uint32_t)(ncy * wq + ncx);
+                    } else {
+                        auto it = key8.find(std::make_tuple((Dy + 1) * 3 + Dx + 1, (int)ncy, (int)ncx));
+                        if (it == key8.end()) raise(NBBGPU_ERR_CUDA, "internal: micro-block external without a halo slot");
+                        off = 4u * (uint32_t)(Cp + it->second);
+                    }
+                }
+                t[((size_t)by * bpr + bx) * W::NEP + e] = off;
+            }
+        }
+    return t;
+}
 
 PackedPlan build_packed_plan(const HostFrac& F, int q) {
     if (q < 2 || (q & 1) || q > F.r) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "packed tile level must be even, 2 <= q <= level");
@@ -362,6 +432,19 @@ PackedPlan build_packed_plan(const HostFrac& F, int q) {
         PP.nbr[0][e] = 4 * word;
     }
     if (PP.T % 32) PP.lastmask = (1u << (PP.T % 32)) - 1u;
+    // micro-block program for descriptors with compile-time wiring
+    // (NBBGPU_GENERIC=1 forces the table-driven program, for comparisons)
+    const int tag = getenv("NBBGPU_GENERIC") ? kTagNone : descriptor_tag(F);
+    if (block_level_for(tag, PP.wq) > 0) {
+        PP.tag = tag;
+        switch (tag) {
+            case kTagTriangle: PP.btab = build_block_table<TriangleTag, 2>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+            case kTagCarpet: PP.btab = build_block_table<CarpetTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+            case kTagVicsek: PP.btab = build_block_table<VicsekTag, 2>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+            case kTagH: PP.btab = build_block_table<HTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+            case kTagCandy: PP.btab = build_block_table<CandyTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+        }
+    }
     PP.loc.resize(PP.C);
     for (int i = 0; i < PP.C; ++i) {
         int64_t xl, yl;
@@ -456,6 +539,7 @@ struct nbbgpu_sim {
     uint32_t* d_pntab = nullptr;            // [nD][T] linear neighbour tiles
     uint32_t* d_psrc = nullptr;
     uint32_t* d_ploc = nullptr;
+    uint32_t* d_pbtab = nullptr;            // micro-block external offsets
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
 
@@ -598,6 +682,11 @@ void ensure_packed_tables(nbbgpu_t h) {
     if (!P.slot.empty()) CK(cudaMemcpy(h->d_pslot, P.slot.data(), P.slot.size() * 4, cudaMemcpyHostToDevice));
     dmalloc_cap(h->d_psrc, P.srcidx.size() * 4, "halo table");
     if (!P.srcidx.empty()) CK(cudaMemcpy(h->d_psrc, P.srcidx.data(), P.srcidx.size() * 4, cudaMemcpyHostToDevice));
+    if (!P.btab.empty()) {
+        dmalloc_cap(h->d_pbtab, P.btab.size() * 4, "micro-block table");
+        CK(cudaMemcpy(h->d_pbtab, P.btab.data(), P.btab.size() * 4, cudaMemcpyHostToDevice));
+        tb += P.btab.size() * 4;
+    }
     dmalloc_cap(h->d_ploc, P.loc.size() * 4, "lambda table");
     CK(cudaMemcpy(h->d_ploc, P.loc.data(), P.loc.size() * 4, cudaMemcpyHostToDevice));
     const uint64_t nt = (uint64_t)P.nD * P.T;
@@ -768,9 +857,9 @@ void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t&
     bit = (uint32_t)(t % 32);
 }
 
-template <bool CONWAY, int DEG, bool WIDE>
+template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0>
 void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_kernel<CONWAY, DEG, WIDE>;
+    auto kern = step_packed_kernel<CONWAY, DEG, WIDE, FT, P, WQ>;
     const size_t smem = 16 + 2 * (size_t)p.SW * 4;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
@@ -796,9 +885,27 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     p.lastmask = P.lastmask;
     p.birth = birth; p.survive = survive;
     p.nbr = h->d_pnbr[moore];
-    p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc;
+    p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc; p.btab = h->d_pbtab;
     if (p.g1 <= p.g0) return;
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
+    if (P.tag != kTagNone) {
+        const int dg = moore ? 8 : 4;
+#define NBB_BK(TAG, FT, BP, W, WD)                                                                      \
+    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
+        if (conway && dg == 8) return launch_packed_t<true, 8, WD, FT, BP, W>(h, p);                    \
+        if (conway) return launch_packed_t<true, 4, WD, FT, BP, W>(h, p);                               \
+        if (dg == 8) return launch_packed_t<false, 8, WD, FT, BP, W>(h, p);                             \
+        return launch_packed_t<false, 4, WD, FT, BP, W>(h, p);                                          \
+    }
+        NBB_BK(kTagTriangle, TriangleTag, 2, 81, false)
+        NBB_BK(kTagTriangle, TriangleTag, 2, 27, false)
+        NBB_BK(kTagCarpet, CarpetTag, 1, 64, false)
+        NBB_BK(kTagVicsek, VicsekTag, 2, 25, false)
+        NBB_BK(kTagH, HTag, 1, 49, false)
+        NBB_BK(kTagCandy, CandyTag, 1, 144, true)
+#undef NBB_BK
+        raise(NBBGPU_ERR_CUDA, "internal: micro-block plan without a kernel");
+    }
 #define NBB_PK(CW, DG, WD) if (conway == CW && (moore ? 8 : 4) == DG && P.wide == WD) return launch_packed_t<CW, DG, WD>(h, p)
     NBB_PK(true, 8, false); NBB_PK(false, 8, false); NBB_PK(true, 4, false); NBB_PK(false, 4, false);
     NBB_PK(true, 8, true); NBB_PK(false, 8, true); NBB_PK(true, 4, true); NBB_PK(false, 4, true);
@@ -983,6 +1090,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_pntab) cudaFree(h->d_pntab);
     if (h->d_psrc) cudaFree(h->d_psrc);
     if (h->d_ploc) cudaFree(h->d_ploc);
+    if (h->d_pbtab) cudaFree(h->d_pbtab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
     if (h->d_send_all) cudaFree(h->d_send_all);

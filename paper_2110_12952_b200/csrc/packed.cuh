@@ -19,6 +19,9 @@
 // give the reference's byte layout (cy*w + cx) back on download.
 #pragma once
 
+#include <type_traits>
+
+#include "blocks.cuh"
 #include "naive.cuh"
 #include "tiled.cuh"
 
@@ -46,6 +49,7 @@ struct PackedStepParams {
     const uint32_t* slot;    // per halo slot: (direction slot << 16) | boundary source m
     const uint32_t* ntab;    // [nD][T] linear neighbour tile or kNoTile
     const uint32_t* srcidx;  // per boundary source m: its local cell
+    const uint32_t* btab;    // micro-block kernels: per block NEP stage byte offsets of its externals
 };
 
 // ---- mbarrier + 1-D bulk copy (TMA engine) -----------------------------------
@@ -104,11 +108,56 @@ __device__ __forceinline__ uint32_t cell_word(const uint8_t* Sb, const void* nbr
     return apply_rule_bits<CONWAY>(cnt, own, KB, KS);
 }
 
+// The bit-sliced step of every cell of micro-block `blk` (blocks.cuh): NB own
+// words and NE external words in registers, compile-time wiring, results to Dg.
+template <class FT, int P, int WQ, bool CONWAY, int DEG>
+__device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* btab, uint32_t blk,
+                                            uint32_t* Dg, uint32_t vmask, const uint32_t (&KB)[9],
+                                            const uint32_t (&KS)[9]) {
+    using W = Wiring<FT, P>;
+    constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
+    constexpr int BPR = WQ / BW;
+    const uint32_t by = blk / BPR, bx = blk - by * BPR;
+    const uint32_t base = by * (BH * WQ) + bx * BW;
+    const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
+    uint32_t own[NB];
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        own[N] = Sw[(N / BW) * WQ + N % BW];
+    });
+    uint32_t ext[NEP];
+    const uint4* t4 = reinterpret_cast<const uint4*>(btab) + (size_t)blk * (NEP / 4);
+    static_for<NEP / 4>([&](auto e4) {
+        constexpr int E = decltype(e4)::value;
+        const uint4 v = __ldg(t4 + E);
+        ext[4 * E + 0] = *reinterpret_cast<const uint32_t*>(Sb + v.x);
+        ext[4 * E + 1] = *reinterpret_cast<const uint32_t*>(Sb + v.y);
+        ext[4 * E + 2] = *reinterpret_cast<const uint32_t*>(Sb + v.z);
+        ext[4 * E + 3] = *reinterpret_cast<const uint32_t*>(Sb + v.w);
+    });
+    uint32_t* Dw = Dg + base;
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        uint32_t x[8];
+        static_for<8>([&](auto j) {
+            constexpr int J = decltype(j)::value;
+            constexpr int SJ = W::d.src[N][J];
+            if constexpr (J >= DEG || SJ == kWireAbsent) x[J] = 0u;
+            else if constexpr (SJ >= 0) x[J] = own[SJ];
+            else x[J] = ext[-SJ - 2];
+        });
+        const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+        Dw[(N / BW) * WQ + N % BW] = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
+    });
+}
+
 // One step over the owned groups.  Per CTA a 2-stage ring: the record of the next
 // group is in flight (one cp.async.bulk, mbarrier completion) while the halo words
 // of the current one are gathered from the boundary plane and its C words are
-// computed; results go straight to HBM with coalesced 32-bit stores.
-template <bool CONWAY, int DEG, bool WIDE>
+// computed; results go straight to HBM with coalesced 32-bit stores.  FT = void:
+// generic table-driven program (cell_word); else the micro-block program of the
+// compile-time descriptor FT at block level P and tile width WQ.
+template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0>
 __global__ void __launch_bounds__(kPackedThreads)
 step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                    const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
@@ -180,9 +229,15 @@ step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, u
         // ---- program: every local cell, straight to HBM -------------------------------
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
         uint32_t* D = dst + (uint64_t)g * p.Cp;
+        if constexpr (std::is_void<FT>::value) {
 #pragma unroll 2
-        for (uint32_t i = tid; i < p.C; i += kPackedThreads)
-            D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
+            for (uint32_t i = tid; i < p.C; i += kPackedThreads)
+                D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
+        } else {
+            constexpr uint32_t NBLK = (WQ / Wiring<FT, P>::BW) * (WQ / Wiring<FT, P>::BH);
+            for (uint32_t blk = tid; blk < NBLK; blk += kPackedThreads)
+                block_words<FT, P, WQ, CONWAY, DEG>(Sb, p.btab, blk, D, vmask, KB, KS);
+        }
         // boundary plane of the new state (a few words per group: recomputed)
         for (uint32_t m = tid; m < p.nSrc; m += kPackedThreads)
             bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;

@@ -150,8 +150,18 @@ def test_packed_b0_rules_and_partial_groups():
 
 def test_packed_tile_levels_forced(monkeypatch):
     # every admissible packed tile level of a few cases gives the same bytes
-    for desc, r, qs in [(T, 9, (2, 4, 6, 8)), (CARPET, 4, (2, 4)), (VICSEK, 5, (2, 4))]:
-        for q in qs:
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    cases = [(T, 9, (2, 4, 6, 8)), (T, 10, (6, 8)), (CARPET, 4, (2, 4)), (CARPET, 5, (4,)),
+             (VICSEK, 5, (2, 4)), (H, 4, (2, 4)), (H, 5, (4,)), (Y, 4, (2, 4)), (Y, 5, (4,))]
+    # micro-block programs (blocks.cuh) and the generic table-driven one
+    for desc, r, qs in cases:
+        for q, generic in [(q, g) for q in qs for g in (False, True)]:
+            if generic:
+                monkeypatch.setenv("NBBGPU_GENERIC", "1")
+            else:
+                monkeypatch.delenv("NBBGPU_GENERIC", raising=False)
             monkeypatch.setenv("NBBGPU_PACKED_Q", str(q))
             sim = Simulation(desc, r, Backend.GpuCompact)
             assert sim.active_kernel() == ("packed", q)
