@@ -304,7 +304,7 @@ constexpr int kPackedMaxCells = 24576;  // two smem stages of <= 96 KB
 struct PackedPlan {
     int q = -1, wq = 1, C = 1, Cp = 4, L = 0;
     int64_t Wc = 0, Hc = 0, T = 0, NG = 0, sq = 1;
-    int nH = 0, nD = 0, nSrc = 0;
+    int nH = 0, nHp = 0, nD = 0, nSrc = 0;
     int8_t dlist[8] = {0};
     std::vector<uint8_t> slotD;     // per slot: direction D = (dy+1)*3 + dx+1
     std::vector<uint32_t> slot;     // per slot: (direction slot << 16) | boundary source m
@@ -315,6 +315,7 @@ struct PackedPlan {
     uint32_t SW = 0;                // words per smem stage
     uint32_t lastmask = 0xFFFFFFFFu;
     int tag = 0;                    // micro-block descriptor (kTag*), 0 = generic program
+    int bP = 0;                     // micro-block level
     std::vector<uint32_t> btab;     // micro-block external offsets (blocks.cuh)
 };
 
@@ -352,12 +353,12 @@ int block_level_for(int tag, int wq) {
 
 // per micro-block: stage byte offsets of its NE external positions (blocks.cuh)
 template <class FT, int P>
-std::vector<uint32_t> build_block_table(const HostFrac& F, int q, int wq, int Cp, int nH,
+std::vector<uint32_t> build_block_table(const HostFrac& F, int q, int wq, int Cp, int nHp,
                                         const std::map<std::tuple<int, int, int>, int>& key8) {
     using W = Wiring<FT, P>;
     const int bpr = wq / W::BW, bpc = wq / W::BH;
     const int64_t tside = F.spow[q];
-    const uint32_t zero = 4u * (uint32_t)(Cp + nH);
+    const uint32_t zero = 4u * (uint32_t)(Cp + nHp);
     std::vector<uint32_t> t((size_t)bpr * bpc * W::NEP, zero);
     for (int by = 0; by < bpc; ++by)
         for (int bx = 0; bx < bpr; ++bx) {
@@ -408,9 +409,11 @@ PackedPlan build_packed_plan(const HostFrac& F, int q) {
         key8[std::make_tuple((int)P8.hD[j], (int)P8.ha[j], (int)P8.hc[j])] = j;
     }
     PP.nSrc = (int)PP.srcidx.size();
-    const uint32_t zero = (uint32_t)(PP.Cp + PP.nH);
+    // stage: [0, Cp) record | [Cp, Cp + nHp) halo words | zero word at Cp + nHp
+    PP.nHp = (PP.nH + 3) & ~3;
+    const uint32_t zero = (uint32_t)(PP.Cp + PP.nHp);
     PP.wide = 4ull * zero > 0xFFFFull;
-    PP.SW = (zero + 1 + 3) & ~3u;
+    PP.SW = zero + 4;
     PP.nbr[1].resize((size_t)PP.C * 8);
     PP.nbr[0].resize((size_t)PP.C * 8);
     for (size_t e = 0; e < PP.nbr[1].size(); ++e) {
@@ -438,11 +441,11 @@ PackedPlan build_packed_plan(const HostFrac& F, int q) {
     if (block_level_for(tag, PP.wq) > 0) {
         PP.tag = tag;
         switch (tag) {
-            case kTagTriangle: PP.btab = build_block_table<TriangleTag, 2>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
-            case kTagCarpet: PP.btab = build_block_table<CarpetTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
-            case kTagVicsek: PP.btab = build_block_table<VicsekTag, 2>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
-            case kTagH: PP.btab = build_block_table<HTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
-            case kTagCandy: PP.btab = build_block_table<CandyTag, 1>(F, q, PP.wq, PP.Cp, PP.nH, key8); break;
+            case kTagTriangle: PP.btab = build_block_table<TriangleTag, 2>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
+            case kTagCarpet: PP.btab = build_block_table<CarpetTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
+            case kTagVicsek: PP.btab = build_block_table<VicsekTag, 2>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
+            case kTagH: PP.btab = build_block_table<HTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
+            case kTagCandy: PP.btab = build_block_table<CandyTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
         }
     }
     PP.loc.resize(PP.C);
@@ -540,6 +543,7 @@ struct nbbgpu_sim {
     uint32_t* d_psrc = nullptr;
     uint32_t* d_ploc = nullptr;
     uint32_t* d_pbtab = nullptr;            // micro-block external offsets
+    uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
 
@@ -689,6 +693,8 @@ void ensure_packed_tables(nbbgpu_t h) {
     }
     dmalloc_cap(h->d_ploc, P.loc.size() * 4, "lambda table");
     CK(cudaMemcpy(h->d_ploc, P.loc.data(), P.loc.size() * 4, cudaMemcpyHostToDevice));
+    dmalloc_cap(h->d_phalo, (uint64_t)P.NG * P.nHp * 4, "halo words");
+    tb += (uint64_t)P.NG * P.nHp * 4;
     const uint64_t nt = (uint64_t)P.nD * P.T;
     dmalloc_cap(h->d_pntab, nt * 4, "coarse neighbour table");
     tb += (P.slot.size() + P.srcidx.size() + P.loc.size() + nt) * 4;
@@ -857,29 +863,48 @@ void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t&
     bit = (uint32_t)(t % 32);
 }
 
-template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0>
+template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0, int NT = kPackedThreads,
+          bool STAB = false>
 void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_kernel<CONWAY, DEG, WIDE, FT, P, WQ>;
-    const size_t smem = 16 + 2 * (size_t)p.SW * 4;
+    auto kern = step_packed_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NT, STAB>;
+    const size_t smem = 16 + (STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0) + 2 * (size_t)p.SW * 4;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr_set = true;
     }
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPackedThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     const uint64_t groups = p.g1 - p.g0;
     const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
-    kern<<<(unsigned)blocks, kPackedThreads, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
+    kern<<<(unsigned)blocks, NT, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
+}
+
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NCW, int NS, bool STAB>
+void launch_packed_ws_t(nbbgpu_t h, const PackedStepParams& p) {
+    auto kern = step_packed_ws_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NCW, NS, STAB>;
+    const size_t smem = 16 * NS + (STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0) + (size_t)NS * p.SW * 4;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: warp-specialised stage ring exceeds shared memory");
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const uint64_t groups = p.g1 - p.g0;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)sms));
+    kern<<<(unsigned)blocks, (NCW + 1) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
 void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const PackedPlan& P = h->pp;
     PackedStepParams p{};
     p.C = (uint32_t)P.C; p.Cp = (uint32_t)P.Cp; p.SW = P.SW;
-    p.nH = (uint32_t)P.nH; p.nSrc = (uint32_t)P.nSrc;
+    p.nH = (uint32_t)P.nH; p.nHp = (uint32_t)P.nHp; p.nSrc = (uint32_t)P.nSrc;
+    p.halo = h->d_phalo;
     p.T = (uint32_t)P.T; p.NG = (uint32_t)P.NG;
     p.g0 = (uint32_t)h->pg0; p.g1 = (uint32_t)h->pg1;
     p.lastmask = P.lastmask;
@@ -887,22 +912,42 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     p.nbr = h->d_pnbr[moore];
     p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc; p.btab = h->d_pbtab;
     if (p.g1 <= p.g0) return;
+    // halo words of every owned group from the boundary plane, then the step
+    if (P.nH > 0) {
+        const uint64_t warps = (uint64_t)(p.g1 - p.g0) * (uint64_t)((P.nH + 3) / 4);
+        halo_words_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
+        CK(cudaGetLastError());
+    }
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
     if (P.tag != kTagNone) {
         const int dg = moore ? 8 : 4;
-#define NBB_BK(TAG, FT, BP, W, WD)                                                                      \
+    // NT threads: one micro-block per thread per group where it fits a CTA; the
+    // block table in shared memory where it fits next to the two stages
+#define NBB_BK(TAG, FT, BP, W, WD, NTH, ST)                                                             \
     if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
-        if (conway && dg == 8) return launch_packed_t<true, 8, WD, FT, BP, W>(h, p);                    \
-        if (conway) return launch_packed_t<true, 4, WD, FT, BP, W>(h, p);                               \
-        if (dg == 8) return launch_packed_t<false, 8, WD, FT, BP, W>(h, p);                             \
-        return launch_packed_t<false, 4, WD, FT, BP, W>(h, p);                                          \
+        if (conway && dg == 8) return launch_packed_t<true, 8, WD, FT, BP, W, NTH, ST>(h, p);           \
+        if (conway) return launch_packed_t<true, 4, WD, FT, BP, W, NTH, ST>(h, p);                      \
+        if (dg == 8) return launch_packed_t<false, 8, WD, FT, BP, W, NTH, ST>(h, p);                    \
+        return launch_packed_t<false, 4, WD, FT, BP, W, NTH, ST>(h, p);                                 \
     }
-        NBB_BK(kTagTriangle, TriangleTag, 2, 81, false)
-        NBB_BK(kTagTriangle, TriangleTag, 2, 27, false)
-        NBB_BK(kTagCarpet, CarpetTag, 1, 64, false)
-        NBB_BK(kTagVicsek, VicsekTag, 2, 25, false)
-        NBB_BK(kTagH, HTag, 1, 49, false)
-        NBB_BK(kTagCandy, CandyTag, 1, 144, true)
+        static const int tri_cfg = getenv("NBBGPU_TRI_CFG") ? atoi(getenv("NBBGPU_TRI_CFG")) : 0;  // tuning knob
+#define NBB_WS(TAG, FT, BP, W, WD, NCW, NS, ST)                                                         \
+    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
+        if (conway && dg == 8) return launch_packed_ws_t<true, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);    \
+        if (conway) return launch_packed_ws_t<true, 4, WD, FT, BP, W, NCW, NS, ST>(h, p);               \
+        if (dg == 8) return launch_packed_ws_t<false, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);             \
+        return launch_packed_ws_t<false, 4, WD, FT, BP, W, NCW, NS, ST>(h, p);                          \
+    }
+        if (tri_cfg == 1) { NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 256, false) }
+        if (tri_cfg == 2) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 31, 4, true) }
+        if (tri_cfg == 3) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 6, false) }
+        if (tri_cfg == 0) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 4, true) }
+        NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 736, true)
+        NBB_BK(kTagTriangle, TriangleTag, 2, 27, false, 96, true)
+        NBB_BK(kTagCarpet, CarpetTag, 1, 64, false, 512, true)
+        NBB_BK(kTagVicsek, VicsekTag, 2, 25, false, 32, true)
+        NBB_BK(kTagH, HTag, 1, 49, false, 352, true)
+        NBB_BK(kTagCandy, CandyTag, 1, 144, true, 864, false)
 #undef NBB_BK
         raise(NBBGPU_ERR_CUDA, "internal: micro-block plan without a kernel");
     }
@@ -1091,6 +1136,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_psrc) cudaFree(h->d_psrc);
     if (h->d_ploc) cudaFree(h->d_ploc);
     if (h->d_pbtab) cudaFree(h->d_pbtab);
+    if (h->d_phalo) cudaFree(h->d_phalo);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
     if (h->d_send_all) cudaFree(h->d_send_all);

@@ -41,7 +41,7 @@ struct PackedGeom {
 
 struct PackedStepParams {
     uint32_t C, Cp, SW;      // local cells, words per group record, words per smem stage
-    uint32_t nH, nSrc;       // halo slots, boundary sources
+    uint32_t nH, nHp, nSrc;  // halo slots (padded to 4), boundary sources
     uint32_t T, NG, g0, g1;  // tiles, groups, owned groups [g0, g1)
     uint32_t lastmask;       // valid tile bits of group NG - 1
     uint32_t birth, survive;
@@ -50,7 +50,45 @@ struct PackedStepParams {
     const uint32_t* ntab;    // [nD][T] linear neighbour tile or kNoTile
     const uint32_t* srcidx;  // per boundary source m: its local cell
     const uint32_t* btab;    // micro-block kernels: per block NEP stage byte offsets of its externals
+    uint32_t* halo;          // [NG][nHp] halo words of the step (halo_words_kernel)
 };
+
+// Halo words of the owned groups for one step: H[g][j] bit b = state of the source
+// cell of slot j in the neighbour tile of tile 32 g + b (0 when there is none),
+// read from the boundary plane of the front state.  One warp per (group, 4 slots);
+// fully parallel, so the step kernel never waits on a dependent gather.
+__global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
+                                  uint32_t* __restrict__ H) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t spw = (p.nH + 3) / 4;
+    const uint64_t nw = (uint64_t)(p.g1 - p.g0) * spw;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = p.g0 + (uint32_t)(wi / spw), j0 = (uint32_t)(wi % spw) * 4;
+        const uint32_t t = g * 32 + lane;
+        uint32_t t2[4], sl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t j = j0 + u;
+            t2[u] = kNoTile;
+            sl[u] = 0;
+            if (j < p.nH) {
+                sl[u] = __ldg(p.slot + j);
+                if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
+            }
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t v = t2[u] != kNoTile
+                                   ? (__ldg(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
+                                   : 0u;
+            const uint32_t word = __ballot_sync(0xFFFFFFFFu, v != 0);
+            if (lane == (uint32_t)u) mine = word;
+        }
+        if (lane < 4 && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
+    }
+}
 
 // ---- mbarrier + 1-D bulk copy (TMA engine) -----------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -110,7 +148,7 @@ __device__ __forceinline__ uint32_t cell_word(const uint8_t* Sb, const void* nbr
 
 // The bit-sliced step of every cell of micro-block `blk` (blocks.cuh): NB own
 // words and NE external words in registers, compile-time wiring, results to Dg.
-template <class FT, int P, int WQ, bool CONWAY, int DEG>
+template <class FT, int P, int WQ, bool CONWAY, int DEG, bool STAB>
 __device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* btab, uint32_t blk,
                                             uint32_t* Dg, uint32_t vmask, const uint32_t (&KB)[9],
                                             const uint32_t (&KS)[9]) {
@@ -129,7 +167,9 @@ __device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* b
     const uint4* t4 = reinterpret_cast<const uint4*>(btab) + (size_t)blk * (NEP / 4);
     static_for<NEP / 4>([&](auto e4) {
         constexpr int E = decltype(e4)::value;
-        const uint4 v = __ldg(t4 + E);
+        uint4 v;
+        if constexpr (STAB) v = t4[E];  // table staged in shared memory
+        else v = __ldg(t4 + E);
         ext[4 * E + 0] = *reinterpret_cast<const uint32_t*>(Sb + v.x);
         ext[4 * E + 1] = *reinterpret_cast<const uint32_t*>(Sb + v.y);
         ext[4 * E + 2] = *reinterpret_cast<const uint32_t*>(Sb + v.z);
@@ -157,16 +197,35 @@ __device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* b
 // computed; results go straight to HBM with coalesced 32-bit stores.  FT = void:
 // generic table-driven program (cell_word); else the micro-block program of the
 // compile-time descriptor FT at block level P and tile width WQ.
-template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0>
-__global__ void __launch_bounds__(kPackedThreads)
+template <class FT, int P, int WQ>
+struct BlockGeom {
+    static constexpr int NBLK = (WQ / Wiring<FT, P>::BW) * (WQ / Wiring<FT, P>::BH);
+    static constexpr uint32_t TAB_BYTES = (uint32_t)NBLK * Wiring<FT, P>::NEP * 4;
+};
+template <int P, int WQ>
+struct BlockGeom<void, P, WQ> {
+    static constexpr int NBLK = 0;
+    static constexpr uint32_t TAB_BYTES = 0;
+};
+
+// NT threads per CTA; STAB: the micro-block table is staged in shared memory once
+// per CTA (persistent CTAs), else read through L1.
+template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0, int NT = kPackedThreads,
+          bool STAB = false>
+__global__ void __launch_bounds__(NT)
 step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                    const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t mb = smem_u32(sm);  // two mbarriers at [0, 16)
-    uint8_t* st = sm + 16;
+    constexpr uint32_t TABB = STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0u;
+    const uint32_t* tab = STAB ? reinterpret_cast<const uint32_t*>(sm + 16) : p.btab;
+    uint8_t* st = sm + 16 + TABB;
     const uint32_t stage_bytes = p.SW * 4;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NWARPS = kPackedThreads / 32;
+    const int tid = threadIdx.x;
+    if constexpr (STAB) {
+        for (uint32_t i = tid; i < TABB / 16; i += NT)
+            reinterpret_cast<uint4*>(sm + 16)[i] = __ldg(reinterpret_cast<const uint4*>(p.btab) + i);
+    }
 
     uint32_t KB[9], KS[9];
 #pragma unroll
@@ -179,67 +238,41 @@ step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, u
         mbar_init(mb + 8, 1);
         mbar_fence_init();
     }
-    if (tid < 2) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nH] = 0u;  // absent
+    if (tid < 2) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
     __syncthreads();
 
-    const uint32_t rec_bytes = p.Cp * 4;
+    const uint32_t rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
+    // group record + its halo words into stage s (one mbarrier, two bulk copies)
+    auto load_group = [&](uint32_t gg, int s) {
+        const uint32_t bar = mb + 8 * s;
+        const uint32_t dst_s = smem_u32(st + s * stage_bytes);
+        mbar_expect_tx(bar, rec_bytes + halo_bytes);
+        bulk_g2s(dst_s, src + (uint64_t)gg * p.Cp, rec_bytes, bar);
+        if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)gg * p.nHp, halo_bytes, bar);
+    };
     uint32_t g = p.g0 + blockIdx.x;
-    if (tid == 0 && g < p.g1) {
-        mbar_expect_tx(mb, rec_bytes);
-        bulk_g2s(smem_u32(st), src + (uint64_t)g * p.Cp, rec_bytes, mb);
-    }
+    if (tid == 0 && g < p.g1) load_group(g, 0);
     uint32_t phase = 0;
     for (int s = 0; g < p.g1; g += gridDim.x, s ^= 1) {
         const uint32_t gn = g + gridDim.x;
-        if (tid == 0 && gn < p.g1) {  // stage s^1 was released by the last __syncthreads
-            mbar_expect_tx(mb + 8 * (s ^ 1), rec_bytes);
-            bulk_g2s(smem_u32(st + (s ^ 1) * stage_bytes), src + (uint64_t)gn * p.Cp, rec_bytes, mb + 8 * (s ^ 1));
-        }
-        uint8_t* Sb = st + s * stage_bytes;
-        uint32_t* S = reinterpret_cast<uint32_t*>(Sb);
-        // ---- halo words: warp w gathers slots w, w + 8, ... from the boundary plane
-        const uint32_t t = g * 32 + lane;
-        for (uint32_t jb = warp; jb < p.nH; jb += NWARPS * 4) {
-            uint32_t t2[4], sl[4], v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = jb + NWARPS * u;
-                t2[u] = kNoTile;
-                sl[u] = 0;
-                if (j < p.nH) {
-                    sl[u] = __ldg(p.slot + j);
-                    if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                v[u] = t2[u] != kNoTile
-                           ? (__ldg(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
-                           : 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = jb + NWARPS * u;
-                const uint32_t word = __ballot_sync(0xFFFFFFFFu, v[u] != 0);
-                if (lane == 0 && j < p.nH) S[p.Cp + j] = word;
-            }
-        }
-        mbar_wait(mb + 8 * s, (phase >> s) & 1u);
+        if (tid == 0 && gn < p.g1) load_group(gn, s ^ 1);  // stage s^1 released by the last __syncthreads
+        const uint8_t* Sb = st + s * stage_bytes;
+        mbar_wait(mb + 8 * s, (phase >> s) & 1u);  // record + halo words landed (TMA)
         phase ^= 1u << s;
-        __syncthreads();
         // ---- program: every local cell, straight to HBM -------------------------------
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
         uint32_t* D = dst + (uint64_t)g * p.Cp;
         if constexpr (std::is_void<FT>::value) {
 #pragma unroll 2
-            for (uint32_t i = tid; i < p.C; i += kPackedThreads)
+            for (uint32_t i = tid; i < p.C; i += NT)
                 D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
         } else {
-            constexpr uint32_t NBLK = (WQ / Wiring<FT, P>::BW) * (WQ / Wiring<FT, P>::BH);
-            for (uint32_t blk = tid; blk < NBLK; blk += kPackedThreads)
-                block_words<FT, P, WQ, CONWAY, DEG>(Sb, p.btab, blk, D, vmask, KB, KS);
+            constexpr uint32_t NBLK = BlockGeom<FT, P, WQ>::NBLK;
+            for (uint32_t blk = tid; blk < NBLK; blk += NT)
+                block_words<FT, P, WQ, CONWAY, DEG, STAB>(Sb, tab, blk, D, vmask, KB, KS);
         }
         // boundary plane of the new state (a few words per group: recomputed)
-        for (uint32_t m = tid; m < p.nSrc; m += kPackedThreads)
+        for (uint32_t m = tid; m < p.nSrc; m += NT)
             bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
         __syncthreads();
     }
@@ -264,6 +297,88 @@ __global__ void build_ntab_linear_kernel(Frac f, int L, uint32_t Wc, uint32_t Hc
             if (coarse_neighbor<K, S>(f, L, X, Y, D % 3 - 1, D / 3 - 1, X2, Y2)) v = Y2 * Wc + X2;
             out[(uint64_t)ds * n + i] = v;
         }
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+// Warp-specialised persistent variant of the micro-block step (one CTA per SM):
+// a producer warp streams group records + halo words into an NS-stage ring with
+// cp.async.bulk (full barriers carry the transaction bytes); NCW consumer warps
+// each take 32-block chunks of every group and release a stage through its empty
+// barrier -- no CTA-wide barrier in the loop, so warps drift up to NS-1 groups
+// apart instead of waiting for the slowest one.  The micro-block table is staged in
+// shared memory once (STAB) or read through L1.
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NCW, int NS, bool STAB>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+step_packed_ws_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                      const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
+    (void)bsrc;
+    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
+    constexpr int NCHUNK = (NBLK + 31) / 32;
+    constexpr uint32_t TABB = STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0u;
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
+    const uint32_t* tab = STAB ? reinterpret_cast<const uint32_t*>(sm + 16 * NS) : p.btab;
+    uint8_t* st = sm + 16 * NS + TABB;
+    const uint32_t stage_bytes = p.SW * 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, NCW);
+        }
+        mbar_fence_init();
+    }
+    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
+    if constexpr (STAB) {
+        for (uint32_t i = tid; i < TABB / 16; i += (NCW + 1) * 32)
+            reinterpret_cast<uint4*>(sm + 16 * NS)[i] = __ldg(reinterpret_cast<const uint4*>(p.btab) + i);
+    }
+    __syncthreads();
+
+    const uint32_t rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
+    if (warp == NCW) {  // ---- producer -------------------------------------------------
+        if (lane == 0) {
+            uint32_t i = 0;
+            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+                const uint32_t s = i % NS;
+                if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
+                const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
+                mbar_expect_tx(bar, rec_bytes + halo_bytes);
+                bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
+                if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
+            }
+        }
+        return;
+    }
+    // ---- consumers -----------------------------------------------------------------
+    uint32_t i = 0;
+    for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+        const uint32_t s = i % NS;
+        mbar_wait(full0 + 8 * s, (i / NS) & 1u);
+        const uint8_t* Sb = st + s * stage_bytes;
+        const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+        uint32_t* D = dst + (uint64_t)g * p.Cp;
+        // chunk c of this group -> warp (c + i) mod NCW: the odd chunks rotate
+        for (int c = (int)((warp + NCW - (i % NCW)) % NCW); c < NCHUNK; c += NCW) {
+            const uint32_t blk = (uint32_t)c * 32 + lane;
+            if (blk < (uint32_t)NBLK) block_words<FT, P, WQ, CONWAY, DEG, STAB>(Sb, tab, blk, D, vmask, KB, KS);
+        }
+        if ((uint32_t)warp == i % NCW)  // boundary plane of the new state
+            for (uint32_t m = lane; m < p.nSrc; m += 32)
+                bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * s);
     }
 }
 
