@@ -899,6 +899,24 @@ void launch_packed_ws_t(nbbgpu_t h, const PackedStepParams& p) {
     kern<<<(unsigned)blocks, (NCW + 1) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
+void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
+    auto kern = step_packed_ws3_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO>;
+    constexpr int NCHUNK = (BlockGeom<FT, P, WQ>::NBLK + 31) / 32;
+    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * p.Cp * 4;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: stage rings exceed shared memory");
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const uint64_t groups = p.g1 - p.g0;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)sms));
+    kern<<<(unsigned)blocks, (NCHUNK * NGRP + 2) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur ^ 1]);
+}
+
 void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const PackedPlan& P = h->pp;
     PackedStepParams p{};
@@ -941,7 +959,16 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
         if (tri_cfg == 1) { NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 256, false) }
         if (tri_cfg == 2) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 31, 4, true) }
         if (tri_cfg == 3) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 6, false) }
-        if (tri_cfg == 0) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 4, true) }
+        if (tri_cfg == 4) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 4, true) }
+#define NBB_WS3(TAG, FT, BP, W, WD, NGRP, NS, NO)                                                        \
+    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
+        if (conway && dg == 8) return launch_packed_ws3_t<true, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);  \
+        if (conway) return launch_packed_ws3_t<true, 4, WD, FT, BP, W, NGRP, NS, NO>(h, p);             \
+        if (dg == 8) return launch_packed_ws3_t<false, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);           \
+        return launch_packed_ws3_t<false, 4, WD, FT, BP, W, NGRP, NS, NO>(h, p);                        \
+    }
+        if (tri_cfg == 0) { NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 4, 2) }
+        if (tri_cfg == 5) { NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 5, 3) }
         NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 736, true)
         NBB_BK(kTagTriangle, TriangleTag, 2, 27, false, 96, true)
         NBB_BK(kTagCarpet, CarpetTag, 1, 64, false, 512, true)

@@ -382,6 +382,165 @@ step_packed_ws_kernel(const PackedStepParams p, const uint32_t* __restrict__ src
     }
 }
 
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Micro-block step with the external offsets held in registers (toff) and the
+// results written to a shared-memory output record (Do).
+template <class FT, int P, int WQ, bool CONWAY, int DEG>
+__device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t (&toff)[Wiring<FT, P>::NEP],
+                                              uint32_t blk, uint32_t* Do, uint32_t vmask, const uint32_t (&KB)[9],
+                                              const uint32_t (&KS)[9]) {
+    using W = Wiring<FT, P>;
+    constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
+    constexpr int BPR = WQ / BW;
+    const uint32_t by = blk / BPR, bx = blk - by * BPR;
+    const uint32_t base = by * (BH * WQ) + bx * BW;
+    const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
+    uint32_t own[NB], ext[NEP];
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        own[N] = Sw[(N / BW) * WQ + N % BW];
+    });
+    static_for<NEP>([&](auto e) {
+        constexpr int E = decltype(e)::value;
+        ext[E] = *reinterpret_cast<const uint32_t*>(Sb + toff[E]);
+    });
+    uint32_t* Dw = Do + base;
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        uint32_t x[8];
+        static_for<8>([&](auto j) {
+            constexpr int J = decltype(j)::value;
+            constexpr int SJ = W::d.src[N][J];
+            if constexpr (J >= DEG || SJ == kWireAbsent) x[J] = 0u;
+            else if constexpr (SJ >= 0) x[J] = own[SJ];
+            else x[J] = ext[-SJ - 2];
+        });
+        const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+        Dw[(N / BW) * WQ + N % BW] = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
+    });
+}
+
+// Persistent, warp-specialised micro-block step (one CTA per SM), TMA in and out:
+//   producer warp : group record + halo words -> NS-stage input ring (cp.async.bulk,
+//                   full barriers carry the bytes; empty barriers free a stage);
+//   NGRP x NCHUNK consumer warps : warp (k, c) evaluates the 32 micro-blocks of
+//                   chunk c of every group i = k (mod NGRP); its blocks never change,
+//                   so their external offsets live in registers for the whole kernel;
+//                   results go to an NO-deep shared output ring;
+//   storer warp   : one cp.async.bulk shared->global store per finished group.
+// No CTA-wide barrier in the loop; stores leave as whole 26 KB records.
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
+__global__ void __launch_bounds__(((BlockGeom<FT, P, WQ>::NBLK + 31) / 32 * NGRP + 2) * 32, 1)
+step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                       uint32_t* __restrict__ bdst) {
+    using W = Wiring<FT, P>;
+    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
+    constexpr int NCHUNK = (NBLK + 31) / 32;
+    constexpr int NCW = NCHUNK * NGRP;
+    constexpr int NEP = W::NEP;
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
+    const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
+    uint8_t* st = sm + 16 * (NS + NO);
+    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
+    uint8_t* outs = st + NS * stage_bytes;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, NCHUNK);
+        }
+        for (int o = 0; o < NO; ++o) {
+            mbar_init(ofull0 + 8 * o, NCHUNK);
+            mbar_init(oempty0 + 8 * o, 1);
+        }
+        mbar_fence_init();
+    }
+    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
+    for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
+        reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * rec_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    if (warp == NCW) {  // ---- producer -------------------------------------------------
+        if (lane == 0) {
+            uint32_t i = 0;
+            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+                const uint32_t s = i % NS;
+                if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
+                const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
+                mbar_expect_tx(bar, rec_bytes + halo_bytes);
+                bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
+                if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
+            }
+        }
+        return;
+    }
+    if (warp == NCW + 1) {  // ---- storer ---------------------------------------------------
+        if (lane == 0) {
+            uint32_t i = 0;
+            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+                const uint32_t o = i % NO;
+                mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);
+                bulk_s2g(dst + (uint64_t)g * p.Cp, smem_u32(outs + o * rec_bytes), rec_bytes);
+                bulk_wait_read_all();  // the output record may be rewritten
+                mbar_arrive(oempty0 + 8 * o);
+            }
+            bulk_wait_all();
+        }
+        return;
+    }
+    // ---- consumers ---------------------------------------------------------------------
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    const int set = warp / NCHUNK, c = warp - set * NCHUNK;
+    const uint32_t blk = (uint32_t)c * 32 + lane;
+    const bool active = blk < (uint32_t)NBLK;
+    uint32_t toff[NEP];
+    {
+        const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
+        static_for<NEP / 4>([&](auto e4) {
+            constexpr int E = decltype(e4)::value;
+            const uint4 v = __ldg(t4 + E);
+            toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
+        });
+    }
+    uint32_t i = (uint32_t)set;
+    for (uint32_t g = p.g0 + blockIdx.x + (uint32_t)set * gridDim.x; g < p.g1; g += NGRP * gridDim.x, i += NGRP) {
+        const uint32_t s = i % NS, o = i % NO;
+        mbar_wait(full0 + 8 * s, (i / NS) & 1u);
+        if (i >= NO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
+        const uint8_t* Sb = st + s * stage_bytes;
+        uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * rec_bytes);
+        const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+        if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
+        if (c == 0)  // boundary plane of the new state
+            for (uint32_t m = lane; m < p.nSrc; m += 32)
+                bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+        fence_proxy_async_smem();  // the bulk store reads Do through the async proxy
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(empty0 + 8 * s);
+            mbar_arrive(ofull0 + 8 * o);
+        }
+    }
+}
+
 // ---- boundary plane from a packed state ---------------------------------------
 __global__ void bnd_refresh_kernel(const uint32_t* __restrict__ P, uint32_t Cp, uint32_t NG, uint32_t nSrc,
                                    const uint32_t* __restrict__ srcidx, uint32_t* __restrict__ B) {
