@@ -35,6 +35,7 @@ LEVEL = 20
 SEED, DENSITY = 42, 0.5
 BIRTH, SURVIVE = 0x8, 0xC  # B3/S23
 BYTES_PER_UPDATE = 2       # read own state byte + write next-state byte
+PACKED_BYTES_PER_UPDATE = 0.25  # packed model: read own state bit + write next-state bit
 
 
 def peaks():
@@ -212,7 +213,7 @@ def run_ours(args):
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="torch")
         else:
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="torch", host_staging=True)
-        owned = dsim.plan.hi - dsim.plan.lo
+        owned = dsim.owned_cells()
     else:
         owned = cells
 
@@ -239,23 +240,37 @@ def run_ours(args):
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    kernel_ms = 0.0
-    launches = 0
+    n0 = C.c_uint64()
+    _abi.check(L.nbbgpu_launch_count(h, C.byref(n0)))
     t_wall = time.perf_counter()
     ev0.record(ext)
+    # K steps back to back on the engine stream (packed: halo-words kernel + step
+    # kernel per step; N > 1 adds the halo pack / NCCL send-recv / unpack on-stream)
     if ws == 1:
-        # one launch per step, back to back on the engine stream
-        kernel_ms = sim.step_timed(rule, args.steps)
-        launches += args.steps
+        sim.step(rule, args.steps)
+    elif dsim.transport == "nccl":
+        sim.step(rule, args.steps)
     else:
-        # nccl: step kernel + pack + ncclSend/Recv + unpack per step, all on-stream
-        kernel_ms = dsim.step_timed(rule, args.steps)
-        launches += args.steps * (1 + dsim.launches_per_exchange)
+        dsim.step(rule, args.steps)
     ev1.record(ext)
     barrier()
     t_wall = time.perf_counter() - t_wall
     clk = clocks.stop()
     step_ms = ev0.elapsed_time(ev1)
+    n1 = C.c_uint64()
+    _abi.check(L.nbbgpu_launch_count(h, C.byref(n1)))
+    launches = n1.value - n0.value
+    if dsim is not None and dsim.transport != "nccl":
+        launches += args.steps * dsim.launches_per_exchange
+    # second pass of K steps with CUDA events around every main step kernel: its own
+    # average duration for the roofline (per-kernel events add gaps, so the headline
+    # value above is timed without them)
+    barrier()
+    if ws == 1:
+        _, kernel_ms, _ = sim.step_profiled(rule, args.steps)
+    else:
+        _, kernel_ms, _ = dsim.step_profiled(rule, args.steps)
+    barrier()
     if dist is not None:
         tt = torch.tensor([step_ms, kernel_ms], dtype=torch.float64,
                           device=f"cuda:{device}" if args.dist_backend == "nccl" else "cpu")
@@ -276,15 +291,18 @@ def run_ours(args):
         host_in = torch.empty(cells, dtype=torch.uint8).pin_memory()
         host_out = torch.empty(cells, dtype=torch.uint8).pin_memory()
         _abi.check(L.nbbgpu_download(h, C.c_void_p(host_in.data_ptr()), cells))
-        barrier()
-        t0 = time.perf_counter()
-        _abi.check(L.nbbgpu_upload(h, C.c_void_p(host_in.data_ptr()), cells))
-        for _ in range(args.steps):
-            sim.step(rule)
-            exchange()
-        _abi.check(L.nbbgpu_download(h, C.c_void_p(host_out.data_ptr()), cells))
-        barrier()
-        e2e_s = time.perf_counter() - t0
+        reps = []
+        for _ in range(3):  # median of 3 end-to-end runs (host memory behaviour varies)
+            barrier()
+            t0 = time.perf_counter()
+            _abi.check(L.nbbgpu_upload(h, C.c_void_p(host_in.data_ptr()), cells))
+            for _ in range(args.steps):
+                sim.step(rule)
+                exchange()
+            _abi.check(L.nbbgpu_download(h, C.c_void_p(host_out.data_ptr()), cells))
+            barrier()
+            reps.append(time.perf_counter() - t0)
+        e2e_s = sorted(reps)[1]
         if dist is not None:
             tt = torch.tensor([e2e_s], dtype=torch.float64,
                               device=f"cuda:{device}" if args.dist_backend == "nccl" else "cpu")
@@ -292,7 +310,9 @@ def run_ours(args):
             e2e_s = float(tt[0])
         e2e = {"value": cells * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": cells / args.steps, "d2h_bytes_per_step": cells / args.steps,
-               "how": "upload(pinned host state) + K x nbbgpu_step(1) + download(pinned host), wall clock"}
+               "how": ("upload(pinned host state, reference bytes) + K x nbbgpu_step(1) + download(pinned "
+                       "host, reference bytes), wall clock, median of 3; the bytes<->packed conversion "
+                       "runs on the device, pipelined with the DMA copies")}
 
     if rank != 0:
         if dist is not None:
@@ -302,22 +322,35 @@ def run_ours(args):
 
     peak, peak_src = peaks()
     kernel_ms_per_launch = kernel_ms / args.steps
-    achieved = BYTES_PER_UPDATE * owned / (kernel_ms_per_launch / 1e3) / 1e9
+    packed = kern == "packed"
+    # algorithmic bytes per launch: packed layout = read + write 1 bit per owned cell
+    # (SURVEY.md 8d's packed model); byte layouts = 2 B per owned cell
+    bpu = PACKED_BYTES_PER_UPDATE if packed else BYTES_PER_UPDATE
+    achieved = bpu * owned / (kernel_ms_per_launch / 1e3) / 1e9
+    achieved_2b = BYTES_PER_UPDATE * owned / (kernel_ms_per_launch / 1e3) / 1e9
     traffic, ncu = ncu_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32 bit-sliced (1 bit per cell, 32 tiles per word)" if packed else "u8",
         "data": "synthetic: seed_random(42, 0.5) generated on the device (rng.hpp cell_alive)",
         "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore "
                                "(BASELINE.json configs[3]; north-star target)",
                    "level": args.level, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
                    "parallelism": f"partitioned x{n}" if n > 1 else "single GPU",
-                   "l2": "state 6.97 GB >> 126 MB L2: inputs larger than L2, no flush"},
+                   "state_bytes_per_buffer": (cells + 7) // 8 if packed else cells,
+                   "l2": (f"state {((cells + 7) // 8 if packed else cells) / 1e9:.2f} GB per buffer vs 126 MB L2: "
+                          "inputs larger than L2, no flush")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "model": "2 B per compact cell-update (SURVEY.md 8d) x owned cells per launch",
-                     "peak_source": peak_src, "kernel_ms_per_launch": kernel_ms_per_launch},
+                     "model": ("packed: 2 bits (read own + write next state, 1 bit each) per compact "
+                               "cell-update x owned cells per launch (SURVEY.md 8d packed model)" if packed else
+                               "2 B per compact cell-update (SURVEY.md 8d) x owned cells per launch"),
+                     "peak_source": peak_src, "kernel_ms_per_launch": kernel_ms_per_launch,
+                     "model_2B": {"achieved": achieved_2b, "frac": achieved_2b / peak,
+                                  "note": "the reference's 1 byte per cell (grid.hpp:15); > 1 means the "
+                                          "packed layout moves fewer bytes than the byte model assumes"}},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,

@@ -91,6 +91,17 @@ int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t
 int nbbgpu_step_timed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
                       float* device_ms);
 
+/* nbbgpu_step_timed plus: the summed device time of the main step kernels alone
+ * (CUDA events around each of them, on the handle's stream) and the number of
+ * engine kernels launched (step, halo-words and halo pack/unpack kernels; NCCL's
+ * own kernels not counted). */
+int nbbgpu_step_profiled(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
+                         float* total_ms, float* main_kernel_ms, uint64_t* launches);
+
+/* Engine kernels launched by step calls on this handle so far (as counted by
+ * nbbgpu_step_profiled). */
+int nbbgpu_launch_count(nbbgpu_t h, uint64_t* out);
+
 /* Simulation::state_hash (stencil.cpp:196-234): wrapping uint64 sum of
  * coord_mix(x, y) over alive cells. */
 int nbbgpu_state_hash(nbbgpu_t h, uint64_t* out);

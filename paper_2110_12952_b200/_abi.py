@@ -26,6 +26,9 @@ SIGNATURES = {
     "nbbgpu_seed": (C.c_int, [_H, C.c_uint64, C.c_double]),
     "nbbgpu_step": (C.c_int, [_H, C.c_uint16, C.c_uint16, C.c_int, C.c_int64]),
     "nbbgpu_step_timed": (C.c_int, [_H, C.c_uint16, C.c_uint16, C.c_int, C.c_int64, _P(C.c_float)]),
+    "nbbgpu_step_profiled": (C.c_int, [_H, C.c_uint16, C.c_uint16, C.c_int, C.c_int64, _P(C.c_float),
+                                       _P(C.c_float), _P(C.c_uint64)]),
+    "nbbgpu_launch_count": (C.c_int, [_H, _P(C.c_uint64)]),
     "nbbgpu_state_hash": (C.c_int, [_H, _P(C.c_uint64)]),
     "nbbgpu_iteration": (C.c_int, [_H, _P(C.c_int64)]),
     "nbbgpu_stored_cells": (C.c_int, [_H, _P(C.c_uint64)]),

@@ -546,6 +546,10 @@ struct nbbgpu_sim {
     uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
+    // profiling (nbbgpu_step_profiled): events around each main step kernel, launch count
+    std::vector<cudaEvent_t>* prof = nullptr;  // pre-created pool
+    size_t prof_idx = 0;
+    uint64_t launches = 0;
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -636,6 +640,12 @@ int resolve_kernel_for(nbbgpu_t h, int kernel) {
     return NBBGPU_KERNEL_NAIVE;
 }
 int resolve_kernel(nbbgpu_t h) { return resolve_kernel_for(h, h->kernel); }
+
+// event pair around the main step kernel when profiling (nbbgpu_step_profiled)
+void prof_mark(nbbgpu_t h) {
+    if (!h->prof || h->prof_idx >= h->prof->size()) return;
+    CK(cudaEventRecord((*h->prof)[h->prof_idx++], h->stream));
+}
 int layout_of_kernel(int k) { return k == NBBGPU_KERNEL_PACKED ? 1 : 0; }
 
 // ---------------------------------------------------------------------------
@@ -763,70 +773,128 @@ void bnd_refresh(nbbgpu_t h) {
 }
 
 // coarse rows per staging chunk for byte <-> packed conversions (bounded device memory)
-// (NBBGPU_STAGE_BYTES overrides the 256 MB default; the tests force many chunks)
+// (NBBGPU_STAGE_BYTES overrides the 64 MB default; the tests force many chunks)
 int64_t chunk_rows(nbbgpu_t h) {
-    uint64_t stage = 256ull << 20;
+    uint64_t stage = 64ull << 20;
     if (const char* e = getenv("NBBGPU_STAGE_BYTES")) stage = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
     const uint64_t row_bytes = (uint64_t)h->pp.wq * (uint64_t)h->hf.w;
     return (int64_t)std::max<uint64_t>(1, stage / std::max<uint64_t>(1, row_bytes));
 }
 
-// bytes (host or device, reference layout) -> packed buffer dstP.  Returns false if
-// a byte > 1 was seen (dstP then holds garbage; callers restore).
+// device memory is converted in place; host memory (pinned or pageable) streams
+// through two staging chunks: DMA copies on a second stream overlap the
+// conversion kernels on the engine stream (PCIe-bound, ~55 GB/s pinned)
+bool is_device_mem(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct StagePipe {
+    nbbgpu_t h;
+    cudaStream_t xs = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    uint8_t* buf[2] = {nullptr, nullptr};
+    explicit StagePipe(nbbgpu_t hh, uint64_t bytes) : h(hh) {
+        CK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+            dmalloc_cap(buf[i], bytes, "staging buffer");
+        }
+    }
+    ~StagePipe() {
+        if (xs) cudaStreamSynchronize(xs);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        for (int i = 0; i < 2; ++i) {
+            if (buf[i]) cudaFree(buf[i]);
+            if (ready[i]) cudaEventDestroy(ready[i]);
+            if (done[i]) cudaEventDestroy(done[i]);
+        }
+        if (xs) cudaStreamDestroy(xs);
+    }
+};
+
+size_t conv_smem(nbbgpu_t h) { return (size_t)kConvWarps * 32 * h->pp.wq; }
+
+void launch_pack(nbbgpu_t h, const uint8_t* chunk, int64_t Y0, int64_t Y1, uint32_t* dstP) {
+    const PackedPlan& P = h->pp;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        CK(cudaFuncSetAttribute(unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((warps + kConvWarps - 1) / kConvWarps, 148ull * 16));
+    pack_kernel<<<blocks, kConvWarps * 32, conv_smem(h), h->stream>>>(packed_geom(h), chunk, (uint32_t)Y0, (uint32_t)Y1, dstP, h->d_flag);
+    CK(cudaGetLastError());
+}
+
+void launch_unpack(nbbgpu_t h, const uint32_t* srcP, int64_t Y0, int64_t Y1, uint8_t* chunk) {
+    const PackedPlan& P = h->pp;
+    const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((warps + kConvWarps - 1) / kConvWarps, 148ull * 16));
+    unpack_kernel<<<blocks, kConvWarps * 32, conv_smem(h), h->stream>>>(packed_geom(h), srcP, (uint32_t)Y0, (uint32_t)Y1, chunk);
+    CK(cudaGetLastError());
+}
+
+// bytes (reference layout; device or host) -> packed buffer dstP.  Returns false
+// if a byte > 1 was seen (dstP then holds garbage; callers restore).
 bool packed_from_bytes(nbbgpu_t h, const uint8_t* src, uint32_t* dstP) {
     const PackedPlan& P = h->pp;
-    const PackedGeom G = packed_geom(h);
     CK(cudaMemsetAsync(dstP, 0, packed_words(P) * 4, h->stream));
     CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
-    const int64_t cr = chunk_rows(h);
-    const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
-    const bool dev = is_device_ptr(src);
-    uint8_t* stage = nullptr;
-    if (!dev) dmalloc_cap(stage, std::min<uint64_t>(h->cells, cr * row_bytes), "staging buffer");
-    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr) {
-        const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
-        const uint64_t nb = (uint64_t)(Y1 - Y0) * row_bytes;
-        const uint8_t* chunk = src + (uint64_t)Y0 * row_bytes;
-        if (!dev) {
-            CK(cudaMemcpyAsync(stage, chunk, nb, cudaMemcpyDefault, h->stream));
-            chunk = stage;
+    if (is_device_mem(src)) {
+        launch_pack(h, src, 0, P.Hc, dstP);
+    } else {
+        const int64_t cr = chunk_rows(h);
+        const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
+        StagePipe sp(h, std::min<uint64_t>(h->cells, cr * row_bytes));
+        int k = 0;
+        for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr, k ^= 1) {
+            const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
+            CK(cudaStreamWaitEvent(sp.xs, sp.done[k], 0));  // previous pack of this buffer finished
+            CK(cudaMemcpyAsync(sp.buf[k], src + (uint64_t)Y0 * row_bytes, (uint64_t)(Y1 - Y0) * row_bytes,
+                               cudaMemcpyHostToDevice, sp.xs));
+            CK(cudaEventRecord(sp.ready[k], sp.xs));
+            CK(cudaStreamWaitEvent(h->stream, sp.ready[k], 0));
+            launch_pack(h, sp.buf[k], Y0, Y1, dstP);
+            CK(cudaEventRecord(sp.done[k], h->stream));
         }
-        check_binary_kernel<<<grid_for(nb, 256), 256, 0, h->stream>>>(chunk, nb, h->d_flag);
-        const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
-        pack_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, chunk, (uint32_t)Y0, (uint32_t)Y1, dstP);
-        CK(cudaGetLastError());
-        if (!dev) CK(cudaStreamSynchronize(h->stream));  // stage reuse
     }
     int flag = 0;
     CK(cudaMemcpyAsync(&flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    if (stage) cudaFree(stage);
     return flag == 0;
 }
 
-// packed buffer srcP -> bytes (host or device, reference layout)
+// packed buffer srcP -> bytes (reference layout; device or host)
 void packed_to_bytes(nbbgpu_t h, const uint32_t* srcP, uint8_t* dst) {
     const PackedPlan& P = h->pp;
-    const PackedGeom G = packed_geom(h);
+    if (is_device_mem(dst)) {
+        launch_unpack(h, srcP, 0, P.Hc, dst);
+        CK(cudaStreamSynchronize(h->stream));
+        return;
+    }
     const int64_t cr = chunk_rows(h);
     const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
-    const bool dev = is_device_ptr(dst);
-    uint8_t* stage = nullptr;
-    if (!dev) dmalloc_cap(stage, std::min<uint64_t>(h->cells, cr * row_bytes), "staging buffer");
-    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr) {
+    StagePipe sp(h, std::min<uint64_t>(h->cells, cr * row_bytes));
+    int k = 0;
+    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr, k ^= 1) {
         const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
-        const uint64_t nb = (uint64_t)(Y1 - Y0) * row_bytes;
-        uint8_t* chunk = dev ? dst + (uint64_t)Y0 * row_bytes : stage;
-        const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
-        unpack_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(G, srcP, (uint32_t)Y0, (uint32_t)Y1, chunk);
-        CK(cudaGetLastError());
-        if (!dev) {
-            CK(cudaMemcpyAsync(dst + (uint64_t)Y0 * row_bytes, stage, nb, cudaMemcpyDefault, h->stream));
-            CK(cudaStreamSynchronize(h->stream));
-        }
+        CK(cudaStreamWaitEvent(h->stream, sp.done[k], 0));  // previous copy-out of this buffer finished
+        launch_unpack(h, srcP, Y0, Y1, sp.buf[k]);
+        CK(cudaEventRecord(sp.ready[k], h->stream));
+        CK(cudaStreamWaitEvent(sp.xs, sp.ready[k], 0));
+        CK(cudaMemcpyAsync(dst + (uint64_t)Y0 * row_bytes, sp.buf[k], (uint64_t)(Y1 - Y0) * row_bytes,
+                           cudaMemcpyDeviceToHost, sp.xs));
+        CK(cudaEventRecord(sp.done[k], sp.xs));
     }
-    CK(cudaStreamSynchronize(h->stream));
-    if (stage) cudaFree(stage);
+    CK(cudaStreamSynchronize(sp.xs));
 }
 
 // switch the state layout, converting the front state on the device
@@ -863,11 +931,11 @@ void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t&
     bit = (uint32_t)(t % 32);
 }
 
-template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0, int NT = kPackedThreads,
-          bool STAB = false>
+template <bool CONWAY, int DEG, bool WIDE>
 void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NT, STAB>;
-    const size_t smem = 16 + (STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0) + 2 * (size_t)p.SW * 4;
+    constexpr int NT = kPackedThreads;
+    auto kern = step_packed_kernel<CONWAY, DEG, WIDE>;
+    const size_t smem = 16 + 2 * (size_t)p.SW * 4;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -910,11 +978,12 @@ void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
         attr_set = true;
     }
     if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: stage rings exceed shared memory");
-    int sms = 148;
+    int sms = 148, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCHUNK * NGRP + 2) * 32, smem));
     const uint64_t groups = p.g1 - p.g0;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)sms));
-    kern<<<(unsigned)blocks, (NCHUNK * NGRP + 2) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur ^ 1]);
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
+    kern<<<(unsigned)blocks, (NCHUNK * NGRP + 2) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
 void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
@@ -930,25 +999,22 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     p.nbr = h->d_pnbr[moore];
     p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc; p.btab = h->d_pbtab;
     if (p.g1 <= p.g0) return;
-    // halo words of every owned group from the boundary plane, then the step
+    // halo words of every owned group from the boundary plane (separate kernel);
+    // the step kernel bulk-loads them with each group record
     if (P.nH > 0) {
         const uint64_t warps = (uint64_t)(p.g1 - p.g0) * (uint64_t)((P.nH + 3) / 4);
         halo_words_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
         CK(cudaGetLastError());
+        ++h->launches;
     }
+    ++h->launches;  // the step kernel below
+    prof_mark(h);
+    struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
     if (P.tag != kTagNone) {
         const int dg = moore ? 8 : 4;
-    // NT threads: one micro-block per thread per group where it fits a CTA; the
-    // block table in shared memory where it fits next to the two stages
-#define NBB_BK(TAG, FT, BP, W, WD, NTH, ST)                                                             \
-    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
-        if (conway && dg == 8) return launch_packed_t<true, 8, WD, FT, BP, W, NTH, ST>(h, p);           \
-        if (conway) return launch_packed_t<true, 4, WD, FT, BP, W, NTH, ST>(h, p);                      \
-        if (dg == 8) return launch_packed_t<false, 8, WD, FT, BP, W, NTH, ST>(h, p);                    \
-        return launch_packed_t<false, 4, WD, FT, BP, W, NTH, ST>(h, p);                                 \
-    }
-        static const int tri_cfg = getenv("NBBGPU_TRI_CFG") ? atoi(getenv("NBBGPU_TRI_CFG")) : 0;  // tuning knob
+    // Micro-block kernels: the persistent TMA-in/TMA-out warp-specialised kernel
+    // (ws3) where a group's chunks fit one CTA, else the chunk-rotating ws kernel.
 #define NBB_WS(TAG, FT, BP, W, WD, NCW, NS, ST)                                                         \
     if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
         if (conway && dg == 8) return launch_packed_ws_t<true, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);    \
@@ -956,10 +1022,6 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
         if (dg == 8) return launch_packed_ws_t<false, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);             \
         return launch_packed_ws_t<false, 4, WD, FT, BP, W, NCW, NS, ST>(h, p);                          \
     }
-        if (tri_cfg == 1) { NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 256, false) }
-        if (tri_cfg == 2) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 31, 4, true) }
-        if (tri_cfg == 3) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 6, false) }
-        if (tri_cfg == 4) { NBB_WS(kTagTriangle, TriangleTag, 2, 81, false, 23, 4, true) }
 #define NBB_WS3(TAG, FT, BP, W, WD, NGRP, NS, NO)                                                        \
     if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
         if (conway && dg == 8) return launch_packed_ws3_t<true, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);  \
@@ -967,15 +1029,14 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
         if (dg == 8) return launch_packed_ws3_t<false, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);           \
         return launch_packed_ws3_t<false, 4, WD, FT, BP, W, NGRP, NS, NO>(h, p);                        \
     }
-        if (tri_cfg == 0) { NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 4, 2) }
-        if (tri_cfg == 5) { NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 5, 3) }
-        NBB_BK(kTagTriangle, TriangleTag, 2, 81, false, 736, true)
-        NBB_BK(kTagTriangle, TriangleTag, 2, 27, false, 96, true)
-        NBB_BK(kTagCarpet, CarpetTag, 1, 64, false, 512, true)
-        NBB_BK(kTagVicsek, VicsekTag, 2, 25, false, 32, true)
-        NBB_BK(kTagH, HTag, 1, 49, false, 352, true)
-        NBB_BK(kTagCandy, CandyTag, 1, 144, true, 864, false)
-#undef NBB_BK
+        NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 4, 2)
+        NBB_WS3(kTagTriangle, TriangleTag, 2, 27, false, 8, 16, 8)
+        NBB_WS3(kTagCarpet, CarpetTag, 1, 64, false, 1, 4, 2)
+        NBB_WS3(kTagVicsek, VicsekTag, 2, 25, false, 16, 24, 16)
+        NBB_WS3(kTagH, HTag, 1, 49, false, 2, 6, 4)
+        NBB_WS(kTagCandy, CandyTag, 1, 144, true, 27, 2, false)
+#undef NBB_WS
+#undef NBB_WS3
         raise(NBBGPU_ERR_CUDA, "internal: micro-block plan without a kernel");
     }
 #define NBB_PK(CW, DG, WD) if (conway == CW && (moore ? 8 : 4) == DG && P.wide == WD) return launch_packed_t<CW, DG, WD>(h, p)
@@ -1042,6 +1103,9 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const uint8_t* src = h->front();
     uint8_t* dst = h->back();
     if (h->mode == NBBGPU_MODE_BB) {
+        ++h->launches;
+        prof_mark(h);
+        struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
         const uint64_t n = (uint64_t)h->hf.side * h->hf.side;
         const int s = h->hf.s;
         if ((s == 2 || s == 4) && h->hf.side % 16 == 0 && h->kernel != NBBGPU_KERNEL_NAIVE) {
@@ -1087,6 +1151,9 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
         launch_step_packed(h, birth, survive, moore);
         return;
     }
+    ++h->launches;  // one kernel per step on the byte layouts
+    prof_mark(h);
+    struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
     if (kern == NBBGPU_KERNEL_NAIVE) {
         uint64_t lo, hi;
         owned_range(h, lo, hi);
@@ -1395,24 +1462,65 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
 }
 
 static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
-                      float* ms) {
+                      float* ms, float* main_ms = nullptr, uint64_t* launches = nullptr) {
     check_handle(h);
     if (nsteps < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "steps must be >= 0");
     moore = moore ? 1 : 0;
     const int rk = resolve_kernel(h);
     if (layout_of_kernel(rk) != h->layout) raise(NBBGPU_ERR_CUDA, "internal: state layout does not match the kernel");
     if (rk == NBBGPU_KERNEL_TILED) ensure_plan(h, moore);
-    CK(cudaEventRecord(h->ev0, h->stream));
-    for (int64_t i = 0; i < nsteps; ++i) {
-        launch_step(h, birth, survive, moore);
-        h->cur ^= 1;
-        ++h->iteration;
-        if (h->comm) exchange_on_stream(h);  // halo bytes of the new front, on-stream
+    std::vector<cudaEvent_t> prof;
+    if (main_ms) {
+        prof.resize((size_t)nsteps * 2);
+        for (auto& e : prof) CK(cudaEventCreate(&e));
+        h->prof = &prof;
+        h->prof_idx = 0;
     }
+    const uint64_t l0 = h->launches;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    try {
+        for (int64_t i = 0; i < nsteps; ++i) {
+            launch_step(h, birth, survive, moore);
+            h->cur ^= 1;
+            ++h->iteration;
+            if (h->comm) exchange_on_stream(h);  // halo of the new front, on-stream
+        }
+    } catch (...) {
+        h->prof = nullptr;
+        for (auto e : prof) cudaEventDestroy(e);
+        throw;
+    }
+    h->prof = nullptr;
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+    if (main_ms) {
+        float acc = 0.f;
+        for (size_t i = 0; i + 1 < h->prof_idx; i += 2) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, prof[i], prof[i + 1]));
+            acc += t;
+        }
+        *main_ms = acc;
+    }
+    for (auto e : prof) cudaEventDestroy(e);
+    if (launches) *launches = h->launches - l0;
+}
+
+int nbbgpu_launch_count(nbbgpu_t h, uint64_t* out) {
+    return guarded([&] {
+        if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
+        *out = h->launches;
+    });
+}
+
+int nbbgpu_step_profiled(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
+                         float* total_ms, float* main_kernel_ms, uint64_t* launches) {
+    return guarded([&] {
+        float dummy = 0.f;
+        step_impl(h, birth, survive, moore, nsteps, total_ms, main_kernel_ms ? main_kernel_ms : &dummy, launches);
+    });
 }
 
 int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps) {

@@ -191,12 +191,10 @@ __device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* b
     });
 }
 
-// One step over the owned groups.  Per CTA a 2-stage ring: the record of the next
-// group is in flight (one cp.async.bulk, mbarrier completion) while the halo words
-// of the current one are gathered from the boundary plane and its C words are
-// computed; results go straight to HBM with coalesced 32-bit stores.  FT = void:
-// generic table-driven program (cell_word); else the micro-block program of the
-// compile-time descriptor FT at block level P and tile width WQ.
+// One step over the owned groups.  Per CTA a 2-stage ring: the record + halo words
+// of the next group are in flight (cp.async.bulk, mbarrier completion) while the C
+// words of the current one are computed; results go straight to HBM with
+// coalesced 32-bit stores.
 template <class FT, int P, int WQ>
 struct BlockGeom {
     static constexpr int NBLK = (WQ / Wiring<FT, P>::BW) * (WQ / Wiring<FT, P>::BH);
@@ -208,24 +206,17 @@ struct BlockGeom<void, P, WQ> {
     static constexpr uint32_t TAB_BYTES = 0;
 };
 
-// NT threads per CTA; STAB: the micro-block table is staged in shared memory once
-// per CTA (persistent CTAs), else read through L1.
-template <bool CONWAY, int DEG, bool WIDE, class FT = void, int P = 0, int WQ = 0, int NT = kPackedThreads,
-          bool STAB = false>
-__global__ void __launch_bounds__(NT)
+// Generic (table-driven) program: any descriptor, any tile level.
+template <bool CONWAY, int DEG, bool WIDE>
+__global__ void __launch_bounds__(kPackedThreads)
 step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                    const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t mb = smem_u32(sm);  // two mbarriers at [0, 16)
-    constexpr uint32_t TABB = STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0u;
-    const uint32_t* tab = STAB ? reinterpret_cast<const uint32_t*>(sm + 16) : p.btab;
-    uint8_t* st = sm + 16 + TABB;
+    constexpr int NT = kPackedThreads;
+    uint8_t* st = sm + 16;
     const uint32_t stage_bytes = p.SW * 4;
     const int tid = threadIdx.x;
-    if constexpr (STAB) {
-        for (uint32_t i = tid; i < TABB / 16; i += NT)
-            reinterpret_cast<uint4*>(sm + 16)[i] = __ldg(reinterpret_cast<const uint4*>(p.btab) + i);
-    }
 
     uint32_t KB[9], KS[9];
 #pragma unroll
@@ -262,15 +253,9 @@ step_packed_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, u
         // ---- program: every local cell, straight to HBM -------------------------------
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
         uint32_t* D = dst + (uint64_t)g * p.Cp;
-        if constexpr (std::is_void<FT>::value) {
 #pragma unroll 2
-            for (uint32_t i = tid; i < p.C; i += NT)
-                D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
-        } else {
-            constexpr uint32_t NBLK = BlockGeom<FT, P, WQ>::NBLK;
-            for (uint32_t blk = tid; blk < NBLK; blk += NT)
-                block_words<FT, P, WQ, CONWAY, DEG, STAB>(Sb, tab, blk, D, vmask, KB, KS);
-        }
+        for (uint32_t i = tid; i < p.C; i += NT)
+            D[i] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, i, KB, KS) & vmask;
         // boundary plane of the new state (a few words per group: recomputed)
         for (uint32_t m = tid; m < p.nSrc; m += NT)
             bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
@@ -431,8 +416,9 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
 }
 
 // Persistent, warp-specialised micro-block step (one CTA per SM), TMA in and out:
-//   producer warp : group record + halo words -> NS-stage input ring (cp.async.bulk,
-//                   full barriers carry the bytes; empty barriers free a stage);
+//   producer warp : group record + its halo words (halo_words_kernel output) ->
+//                   NS-stage input ring (cp.async.bulk, full barriers carry the
+//                   bytes; empty barriers free a stage);
 //   NGRP x NCHUNK consumer warps : warp (k, c) evaluates the 32 micro-blocks of
 //                   chunk c of every group i = k (mod NGRP); its blocks never change,
 //                   so their external offsets live in registers for the whole kernel;
@@ -442,7 +428,7 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
 template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
 __global__ void __launch_bounds__(((BlockGeom<FT, P, WQ>::NBLK + 31) / 32 * NGRP + 2) * 32, 1)
 step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                       uint32_t* __restrict__ bdst) {
+                       const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
     using W = Wiring<FT, P>;
     constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
     constexpr int NCHUNK = (NBLK + 31) / 32;
@@ -452,7 +438,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
     uint8_t* st = sm + 16 * (NS + NO);
-    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
+    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4;
     uint8_t* outs = st + NS * stage_bytes;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -480,6 +466,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 const uint32_t s = i % NS;
                 if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
                 const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
+                const uint32_t halo_bytes = p.nHp * 4;
                 mbar_expect_tx(bar, rec_bytes + halo_bytes);
                 bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
                 if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
@@ -640,68 +627,123 @@ __global__ void hash_packed_kernel(PackedGeom G, const uint32_t* __restrict__ lo
     block_sum_atomic(acc, out);
 }
 
-// Reference bytes -> packed, for the tiles [tlo, thi) (coarse rows [Y0, Y1)).
-// `bytes` holds compact rows starting at compact row Y0 * WQ.  Warp per (group,
-// local row a): lane b reads tile b's row bytes, ballots give the words.
-__global__ void pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32_t Y1,
-                            uint32_t* __restrict__ P) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t tlo = Y0 * G.Wc, thi = Y1 * G.Wc;
-    const uint32_t glo = tlo / 32, ghi = (thi + 31) / 32;
-    const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
-    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
-         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
-        const uint32_t t = g * 32 + lane;
-        const bool tv = t >= tlo && t < thi && t < G.T;
-        const uint32_t lanes = __ballot_sync(0xFFFFFFFFu, tv);
-        uint64_t base = 0;
-        if (tv) {
-            const uint32_t X = t % G.Wc, Y = t / G.Wc;
-            base = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+// ---- reference bytes <-> packed -----------------------------------------------
+// Warp per (group, local row a).  Row a of the group's 32 tiles is at most two
+// contiguous byte runs of the reference layout (tiles of one coarse row are
+// adjacent: tile X's row a is bytes [X*WQ, X*WQ + WQ) of compact row Y*WQ + a), so
+// the bytes move with coalesced 4-byte accesses through a per-warp shared buffer
+// of 32 * WQ bytes; the bit transposition happens in shared memory.  `bytes` holds
+// compact rows starting at compact row Y0 * WQ and may be pinned host memory
+// (zero-copy over PCIe) or device memory.
+constexpr int kConvWarps = 4;
+
+// copy n bytes between global g and shared s (both arbitrary alignment), warp-wide;
+// the global side is accessed as aligned 32-bit words wherever possible
+template <bool TO_SHARED>
+__device__ __forceinline__ void warp_copy_run(uint8_t* sbuf, uint8_t* gptr, uint32_t n, uint32_t lane) {
+    const uint32_t head = min(n, (uint32_t)((4 - ((uintptr_t)gptr & 3)) & 3));
+    const uint32_t nw = (n - head) / 4;
+    const uint32_t tail0 = head + nw * 4;
+    if (lane < head) {
+        if (TO_SHARED) sbuf[lane] = gptr[lane]; else gptr[lane] = sbuf[lane];
+    }
+    uint32_t* gw = reinterpret_cast<uint32_t*>(gptr + head);
+    for (uint32_t k = lane; k < nw; k += 32) {
+        uint8_t* sp = sbuf + head + 4 * k;
+        if (TO_SHARED) {
+            const uint32_t v = gw[k];
+            sp[0] = (uint8_t)v; sp[1] = (uint8_t)(v >> 8); sp[2] = (uint8_t)(v >> 16); sp[3] = (uint8_t)(v >> 24);
+        } else {
+            gw[k] = (uint32_t)sp[0] | ((uint32_t)sp[1] << 8) | ((uint32_t)sp[2] << 16) | ((uint32_t)sp[3] << 24);
         }
-        uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
-        for (uint32_t c0 = 0; c0 < G.WQ; c0 += 32) {
-            uint32_t mine = 0;
-            for (uint32_t cc = 0; cc < 32 && c0 + cc < G.WQ; ++cc) {
-                const bool bit = tv && bytes[base + c0 + cc] != 0;
-                const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
-                if (lane == cc) mine = word;
-            }
-            if (c0 + lane < G.WQ) {
-                // groups shared with a neighbouring row chunk keep the other tiles' bits
-                if (lanes == 0xFFFFFFFFu) R[c0 + lane] = mine;
-                else R[c0 + lane] = (R[c0 + lane] & ~lanes) | mine;
-            }
-        }
+    }
+    if (tail0 + lane < n) {
+        if (TO_SHARED) sbuf[tail0 + lane] = gptr[tail0 + lane]; else gptr[tail0 + lane] = sbuf[tail0 + lane];
     }
 }
 
-// Packed -> reference bytes for the tiles of coarse rows [Y0, Y1) (inverse of pack_kernel).
-__global__ void unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_t Y1,
-                              uint8_t* __restrict__ bytes) {
-    const uint32_t lane = threadIdx.x & 31;
+// the (at most two) runs of group g's tiles within [tlo, thi): calls f(first tile,
+// tile count) for each maximal set of valid tiles in one coarse row
+template <class F>
+__device__ __forceinline__ void for_each_run(const PackedGeom& G, uint32_t g, uint32_t tlo, uint32_t thi, F&& f) {
+    uint32_t t = max(g * 32, tlo);
+    const uint32_t tend = min(min(g * 32 + 32, thi), G.T);
+    while (t < tend) {
+        const uint32_t rowend = (t / G.Wc + 1) * G.Wc;
+        const uint32_t e = min(tend, rowend);
+        f(t, e - t);
+        __syncwarp();
+        t = e;
+    }
+}
+
+__global__ void __launch_bounds__(kConvWarps * 32)
+pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32_t Y1, uint32_t* __restrict__ P,
+            int* __restrict__ bad) {
+    extern __shared__ __align__(16) uint8_t conv_sm[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* sb = conv_sm + wib * 32 * G.WQ;
     const uint32_t tlo = Y0 * G.Wc, thi = Y1 * G.Wc;
     const uint32_t glo = tlo / 32, ghi = (thi + 31) / 32;
     const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
-    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
-         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    for (uint64_t wi = blockIdx.x * (uint64_t)kConvWarps + wib; wi < nw; wi += (uint64_t)gridDim.x * kConvWarps) {
         const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
-        const uint32_t t = g * 32 + lane;
-        const bool tv = t >= tlo && t < thi && t < G.T;
-        uint64_t base = 0;
-        if (tv) {
-            const uint32_t X = t % G.Wc, Y = t / G.Wc;
-            base = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+        for (uint32_t k = lane; k < 32 * G.WQ; k += 32) sb[k] = 0;
+        __syncwarp();
+        for_each_run(G, g, tlo, thi, [&](uint32_t t0, uint32_t n) {
+            const uint32_t X = t0 % G.Wc, Y = t0 / G.Wc;
+            const uint64_t off = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+            warp_copy_run<true>(sb + (t0 - g * 32) * G.WQ, const_cast<uint8_t*>(bytes) + off, n * G.WQ, lane);
+        });
+        __syncwarp();
+        uint32_t lanes = 0;  // tiles of this group inside [tlo, thi)
+        {
+            const uint32_t t = g * 32 + lane;
+            lanes = __ballot_sync(0xFFFFFFFFu, t >= tlo && t < thi && t < G.T);
         }
-        const uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
-        for (uint32_t c0 = 0; c0 < G.WQ; c0 += 32) {
-            const uint32_t mine = c0 + lane < G.WQ ? R[c0 + lane] : 0u;
-            for (uint32_t cc = 0; cc < 32 && c0 + cc < G.WQ; ++cc) {
-                const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, cc);
-                if (tv) bytes[base + c0 + cc] = (uint8_t)((word >> lane) & 1u);
+        uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        for (uint32_t c = lane; c < ((G.WQ + 31) & ~31u); c += 32) {
+            uint32_t word = 0, over = 0;
+            if (c < G.WQ) {
+#pragma unroll 8
+                for (uint32_t b = 0; b < 32; ++b) {
+                    const uint32_t v = sb[b * G.WQ + c];
+                    word |= (v != 0 ? 1u : 0u) << b;
+                    over |= v > 1 ? 1u : 0u;
+                }
+                word &= lanes;
+                if (over) *bad = 1;
+                // groups shared with a neighbouring row chunk keep the other tiles' bits
+                R[c] = lanes == 0xFFFFFFFFu ? word : ((R[c] & ~lanes) | word);
             }
         }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kConvWarps * 32)
+unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_t Y1, uint8_t* __restrict__ bytes) {
+    extern __shared__ __align__(16) uint8_t conv_sm[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* sb = conv_sm + wib * 32 * G.WQ;
+    const uint32_t tlo = Y0 * G.Wc, thi = Y1 * G.Wc;
+    const uint32_t glo = tlo / 32, ghi = (thi + 31) / 32;
+    const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
+    for (uint64_t wi = blockIdx.x * (uint64_t)kConvWarps + wib; wi < nw; wi += (uint64_t)gridDim.x * kConvWarps) {
+        const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
+        const uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        for (uint32_t c = lane; c < G.WQ; c += 32) {
+            const uint32_t word = R[c];
+#pragma unroll 8
+            for (uint32_t b = 0; b < 32; ++b) sb[b * G.WQ + c] = (uint8_t)((word >> b) & 1u);
+        }
+        __syncwarp();
+        for_each_run(G, g, tlo, thi, [&](uint32_t t0, uint32_t n) {
+            const uint32_t X = t0 % G.Wc, Y = t0 / G.Wc;
+            const uint64_t off = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
+            warp_copy_run<false>(sb + (t0 - g * 32) * G.WQ, bytes + off, n * G.WQ, lane);
+        });
+        __syncwarp();
     }
 }
 

@@ -275,6 +275,26 @@ class DistributedSimulation:
             self.exchange()
         return ms
 
+    def step_profiled(self, rule, nsteps: int):
+        """(total device ms, device ms of the main step kernels, engine kernel launches)."""
+        if self.transport == "nccl":
+            return self.sim.step_profiled(rule, nsteps)
+        tot = main = 0.0
+        launches = 0
+        for _ in range(nsteps):
+            t, m, n = self.sim.step_profiled(rule, 1)
+            tot, main, launches = tot + t, main + m, launches + n + self.launches_per_exchange
+            self.exchange()
+        return tot, main, launches
+
+    def owned_cells(self) -> int:
+        """Compact cells this rank updates per step."""
+        if not self.plan.packed:
+            return self.plan.hi - self.plan.lo
+        info = packed_info(self.sim.desc, self.sim.level(), self.plan.tile_level)
+        tiles = min(self.plan.hi * 32, info["T"]) - self.plan.lo * 32
+        return tiles * info["C"]
+
     def state_hash(self) -> int:
         import torch
         v = C.c_uint64()

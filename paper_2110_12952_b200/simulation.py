@@ -163,6 +163,15 @@ class Simulation:
                                                 int(nsteps), C.byref(ms)))
         return ms.value
 
+    def step_profiled(self, rule: StencilRule, nsteps: int):
+        """(total device ms, device ms of the main step kernels alone, engine kernel launches)."""
+        self._front_cache = None
+        tot, main, n = C.c_float(), C.c_float(), C.c_uint64()
+        _abi.check(_abi.lib().nbbgpu_step_profiled(self._h, rule.birth & 0xFFFF, rule.survive & 0xFFFF,
+                                                   int(rule.neighborhood == Neighborhood.Moore),
+                                                   int(nsteps), C.byref(tot), C.byref(main), C.byref(n)))
+        return tot.value, main.value, n.value
+
     def state_hash(self) -> int:
         """stencil.cpp:196-234"""
         v = C.c_uint64()

@@ -370,3 +370,26 @@ def test_naive_kernel_with_tensor_core_maps():
                 int(rng.integers(0, 512)), int(rng.integers(0, 512)), Neighborhood.VonNeumann)
             _lockstep_vs_oracle(desc, r, rule, int(rng.integers(0, 2**63)), 0.5, 3,
                                 kernel="naive", map_variant="mma")
+
+
+def test_packed_pinned_host_zero_copy():
+    # pinned (page-locked) host buffers are read / written in place by the
+    # conversion kernels over PCIe; pageable ones go through staging chunks
+    import torch
+    o = oracle.Oracle(T.replicas, 3, 2, 11)
+    o.seed(21, 0.5)
+    sim = Simulation(T, 11, Backend.GpuCompact, SimOptions(kernel="packed"))
+    src = torch.from_numpy(o.front.copy()).pin_memory()
+    L = _abi.lib()
+    _abi.check(L.nbbgpu_upload(sim.handle(), src.data_ptr(), src.numel()))
+    sim.step(conway_rule(), 2)
+    for _ in range(2):
+        o.step(8, 12, True)
+    dst = torch.zeros(src.numel(), dtype=torch.uint8).pin_memory()
+    _abi.check(L.nbbgpu_download(sim.handle(), dst.data_ptr(), dst.numel()))
+    assert np.array_equal(dst.numpy(), o.front)
+    bad = src.clone()
+    bad[17] = 3
+    with pytest.raises(OutOfDomain):
+        _abi.check(L.nbbgpu_upload(sim.handle(), bad.data_ptr(), bad.numel()))
+    assert np.array_equal(sim.front().data, o.front)
