@@ -50,6 +50,8 @@ def run(desc, level, backend=Backend.GpuCompact, steps=10, warmup=3, kernel="aut
            "state_hash": f"{sim.state_hash():016x}"}
     if backend == Backend.GpuCompact:
         out["hbm_gbs_2B_model"] = 2 * cells / (ms / steps / 1e3) / 1e9
+        if sim.active_kernel()[0] == "packed":
+            out["hbm_gbs_packed_model"] = 0.25 * cells / (ms / steps / 1e3) / 1e9
     else:
         out["bb_embedded_cells"] = desc.s ** (2 * level)
         out["hbm_gbs_2B_per_embedded_cell"] = 2 * desc.s ** (2 * level) / (ms / steps / 1e3) / 1e9
@@ -89,16 +91,20 @@ def main():
     H = load_descriptor("@" + os.path.join(ROOT, "descriptors", "h-fractal.desc"))
     Y = load_descriptor("@" + os.path.join(ROOT, "descriptors", "candy.desc"))
     out = {"gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
-    out["config0_T_r10"] = [run(T, 10, steps=100), run(T, 10, Backend.GpuBoundingBox, steps=100)]
-    out["config1_T_r16"] = [run(T, 16, steps=200),
+    out["config0_T_r10"] = [run(T, 10, steps=100), run(T, 10, steps=100, kernel="naive"),
+                            run(T, 10, Backend.GpuBoundingBox, steps=100)]
+    out["config1_T_r16"] = [run(T, 16, steps=1000), run(T, 16, steps=200, kernel="tiled"),
                             run(T, 16, steps=3, kernel="naive", maps="digit"),
                             run(T, 16, steps=3, kernel="naive", maps="mma"),
                             run(T, 16, Backend.GpuBoundingBox, steps=10)]
     out["config1_maps"] = [maps_throughput(T, 16), maps_throughput(T, 20)]
-    out["config2_carpet_r9"] = [run(Cp, 9, steps=50), run(Cp, 9, Backend.GpuBoundingBox, steps=10)]
-    out["config3_T_r18_vs_bb"] = [run(T, 18, steps=20), run(T, 18, Backend.GpuBoundingBox, steps=3)]
-    out["config3_T_r20"] = [run(T, 20, steps=20)]
-    out["config4_generic"] = [run(H, 11, steps=10), run(Y, 8, steps=20), run(H, 10, steps=20)]
+    out["config2_carpet_r9"] = [run(Cp, 9, steps=500), run(Cp, 9, steps=50, kernel="tiled"),
+                                run(Cp, 9, Backend.GpuBoundingBox, steps=10)]
+    out["config3_T_r18_vs_bb"] = [run(T, 18, steps=20), run(T, 18, steps=20, kernel="tiled"),
+                                  run(T, 18, Backend.GpuBoundingBox, steps=3)]
+    out["config3_T_r20"] = [run(T, 20, steps=100), run(T, 20, steps=20, kernel="tiled"), run(T, 22, steps=20)]
+    out["config4_generic"] = [run(H, 11, steps=20), run(Y, 9, steps=20), run(Y, 8, steps=20),
+                              run(H, 10, steps=20)]
     print(json.dumps(out, indent=1))
 
 
