@@ -51,6 +51,8 @@ struct PackedStepParams {
     const uint32_t* srcidx;  // per boundary source m: its local cell
     const uint32_t* btab;    // micro-block kernels: per block NEP stage byte offsets of its externals
     uint32_t* halo;          // [NG][nHp] halo words of the step (halo_words_kernel)
+    int nD;                  // used directions (rows of ntab)
+    uint16_t dfirst[9];      // slots of direction slot ds: [dfirst[ds], dfirst[ds + 1])
 };
 
 // Halo words of the owned groups for one step: H[g][j] bit b = state of the source
@@ -87,6 +89,51 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
             if (lane == (uint32_t)u) mine = word;
         }
         if (lane < 4 && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
+    }
+}
+
+// Large halos (carpet, H: ~200-330 slots per tile): one warp per (group, used
+// direction) -- PER_DIR, few groups -- or per group walking the directions (many
+// groups).  ONE coalesced load gives every lane its neighbour tile in a direction;
+// the direction's slots (contiguous: the plan sorts slots by direction) then cost
+// one load + shift + ballot each, 16 loads in flight per round trip.
+template <bool PER_DIR>
+__global__ void halo_words_wide_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
+                                       uint32_t* __restrict__ H) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t per = PER_DIR ? (uint32_t)p.nD : 1u;
+    const uint64_t nw = (uint64_t)(p.g1 - p.g0) * per;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t g = p.g0 + (uint32_t)(wi / per);
+        const int ds0 = PER_DIR ? (int)(wi % per) : 0, ds1 = PER_DIR ? ds0 + 1 : p.nD;
+        const uint32_t t = g * 32 + lane;
+        uint32_t* Hg = H + (uint64_t)g * p.nHp;
+        for (int ds = ds0; ds < ds1; ++ds) {
+            const uint32_t t2 = t < p.T ? __ldg(p.ntab + (uint64_t)ds * p.T + t) : kNoTile;
+            const bool valid = t2 != kNoTile;
+            const uint32_t* base = bsrc + (uint64_t)(valid ? t2 >> 5 : 0) * p.nSrc;
+            const uint32_t sh = t2 & 31;
+            const uint32_t j_end = p.dfirst[ds + 1];
+            for (uint32_t j0 = p.dfirst[ds]; j0 < j_end; j0 += 32) {
+                uint32_t mine = 0;
+                const uint32_t my_m = j0 + lane < j_end ? (__ldg(p.slot + j0 + lane) & 0xFFFFu) : 0u;
+                for (uint32_t j1 = 0; j1 < 32 && j0 + j1 < j_end; j1 += 16) {
+                    uint32_t v[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_m, j1 + u);
+                        v[u] = (j0 + j1 + u < j_end && valid) ? __ldg(base + m) >> sh : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
+                        if (lane == j1 + u) mine = word;
+                    }
+                }
+                if (j0 + lane < j_end) Hg[j0 + lane] = mine;
+            }
+        }
     }
 }
 
