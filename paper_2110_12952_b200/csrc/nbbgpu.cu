@@ -544,6 +544,7 @@ struct nbbgpu_sim {
     uint32_t* d_ploc = nullptr;
     uint32_t* d_pbtab = nullptr;            // micro-block external offsets
     uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
+    unsigned* d_gbar = nullptr;             // grid barrier of the fused multi-step kernel
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
     // profiling (nbbgpu_step_profiled): events around each main step kernel, launch count
@@ -703,6 +704,8 @@ void ensure_packed_tables(nbbgpu_t h) {
     }
     dmalloc_cap(h->d_ploc, P.loc.size() * 4, "lambda table");
     CK(cudaMemcpy(h->d_ploc, P.loc.data(), P.loc.size() * 4, cudaMemcpyHostToDevice));
+    dmalloc_cap(h->d_gbar, 16, "grid barrier");
+    CK(cudaMemsetAsync(h->d_gbar, 0, 16, h->stream));
     dmalloc_cap(h->d_phalo, (uint64_t)P.NG * P.nHp * 4, "halo words");
     CK(cudaMemsetAsync(h->d_phalo, 0, std::max<uint64_t>(4, (uint64_t)P.NG * P.nHp * 4), h->stream));
     tb += (uint64_t)P.NG * P.nHp * 4;
@@ -987,7 +990,45 @@ void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
     kern<<<(unsigned)blocks, (NCHUNK * NGRP + 2) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
-void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
+void launch_packed_fused_t(nbbgpu_t h, const PackedStepParams& p, int nsteps) {
+    auto kern = step_packed_fused_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO>;
+    constexpr int NCHUNK = (BlockGeom<FT, P, WQ>::NBLK + 31) / 32;
+    constexpr int NT = (NCHUNK * NGRP + 2) * 32;
+    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * p.Cp * 4;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    int sms = 148, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    if (per_sm < 1) raise(NBBGPU_ERR_CUDA, "internal: fused kernel does not fit an SM");
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)(p.g1 - p.g0), (uint64_t)per_sm * sms));
+    PackedStepParams pp = p;
+    uint32_t *P0 = h->pk[0], *P1 = h->pk[1], *B0 = h->bnd[0], *B1 = h->bnd[1];
+    int cur0 = h->cur;
+    unsigned* gbar = h->d_gbar;
+    void* args[] = {&pp, &P0, &P1, &B0, &B1, &cur0, &nsteps, &gbar};
+    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(NT), args, smem, h->stream));
+}
+
+// the fused multi-step kernel exists for the ws3 micro-block configurations
+// Used for small states (<= 8 MB), where launch gaps dominate (T r=16: 11.9 vs 13.3 us per
+// step); large states keep the halo kernel + ws3 pair, whose halo pass runs at full
+// occupancy (T r=20: 0.153 vs 0.162 ms).  NBBGPU_FUSE=0/1 forces either (comparisons).
+bool packed_fusable(nbbgpu_t h) {
+    static const char* env = getenv("NBBGPU_FUSE");
+    const PackedPlan& P = h->pp;
+    if (P.wide) return false;
+    if (env && env[0] == '0') return false;
+    if (!(env && env[0] == '1') && packed_words(P) * 4 > (8ull << 20)) return false;
+    return (P.tag == kTagTriangle && (P.wq == 81 || P.wq == 27)) || (P.tag == kTagCarpet && P.wq == 64) ||
+           (P.tag == kTagVicsek && P.wq == 25) || (P.tag == kTagH && P.wq == 49);
+}
+
+PackedStepParams packed_params(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const PackedPlan& P = h->pp;
     PackedStepParams p{};
     p.C = (uint32_t)P.C; p.Cp = (uint32_t)P.Cp; p.SW = P.SW;
@@ -1005,19 +1046,44 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     p.birth = birth; p.survive = survive;
     p.nbr = h->d_pnbr[moore];
     p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc; p.btab = h->d_pbtab;
+    return p;
+}
+
+// nsteps steps in one cooperative launch (packed_fusable configurations)
+void launch_steps_fused(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int nsteps) {
+    const PackedPlan& P = h->pp;
+    const PackedStepParams p = packed_params(h, birth, survive, moore);
+    if (p.g1 <= p.g0 || nsteps <= 0) return;
+    ++h->launches;
+    prof_mark(h);
+    struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
+    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
+    const int dg = moore ? 8 : 4;
+#define NBB_FU(TAG, FT, BP, W, NGRP, NS, NO)                                                                     \
+    if (P.tag == TAG && P.wq == W) {                                                                             \
+        if (conway && dg == 8) return launch_packed_fused_t<true, 8, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);  \
+        if (conway) return launch_packed_fused_t<true, 4, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);             \
+        if (dg == 8) return launch_packed_fused_t<false, 8, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);           \
+        return launch_packed_fused_t<false, 4, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);                        \
+    }
+    NBB_FU(kTagTriangle, TriangleTag, 2, 81, 1, 4, 2)
+    NBB_FU(kTagTriangle, TriangleTag, 2, 27, 8, 16, 8)
+    NBB_FU(kTagCarpet, CarpetTag, 1, 64, 1, 4, 2)
+    NBB_FU(kTagVicsek, VicsekTag, 2, 25, 16, 24, 16)
+    NBB_FU(kTagH, HTag, 1, 49, 2, 6, 4)
+#undef NBB_FU
+    raise(NBBGPU_ERR_CUDA, "internal: no fused kernel for this plan");
+}
+
+void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
+    const PackedPlan& P = h->pp;
+    const PackedStepParams p = packed_params(h, birth, survive, moore);
     if (p.g1 <= p.g0) return;
     // halo words of every owned group from the boundary plane (separate kernel);
     // the step kernel bulk-loads them with each group record
     if (P.nH > 0) {
-        if (P.nH > 32 && p.g1 - p.g0 >= 8192) {
-            // large halo and enough groups for latency hiding: a warp per group
-            // walking the directions (measured: H r=11 0.357 vs 0.408 ms/step);
-            // fewer groups keep the 4-slots-per-warp kernel (more warps in flight)
-            halo_words_wide_kernel<false><<<grid_for((uint64_t)(p.g1 - p.g0) * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
-        } else {
-            const uint64_t warps = (uint64_t)(p.g1 - p.g0) * (uint64_t)((P.nH + 3) / 4);
-            halo_words_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
-        }
+        const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0);
+        halo_words_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
         CK(cudaGetLastError());
         ++h->launches;
     }
@@ -1245,6 +1311,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_ploc) cudaFree(h->d_ploc);
     if (h->d_pbtab) cudaFree(h->d_pbtab);
     if (h->d_phalo) cudaFree(h->d_phalo);
+    if (h->d_gbar) cudaFree(h->d_gbar);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
     if (h->d_send_all) cudaFree(h->d_send_all);
@@ -1485,7 +1552,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     if (rk == NBBGPU_KERNEL_TILED) ensure_plan(h, moore);
     std::vector<cudaEvent_t> prof;
     if (main_ms) {
-        prof.resize((size_t)nsteps * 2);
+        prof.resize((size_t)std::max<int64_t>(nsteps, 1) * 2);
         for (auto& e : prof) CK(cudaEventCreate(&e));
         h->prof = &prof;
         h->prof_idx = 0;
@@ -1493,11 +1560,23 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     const uint64_t l0 = h->launches;
     CK(cudaEventRecord(h->ev0, h->stream));
     try {
-        for (int64_t i = 0; i < nsteps; ++i) {
-            launch_step(h, birth, survive, moore);
-            h->cur ^= 1;
-            ++h->iteration;
-            if (h->comm) exchange_on_stream(h);  // halo of the new front, on-stream
+        if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm) {
+            // every step in one cooperative launch (chunks bound the launch length)
+            for (int64_t done = 0; done < nsteps;) {
+                const int n = (int)std::min<int64_t>(nsteps - done, 1 << 20);
+                launch_steps_fused(h, birth, survive, moore, n);
+                h->cur ^= (n & 1);
+                h->iteration += n;
+                done += n;
+            }
+        } else {
+            for (int64_t i = 0; i < nsteps; ++i) {
+                if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h)) launch_steps_fused(h, birth, survive, moore, 1);
+                else launch_step(h, birth, survive, moore);
+                h->cur ^= 1;
+                ++h->iteration;
+                if (h->comm) exchange_on_stream(h);  // halo of the new front, on-stream
+            }
         }
     } catch (...) {
         h->prof = nullptr;

@@ -55,86 +55,107 @@ struct PackedStepParams {
     uint16_t dfirst[9];      // slots of direction slot ds: [dfirst[ds], dfirst[ds + 1])
 };
 
+// Boundary-plane / halo loads: through the read-only path when the data was written
+// by an earlier launch (NC), L2-coherent (ld.global.cg) inside the fused multi-step
+// kernel, where the previous step of the same launch wrote it.
+template <bool NC>
+__device__ __forceinline__ uint32_t ld_bnd(const uint32_t* p) {
+    if constexpr (NC) return __ldg(p);
+    else return __ldcg(p);
+}
+
 // Halo words of the owned groups for one step: H[g][j] bit b = state of the source
 // cell of slot j in the neighbour tile of tile 32 g + b (0 when there is none),
-// read from the boundary plane of the front state.  One warp per (group, 4 slots);
-// fully parallel, so the step kernel never waits on a dependent gather.
-__global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
-                                  uint32_t* __restrict__ H) {
-    const uint32_t lane = threadIdx.x & 31;
+// read from the boundary plane of the front state.  Task wi = (group, 4 slots), one
+// warp each; fully parallel, so the step never waits on a dependent gather.
+template <bool NC>
+__device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
+                                           uint64_t wi, uint32_t lane) {
     const uint32_t spw = (p.nH + 3) / 4;
-    const uint64_t nw = (uint64_t)(p.g1 - p.g0) * spw;
-    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
-         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t g = p.g0 + (uint32_t)(wi / spw), j0 = (uint32_t)(wi % spw) * 4;
-        const uint32_t t = g * 32 + lane;
-        uint32_t t2[4], sl[4];
+    const uint32_t g = p.g0 + (uint32_t)(wi / spw), j0 = (uint32_t)(wi % spw) * 4;
+    const uint32_t t = g * 32 + lane;
+    uint32_t t2[4], sl[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t j = j0 + u;
-            t2[u] = kNoTile;
-            sl[u] = 0;
-            if (j < p.nH) {
-                sl[u] = __ldg(p.slot + j);
-                if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u;
+        t2[u] = kNoTile;
+        sl[u] = 0;
+        if (j < p.nH) {
+            sl[u] = __ldg(p.slot + j);
+            if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
+        }
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t v = t2[u] != kNoTile
+                               ? (ld_bnd<NC>(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
+                               : 0u;
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, v != 0);
+        if (lane == (uint32_t)u) mine = word;
+    }
+    if (lane < 4 && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
+}
+
+// Large halos (carpet, H: ~200-330 slots per tile): one task per group walking the
+// used directions.  ONE coalesced load gives every lane its neighbour tile in a
+// direction; the direction's slots (contiguous: the plan sorts slots by direction)
+// then cost one load + shift + ballot each, 16 loads in flight per round trip.
+template <bool NC>
+__device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
+                                               uint32_t g, uint32_t lane) {
+    const uint32_t t = g * 32 + lane;
+    uint32_t* Hg = H + (uint64_t)g * p.nHp;
+    for (int ds = 0; ds < p.nD; ++ds) {
+        const uint32_t t2 = t < p.T ? __ldg(p.ntab + (uint64_t)ds * p.T + t) : kNoTile;
+        const bool valid = t2 != kNoTile;
+        const uint32_t* base = bsrc + (uint64_t)(valid ? t2 >> 5 : 0) * p.nSrc;
+        const uint32_t sh = t2 & 31;
+        const uint32_t j_end = p.dfirst[ds + 1];
+        for (uint32_t j0 = p.dfirst[ds]; j0 < j_end; j0 += 32) {
+            uint32_t mine = 0;
+            const uint32_t my_m = j0 + lane < j_end ? (__ldg(p.slot + j0 + lane) & 0xFFFFu) : 0u;
+            for (uint32_t j1 = 0; j1 < 32 && j0 + j1 < j_end; j1 += 16) {
+                uint32_t v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_m, j1 + u);
+                    v[u] = (j0 + j1 + u < j_end && valid) ? ld_bnd<NC>(base + m) >> sh : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
+                    if (lane == j1 + u) mine = word;
+                }
             }
+            if (j0 + lane < j_end) Hg[j0 + lane] = mine;
         }
-        uint32_t mine = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t v = t2[u] != kNoTile
-                                   ? (__ldg(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
-                                   : 0u;
-            const uint32_t word = __ballot_sync(0xFFFFFFFFu, v != 0);
-            if (lane == (uint32_t)u) mine = word;
-        }
-        if (lane < 4 && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
     }
 }
 
-// Large halos (carpet, H: ~200-330 slots per tile): one warp per (group, used
-// direction) -- PER_DIR, few groups -- or per group walking the directions (many
-// groups).  ONE coalesced load gives every lane its neighbour tile in a direction;
-// the direction's slots (contiguous: the plan sorts slots by direction) then cost
-// one load + shift + ballot each, 16 loads in flight per round trip.
-template <bool PER_DIR>
-__global__ void halo_words_wide_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
-                                       uint32_t* __restrict__ H) {
+// large halo and enough groups for latency hiding -> one warp per group walking the
+// directions (measured: H r=11 0.357 vs 0.408 ms/step); else 4 slots per warp
+__host__ __device__ __forceinline__ bool halo_use_wide(uint32_t nH, uint32_t groups) {
+    return nH > 32 && groups >= 8192;
+}
+__host__ __device__ __forceinline__ uint64_t halo_tasks(uint32_t nH, uint32_t groups) {
+    return halo_use_wide(nH, groups) ? (uint64_t)groups : (uint64_t)groups * ((nH + 3) / 4);
+}
+
+template <bool NC>
+__device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
+                                          uint64_t wi, uint32_t lane) {
+    if (halo_use_wide(p.nH, p.g1 - p.g0)) halo_wide_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
+    else halo4_task<NC>(p, bsrc, H, wi, lane);
+}
+
+__global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
+                                  uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t per = PER_DIR ? (uint32_t)p.nD : 1u;
-    const uint64_t nw = (uint64_t)(p.g1 - p.g0) * per;
+    const uint64_t nw = halo_tasks(p.nH, p.g1 - p.g0);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
-         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t g = p.g0 + (uint32_t)(wi / per);
-        const int ds0 = PER_DIR ? (int)(wi % per) : 0, ds1 = PER_DIR ? ds0 + 1 : p.nD;
-        const uint32_t t = g * 32 + lane;
-        uint32_t* Hg = H + (uint64_t)g * p.nHp;
-        for (int ds = ds0; ds < ds1; ++ds) {
-            const uint32_t t2 = t < p.T ? __ldg(p.ntab + (uint64_t)ds * p.T + t) : kNoTile;
-            const bool valid = t2 != kNoTile;
-            const uint32_t* base = bsrc + (uint64_t)(valid ? t2 >> 5 : 0) * p.nSrc;
-            const uint32_t sh = t2 & 31;
-            const uint32_t j_end = p.dfirst[ds + 1];
-            for (uint32_t j0 = p.dfirst[ds]; j0 < j_end; j0 += 32) {
-                uint32_t mine = 0;
-                const uint32_t my_m = j0 + lane < j_end ? (__ldg(p.slot + j0 + lane) & 0xFFFFu) : 0u;
-                for (uint32_t j1 = 0; j1 < 32 && j0 + j1 < j_end; j1 += 16) {
-                    uint32_t v[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_m, j1 + u);
-                        v[u] = (j0 + j1 + u < j_end && valid) ? __ldg(base + m) >> sh : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
-                        if (lane == j1 + u) mine = word;
-                    }
-                }
-                if (j0 + lane < j_end) Hg[j0 + lane] = mine;
-            }
-        }
-    }
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5)
+        halo_task<true>(p, bsrc, H, wi, lane);
 }
 
 // ---- mbarrier + 1-D bulk copy (TMA engine) -----------------------------------
@@ -572,6 +593,163 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             mbar_arrive(empty0 + 8 * s);
             mbar_arrive(ofull0 + 8 * o);
         }
+    }
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Grid-wide barrier of a cooperative launch: arrival counter + generation word.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// All nsteps steps in ONE cooperative launch (persistent, one CTA per SM): per step
+//   phase H: every warp of the grid gathers halo words (halo_task) into H,
+//   grid barrier,
+//   phase S: the warp-specialised TMA-in / TMA-out micro-block pipeline of
+//            step_packed_ws3_kernel over this CTA's groups (ring counters run on
+//            across steps),
+//   grid barrier (records, boundary words complete), swap.
+// No launch gaps and no halo-kernel tail between steps.  Data written by earlier
+// steps of the launch is read L2-coherently (ld.global.cg / TMA), with proxy fences
+// between generic writes and async-proxy reads.
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
+__global__ void __launch_bounds__(((BlockGeom<FT, P, WQ>::NBLK + 31) / 32 * NGRP + 2) * 32, 1)
+step_packed_fused_kernel(const PackedStepParams p, uint32_t* P0, uint32_t* P1, uint32_t* B0, uint32_t* B1,
+                         int cur0, int nsteps, unsigned* gbar) {
+    using W = Wiring<FT, P>;
+    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
+    constexpr int NCHUNK = (NBLK + 31) / 32;
+    constexpr int NCW = NCHUNK * NGRP;
+    constexpr int NEP = W::NEP;
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
+    const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
+    uint8_t* st = sm + 16 * (NS + NO);
+    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
+    uint8_t* outs = st + NS * stage_bytes;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, NCHUNK);
+        }
+        for (int o = 0; o < NO; ++o) {
+            mbar_init(ofull0 + 8 * o, NCHUNK);
+            mbar_init(oempty0 + 8 * o, 1);
+        }
+        mbar_fence_init();
+    }
+    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
+    for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
+        reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * rec_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    // groups of this CTA per step; l-th of them = g0 + blockIdx.x + l * gridDim.x
+    const uint32_t ng = p.g1 - p.g0;
+    const uint32_t n_mine = blockIdx.x < ng ? (ng - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    const uint64_t nwarps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint64_t htasks = p.nH ? halo_tasks(p.nH, ng) : 0;
+
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    const int set = warp < NCW ? warp / NCHUNK : 0, c = warp < NCW ? warp - set * NCHUNK : 0;
+    const uint32_t blk = (uint32_t)c * 32 + lane;
+    const bool active = warp < NCW && blk < (uint32_t)NBLK;
+    uint32_t toff[NEP];
+    {
+        const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
+        static_for<NEP / 4>([&](auto e4) {
+            constexpr int E = decltype(e4)::value;
+            const uint4 v = __ldg(t4 + E);
+            toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
+        });
+    }
+    uint32_t ip = 0, is = 0, ic = (uint32_t)set;  // running group counters (producer, storer, consumers)
+
+    for (int step = 0; step < nsteps; ++step) {
+        const int cur = cur0 ^ (step & 1);
+        const uint32_t* src = cur ? P1 : P0;
+        uint32_t* dst = cur ? P0 : P1;
+        const uint32_t* bsrc = cur ? B1 : B0;
+        uint32_t* bdst = cur ? B0 : B1;
+        // ---- phase H: halo words of every owned group ------------------------------
+        for (uint64_t wi = gwarp; wi < htasks; wi += nwarps_total) halo_task<false>(p, bsrc, p.halo, wi, lane);
+        fence_proxy_async_global();  // H (generic writes) is read by TMA next
+        grid_barrier(gbar);
+        // ---- phase S -----------------------------------------------------------------
+        const uint32_t i_end = (uint32_t)(step + 1) * n_mine;
+        if (warp == NCW) {  // producer
+            if (lane == 0) {
+                fence_proxy_async_global();
+                for (; ip < i_end; ++ip) {
+                    const uint32_t g = p.g0 + blockIdx.x + (ip - (uint32_t)step * n_mine) * gridDim.x;
+                    const uint32_t s = ip % NS;
+                    if (ip >= NS) mbar_wait(empty0 + 8 * s, ((ip / NS) - 1) & 1u);
+                    const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
+                    mbar_expect_tx(bar, rec_bytes + halo_bytes);
+                    bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
+                    if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
+                }
+            }
+        } else if (warp == NCW + 1) {  // storer
+            if (lane == 0) {
+                for (; is < i_end; ++is) {
+                    const uint32_t g = p.g0 + blockIdx.x + (is - (uint32_t)step * n_mine) * gridDim.x;
+                    const uint32_t o = is % NO;
+                    mbar_wait(ofull0 + 8 * o, (is / NO) & 1u);
+                    bulk_s2g(dst + (uint64_t)g * p.Cp, smem_u32(outs + o * rec_bytes), rec_bytes);
+                    bulk_wait_read_all();
+                    mbar_arrive(oempty0 + 8 * o);
+                }
+                bulk_wait_all();            // this step's records are in global memory
+                fence_proxy_async_global();
+            }
+        } else {  // consumers
+            for (; ic < i_end; ic += NGRP) {
+                const uint32_t g = p.g0 + blockIdx.x + (ic - (uint32_t)step * n_mine) * gridDim.x;
+                const uint32_t s = ic % NS, o = ic % NO;
+                mbar_wait(full0 + 8 * s, (ic / NS) & 1u);
+                if (ic >= NO) mbar_wait(oempty0 + 8 * o, ((ic / NO) - 1) & 1u);
+                const uint8_t* Sb = st + s * stage_bytes;
+                uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * rec_bytes);
+                const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+                if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
+                if (c == 0)
+                    for (uint32_t m = lane; m < p.nSrc; m += 32)
+                        bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(empty0 + 8 * s);
+                    mbar_arrive(ofull0 + 8 * o);
+                }
+            }
+        }
+        grid_barrier(gbar);  // records + boundary words of this step complete
     }
 }
 

@@ -393,3 +393,26 @@ def test_packed_pinned_host_zero_copy():
     with pytest.raises(OutOfDomain):
         _abi.check(L.nbbgpu_upload(sim.handle(), bad.data_ptr(), bad.numel()))
     assert np.array_equal(sim.front().data, o.front)
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_packed_multistep_fused_and_split(monkeypatch, fuse):
+    # many steps per call: one cooperative launch with grid barriers between the
+    # halo and step phases (NBBGPU_FUSE=1), or a halo + step kernel pair per step
+    monkeypatch.setenv("NBBGPU_FUSE", fuse)
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    for desc, r, q in [(T, 12, 6), (T, 13, 8), (CARPET, 5, 4), (VICSEK, 6, 4), (H, 5, 4)]:
+        monkeypatch.setenv("NBBGPU_PACKED_Q", str(q))
+        for rule in (conway_rule(), StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)):
+            o = oracle.Oracle(desc.replicas, desc.k, desc.s, r)
+            o.seed(5, 0.5)
+            sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+            assert sim.active_kernel() == ("packed", q)
+            sim.seed_random(5, 0.5)
+            for n in (7, 1, 4):
+                sim.step(rule, n)
+                for _ in range(n):
+                    o.step(rule.birth, rule.survive, rule.moore)
+                assert np.array_equal(sim.front().data, o.front), (desc.name, r, q, n, fuse)
+            assert sim.iteration() == 12
+            sim.close()
