@@ -43,10 +43,14 @@ typedef enum {
     NBBGPU_ERR_INVALID = 6         /* null handle / bad argument */
 } nbbgpu_status;
 
-/* Storage layout of a handle: the reference's Layout::LinearCompact for
- * Backend::Compact and Layout::Embedded for Backend::BoundingBox
- * (proj/src/stencil.cpp:108-112). */
-enum { NBBGPU_MODE_COMPACT = 0, NBBGPU_MODE_BB = 1 };
+/* Backend + storage layout of a handle (proj/src/stencil.cpp:108-112):
+ *   COMPACT  Backend::Compact, Layout::LinearCompact (k^r bytes, cy*w + cx)
+ *   BB       Backend::BoundingBox, Layout::Embedded (n^2 bytes)
+ *   LAMBDA   Backend::CompactGrid ("lambda"), Layout::Embedded, stepped over
+ *            the k^r compact indices (stencil.cpp:313-332)
+ *   BLOCKED  Backend::Compact with SimOptions::block_size = rho = s^m,
+ *            Layout::BlockedCompact (k^(r-m) rho x rho blocks, grid.cpp:54-63) */
+enum { NBBGPU_MODE_COMPACT = 0, NBBGPU_MODE_BB = 1, NBBGPU_MODE_LAMBDA = 2, NBBGPU_MODE_BLOCKED = 3 };
 
 /* Step kernels (nbbgpu_set_kernel).  AUTO picks PACKED when the level admits a
  * packed tile level (even q >= 2), else TILED / NAIVE.  NAIVE is the paper's
@@ -75,6 +79,11 @@ int nbbgpu_device_count(void);
  * cell cap of Grid::Grid (grid.cpp:18-22; default 2 GiB, grid.hpp:13). */
 int nbbgpu_create(const int32_t* replicas_xy, int k, int s, int level, int mode, int device,
                   uint64_t memory_cap, nbbgpu_t* out);
+/* nbbgpu_create with SimOptions::block_size (stencil.hpp:59-64): block_size > 0
+ * requires mode BLOCKED and must be a power of s not above s^level
+ * (geometry.cpp:69-108, OutOfDomain otherwise); nbbgpu_create == block_size 0. */
+int nbbgpu_create_ex(const int32_t* replicas_xy, int k, int s, int level, int mode, int block_size,
+                     int device, uint64_t memory_cap, nbbgpu_t* out);
 int nbbgpu_destroy(nbbgpu_t h);
 
 /* Simulation::seed_random (stencil.cpp:138-180): both buffers zeroed, iteration

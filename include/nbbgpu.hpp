@@ -40,17 +40,23 @@ inline void check(int status) {
     }
 }
 
-enum class Mode { Compact = NBBGPU_MODE_COMPACT, BoundingBox = NBBGPU_MODE_BB };
+enum class Mode {
+    Compact = NBBGPU_MODE_COMPACT,
+    BoundingBox = NBBGPU_MODE_BB,
+    Lambda = NBBGPU_MODE_LAMBDA,    // Backend::CompactGrid
+    Blocked = NBBGPU_MODE_BLOCKED   // Backend::Compact with SimOptions::block_size
+};
 
 class Simulation {
 public:
     // replicas: k (gx, gy) pairs in replica-ID order (FractalDescriptor::replicas)
+    // block_size: SimOptions::block_size, only with Mode::Blocked
     Simulation(const std::vector<std::pair<int, int>>& replicas, int growth, int level, Mode mode,
-               std::uint64_t memory_cap = 2ull << 30, int device = 0) {
+               std::uint64_t memory_cap = 2ull << 30, int device = 0, int block_size = 0) {
         std::vector<int32_t> flat;
         for (auto [x, y] : replicas) { flat.push_back(x); flat.push_back(y); }
-        check(nbbgpu_create(flat.data(), (int)replicas.size(), growth, level, (int)mode, device,
-                            memory_cap, &h_));
+        check(nbbgpu_create_ex(flat.data(), (int)replicas.size(), growth, level, (int)mode, block_size,
+                               device, memory_cap, &h_));
     }
     ~Simulation() { nbbgpu_destroy(h_); }
     Simulation(const Simulation&) = delete;

@@ -84,6 +84,15 @@ def lib():
         L.nbbo_step.restype = None
         L.nbbo_fnv1a64.argtypes = [C.c_void_p, C.c_int64]
         L.nbbo_fnv1a64.restype = C.c_uint64
+        L.nbbo_blocked_index.argtypes = [P(_Mapper), P(_Mapper), C.c_int64, C.c_int64, C.c_int64]
+        L.nbbo_blocked_index.restype = C.c_int64
+        L.nbbo_blocked_seed.argtypes = [P(_Mapper), P(_Mapper), C.c_int64, C.c_uint64, C.c_double, C.c_void_p]
+        L.nbbo_blocked_seed.restype = None
+        L.nbbo_blocked_hash.argtypes = [P(_Mapper), P(_Mapper), C.c_int64, C.c_void_p]
+        L.nbbo_blocked_hash.restype = C.c_uint64
+        L.nbbo_blocked_step.argtypes = [P(_Mapper), P(_Mapper), C.c_int64, C.c_uint16, C.c_uint16, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
+        L.nbbo_blocked_step.restype = None
         _lib = L
     return _lib
 
@@ -97,18 +106,35 @@ class Oracle:
     """The C restatement for one (descriptor, level): maps, seeding, steps, hash.
 
     mode "compact" keeps the reference's linear compact buffer (cy*w+cx, k^r bytes);
-    mode "bb" keeps the embedded n*n buffer.
+    mode "bb" keeps the embedded n*n buffer; mode "lambda" (the CompactGrid
+    backend) the embedded buffer stepped over the compact indices; mode "blocked"
+    (block_size rho = s^m) the BlockedCompact layout of k^(r-m) rho x rho blocks.
     """
 
-    def __init__(self, replicas, k: int, s: int, level: int, mode: str = "compact"):
+    def __init__(self, replicas, k: int, s: int, level: int, mode: str = "compact",
+                 block_size: int = 0):
         self.m = _Mapper()
         arr = (C.c_int32 * (2 * k))(*[int(v) for xy in replicas for v in xy])
         if lib().nbbo_mapper_init(C.byref(self.m), arr, k, s, level) != 0:
             raise ValueError("invalid descriptor/level for the oracle")
-        self.mode = 1 if mode == "bb" else 0
+        self.mode = {"compact": 0, "bb": 1, "lambda": 2, "blocked": 3}[mode]
         self.k, self.s, self.level = k, s, level
         self.side, self.w, self.h = self.m.side, self.m.w, self.m.h
-        n = self.side * self.side if self.mode == 1 else self.w * self.h
+        self.rho = 0
+        if self.mode == 3:
+            mexp, p = 0, 1
+            while p < block_size:
+                p *= s
+                mexp += 1
+            if p != block_size or mexp > level:
+                raise ValueError("block size must be s^m with m <= level")
+            self.rho = block_size
+            self.mc = _Mapper()
+            if lib().nbbo_mapper_init(C.byref(self.mc), arr, k, s, level - mexp) != 0:
+                raise ValueError("invalid coarse level for the oracle")
+            n = self.mc.w * self.mc.h * block_size * block_size
+        else:
+            n = self.side * self.side if self.mode in (1, 2) else self.w * self.h
         self.front = np.zeros(n, dtype=np.uint8)
         self.back = np.zeros(n, dtype=np.uint8)
 
@@ -134,11 +160,25 @@ class Oracle:
     def seed(self, seed: int, density: float) -> None:
         self.front[:] = 0
         self.back[:] = 0
+        if self.mode == 3:
+            lib().nbbo_blocked_seed(C.byref(self.m), C.byref(self.mc), self.rho, seed, density,
+                                    self.front.ctypes.data)
+            return
         lib().nbbo_seed(C.byref(self.m), self.mode, seed, density, self.front.ctypes.data)
+
+    def blocked_index(self, x: int, y: int) -> int:
+        return int(lib().nbbo_blocked_index(C.byref(self.m), C.byref(self.mc), self.rho, x, y))
 
     def step(self, birth: int = 0x8, survive: int = 0xC, moore: bool = True, nsteps: int = 1,
              threads: int = 0) -> None:
         threads = threads or min(os.cpu_count() or 1, 64)
+        if self.mode == 3:
+            for _ in range(nsteps):
+                lib().nbbo_blocked_step(C.byref(self.m), C.byref(self.mc), self.rho, birth, survive,
+                                        int(moore), self.front.ctypes.data, self.back.ctypes.data, 0,
+                                        self.mc.w * self.mc.h)
+                self.front, self.back = self.back, self.front
+            return
         for _ in range(nsteps):
             lib().nbbo_step(C.byref(self.m), self.mode, birth, survive, int(moore),
                             self.front.ctypes.data, self.back.ctypes.data, threads)
@@ -153,6 +193,9 @@ class Oracle:
         self.front, self.back = self.back, self.front
 
     def state_hash(self) -> int:
+        if self.mode == 3:
+            return int(lib().nbbo_blocked_hash(C.byref(self.m), C.byref(self.mc), self.rho,
+                                               self.front.ctypes.data))
         return int(lib().nbbo_state_hash(C.byref(self.m), self.mode, self.front.ctypes.data))
 
     def state_hash_range(self, i0: int, i1: int) -> int:

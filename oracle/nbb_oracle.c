@@ -140,7 +140,7 @@ uint64_t nbbo_coord_mix(int64_t x, int64_t y) {
 
 /* Simulation::seed_random, proj/src/stencil.cpp:138-180 (linear + embedded). */
 void nbbo_seed(const nbbo_mapper* m, int mode, uint64_t seed, double density, uint8_t* f) {
-    if (mode == 1) {
+    if (mode == 1 || mode == 2) { /* embedded storage (bb, lambda) */
         for (int64_t y = 0; y < m->side; ++y)
             for (int64_t x = 0; x < m->side; ++x) {
                 int64_t cx, cy;
@@ -160,7 +160,7 @@ void nbbo_seed(const nbbo_mapper* m, int mode, uint64_t seed, double density, ui
 /* Simulation::state_hash, proj/src/stencil.cpp:196-234 (embedded + linear). */
 uint64_t nbbo_state_hash(const nbbo_mapper* m, int mode, const uint8_t* f) {
     uint64_t hash = 0;
-    if (mode == 1) {
+    if (mode == 1 || mode == 2) { /* embedded storage (bb, lambda) */
         const int64_t total = m->side * m->side;
         for (int64_t i = 0; i < total; ++i)
             if (f[i]) hash += nbbo_coord_mix(i % m->side, i / m->side);
@@ -235,6 +235,97 @@ void nbbo_step_bb(const nbbo_mapper* m, uint16_t birth, uint16_t survive, int mo
         }
 }
 
+/* Simulation::step_compact_grid (the "lambda" backend), proj/src/stencil.cpp:313-332:
+ * embedded storage, the loop visits exactly the k^r compact indices [i0, i1),
+ * neighbours are read in embedded coordinates (no nu). */
+void nbbo_step_lambda(const nbbo_mapper* m, uint16_t birth, uint16_t survive, int moore,
+                      const uint8_t* f, uint8_t* b, int64_t i0, int64_t i1) {
+    const int deg = moore ? 8 : 4;
+    const int64_t n = m->side, w = m->w;
+    for (int64_t i = i0; i < i1; ++i) {
+        int64_t ex, ey;
+        nbbo_to_embedded(m, i % w, i / w, &ex, &ey);
+        int count = 0;
+        for (int j = 0; j < deg; ++j) {
+            const int64_t nx = ex + kOff[j][0], ny = ey + kOff[j][1];
+            if (nx >= 0 && ny >= 0 && nx < n && ny < n) count += f[ny * n + nx];
+        }
+        b[ey * n + ex] = apply_rule(birth, survive, f[ey * n + ex], count);
+    }
+}
+
+/* ---- blocked compact layout (Layout::BlockedCompact) ----------------------------
+ * block b of the coarse mapper mc (level r - m, rho = s^m) holds the rho x rho
+ * embedded mini box with corner lambda_c(b) * rho, row-major: slot
+ * b*rho^2 + ly*rho + lx (grid.cpp:54-63).  mf is the full-level mapper. */
+
+/* Grid::storage_index, BlockedCompact branch (grid.cpp:54-63); -1 if the coarse
+ * cell is not in the coarse fractal. */
+int64_t nbbo_blocked_index(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, int64_t x, int64_t y) {
+    (void)mf;
+    int64_t cx, cy;
+    if (!nbbo_try_to_compact(mc, x / rho, y / rho, &cx, &cy)) return -1;
+    return (cy * mc->w + cx) * rho * rho + (y % rho) * rho + (x % rho);
+}
+
+/* Simulation::seed_random, BlockedCompact branch (stencil.cpp:161-177) */
+void nbbo_blocked_seed(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, uint64_t seed,
+                       double density, uint8_t* f) {
+    const int64_t blocks = mc->w * mc->h;
+    for (int64_t bk = 0; bk < blocks; ++bk) {
+        int64_t cxe, cye;
+        nbbo_to_embedded(mc, bk % mc->w, bk / mc->w, &cxe, &cye);
+        for (int64_t ly = 0; ly < rho; ++ly)
+            for (int64_t lx = 0; lx < rho; ++lx) {
+                const int64_t x = cxe * rho + lx, y = cye * rho + ly;
+                int64_t a, c;
+                if (nbbo_try_to_compact(mf, x, y, &a, &c))
+                    f[bk * rho * rho + ly * rho + lx] = nbbo_cell_alive(seed, x, y, density) ? 1 : 0;
+            }
+    }
+}
+
+/* Simulation::state_hash, BlockedCompact branch (stencil.cpp:217-231) */
+uint64_t nbbo_blocked_hash(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, const uint8_t* f) {
+    (void)mf;
+    uint64_t hash = 0;
+    const int64_t blocks = mc->w * mc->h;
+    for (int64_t bk = 0; bk < blocks; ++bk) {
+        int64_t cxe, cye;
+        nbbo_to_embedded(mc, bk % mc->w, bk / mc->w, &cxe, &cye);
+        for (int64_t ly = 0; ly < rho; ++ly)
+            for (int64_t lx = 0; lx < rho; ++lx)
+                if (f[bk * rho * rho + ly * rho + lx]) hash += nbbo_coord_mix(cxe * rho + lx, cye * rho + ly);
+    }
+    return hash;
+}
+
+/* Simulation::step_compact_blocked, proj/src/stencil.cpp:370-399, blocks [b0, b1) */
+void nbbo_blocked_step(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, uint16_t birth,
+                       uint16_t survive, int moore, const uint8_t* f, uint8_t* b, int64_t b0, int64_t b1) {
+    const int deg = moore ? 8 : 4;
+    const int64_t n = mf->side;
+    for (int64_t bk = b0; bk < b1; ++bk) {
+        int64_t cxe, cye;
+        nbbo_to_embedded(mc, bk % mc->w, bk / mc->w, &cxe, &cye);
+        for (int64_t ly = 0; ly < rho; ++ly)
+            for (int64_t lx = 0; lx < rho; ++lx) {
+                const int64_t x = cxe * rho + lx, y = cye * rho + ly;
+                int64_t a, c;
+                if (!nbbo_try_to_compact(mf, x, y, &a, &c)) continue; /* filler slot, stays dead */
+                int count = 0;
+                for (int j = 0; j < deg; ++j) {
+                    const int64_t nx = x + kOff[j][0], ny = y + kOff[j][1];
+                    if (nx < 0 || ny < 0 || nx >= n || ny >= n) continue;
+                    if (nbbo_try_to_compact(mf, nx, ny, &a, &c))
+                        count += f[nbbo_blocked_index(mf, mc, rho, nx, ny)];
+                }
+                const int64_t slot = bk * rho * rho + ly * rho + lx;
+                b[slot] = apply_rule(birth, survive, f[slot], count);
+            }
+    }
+}
+
 typedef struct {
     const nbbo_mapper* m;
     int mode, moore;
@@ -247,6 +338,7 @@ typedef struct {
 static void* step_worker(void* arg) {
     step_job* j = (step_job*)arg;
     if (j->mode == 1) nbbo_step_bb(j->m, j->birth, j->survive, j->moore, j->f, j->b, j->lo, j->hi);
+    else if (j->mode == 2) nbbo_step_lambda(j->m, j->birth, j->survive, j->moore, j->f, j->b, j->lo, j->hi);
     else nbbo_step_compact(j->m, j->birth, j->survive, j->moore, j->f, j->b, j->lo, j->hi);
     return NULL;
 }
@@ -255,7 +347,7 @@ static void* step_worker(void* arg) {
  * compact splits compact indices into ceil(D/W) chunks. */
 void nbbo_step(const nbbo_mapper* m, int mode, uint16_t birth, uint16_t survive, int moore,
                const uint8_t* f, uint8_t* b, int nthreads) {
-    const int64_t domain = mode == 1 ? m->side : m->w * m->h;
+    const int64_t domain = mode == 1 ? m->side : m->w * m->h;  /* mode 2: compact indices */
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
     if (nthreads == 1 || domain < 2) {

@@ -75,6 +75,21 @@ void nbbo_step(const nbbo_mapper* m, int mode, uint16_t birth, uint16_t survive,
 /* FNV-1a 64 over a byte buffer (the golden-vector fingerprint). */
 uint64_t nbbo_fnv1a64(const uint8_t* p, int64_t n);
 
+/* "lambda" backend step (CompactGrid, stencil.cpp:313-332): embedded buffers,
+ * compact indices [i0, i1).  nbbo_step / nbbo_seed / nbbo_state_hash accept
+ * mode 2 = lambda (embedded storage, compact iteration). */
+void nbbo_step_lambda(const nbbo_mapper* m, uint16_t birth, uint16_t survive, int moore,
+                      const uint8_t* f, uint8_t* b, int64_t i0, int64_t i1);
+
+/* Blocked compact layout (Layout::BlockedCompact, grid.cpp:54-63): mf = full-level
+ * mapper, mc = mapper at level r - m with rho = s^m. */
+int64_t nbbo_blocked_index(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, int64_t x, int64_t y);
+void nbbo_blocked_seed(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, uint64_t seed,
+                       double density, uint8_t* f);
+uint64_t nbbo_blocked_hash(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, const uint8_t* f);
+void nbbo_blocked_step(const nbbo_mapper* mf, const nbbo_mapper* mc, int64_t rho, uint16_t birth,
+                       uint16_t survive, int moore, const uint8_t* f, uint8_t* b, int64_t b0, int64_t b1);
+
 #ifdef __cplusplus
 }
 #endif

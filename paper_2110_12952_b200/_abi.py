@@ -22,6 +22,8 @@ SIGNATURES = {
     "nbbgpu_device_count": (C.c_int, []),
     "nbbgpu_create": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.c_uint64, _P(_H)]),
+    "nbbgpu_create_ex": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_uint64, _P(_H)]),
     "nbbgpu_destroy": (C.c_int, [_H]),
     "nbbgpu_seed": (C.c_int, [_H, C.c_uint64, C.c_double]),
     "nbbgpu_step": (C.c_int, [_H, C.c_uint16, C.c_uint16, C.c_int, C.c_int64]),

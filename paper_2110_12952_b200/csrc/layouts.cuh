@@ -1,0 +1,133 @@
+// layouts.cuh -- the reference's two other storage layouts on the device
+// (SURVEY.md 8(f) f1/f2):
+//   * the "lambda" backend (Backend::CompactGrid): embedded n x n storage, but the
+//     step visits exactly the k^r compact indices through lambda and reads the
+//     neighbours in embedded coordinates (Simulation::step_compact_grid,
+//     proj/src/stencil.cpp:313-332) -- the paper's approach 2;
+//   * the blocked compact layout (Layout::BlockedCompact, --block-size rho = s^m):
+//     k^(r-m) blocks of rho x rho embedded mini boxes, block-major and row-major
+//     inside a block (grid.cpp:54-63), stepped by step_compact_blocked
+//     (stencil.cpp:370-399) -- the paper's best nu configuration (rho = 16).
+// One thread per compact index / block slot; the digit loops are those of
+// common.cuh.  Bit-exact with the reference (tests/test_gpu_layouts.py).
+#pragma once
+
+#include "common.cuh"
+
+namespace nbbgpu {
+
+// Simulation::step_compact_grid (stencil.cpp:313-332)
+template <int K, int S>
+__global__ void step_lambda_kernel(Frac f, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                   uint32_t birth, uint32_t survive, int deg) {
+    const uint64_t total = (uint64_t)f.w * f.h, n = f.side;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t x, y;
+        lambda_map<K, S>(f, (uint32_t)(i % f.w), (uint32_t)(i / f.w), x, y);
+        uint32_t count = 0;
+        for (int j = 0; j < deg; ++j) {
+            const int64_t nx = (int64_t)x + kOffX[j], ny = (int64_t)y + kOffY[j];
+            if (nx >= 0 && ny >= 0 && nx < (int64_t)n && ny < (int64_t)n) count += src[(uint64_t)ny * n + nx];
+        }
+        const uint64_t e = (uint64_t)y * n + x;
+        dst[e] = apply_rule(birth, survive, src[e], count);
+    }
+}
+
+struct BlockedGeom {
+    Frac f;          // full level r
+    Frac fc;         // coarse level r - m
+    uint32_t rho;    // s^m
+    int m;
+};
+
+// every one of the m low digit pairs of the in-block position is a replica:
+// (x, y) is a fractal cell iff its coarse cell is (block present) and this holds
+template <int S>
+__device__ __forceinline__ bool low_member(const Frac& f, uint32_t lx, uint32_t ly, int m) {
+    const uint32_t s = sval<S>(f);
+    for (int mu = 0; mu < m; ++mu) {
+        if (f.id_of_subbox[(ly % s) * s + (lx % s)] < 0) return false;
+        lx /= s;
+        ly /= s;
+    }
+    return true;
+}
+
+// Grid::storage_index, BlockedCompact branch (grid.cpp:54-63); false if the coarse
+// cell of (x, y) is not in the coarse fractal
+template <int K, int S>
+__device__ __forceinline__ bool blocked_index(const BlockedGeom& G, uint32_t x, uint32_t y, uint64_t& idx) {
+    uint32_t cx, cy;
+    if (!nu_map<K, S>(G.fc, x / G.rho, y / G.rho, cx, cy)) return false;
+    idx = ((uint64_t)cy * G.fc.w + cx) * G.rho * G.rho + (uint64_t)(y % G.rho) * G.rho + (x % G.rho);
+    return true;
+}
+
+// Simulation::seed_random, BlockedCompact branch (stencil.cpp:161-177)
+template <int K, int S>
+__global__ void seed_blocked_kernel(BlockedGeom G, uint8_t* __restrict__ front, uint64_t seed_mix,
+                                    double density) {
+    const uint64_t per = (uint64_t)G.rho * G.rho, total = (uint64_t)G.fc.w * G.fc.h * per;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i / per;
+        const uint32_t ly = (uint32_t)((i % per) / G.rho), lx = (uint32_t)(i % G.rho);
+        if (!low_member<S>(G.f, lx, ly, G.m)) continue;  // filler slot stays 0
+        uint32_t X, Y;
+        lambda_map<K, S>(G.fc, (uint32_t)(b % G.fc.w), (uint32_t)(b / G.fc.w), X, Y);
+        front[i] = cell_alive_mixed(seed_mix, X * G.rho + lx, Y * G.rho + ly, density) ? 1 : 0;
+    }
+}
+
+// Simulation::state_hash, BlockedCompact branch (stencil.cpp:217-231)
+template <int K, int S>
+__global__ void hash_blocked_kernel(BlockedGeom G, const uint8_t* __restrict__ front, unsigned long long* out) {
+    const uint64_t per = (uint64_t)G.rho * G.rho, total = (uint64_t)G.fc.w * G.fc.h * per;
+    uint64_t acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!front[i]) continue;
+        const uint64_t b = i / per;
+        const uint32_t ly = (uint32_t)((i % per) / G.rho), lx = (uint32_t)(i % G.rho);
+        uint32_t X, Y;
+        lambda_map<K, S>(G.fc, (uint32_t)(b % G.fc.w), (uint32_t)(b / G.fc.w), X, Y);
+        acc += coord_mix(X * G.rho + lx, Y * G.rho + ly);
+    }
+    block_sum_atomic(acc, out);
+}
+
+// Simulation::step_compact_blocked (stencil.cpp:370-399): one thread per slot;
+// neighbours inside the block are a local offset, the others go through the coarse
+// nu of the neighbouring block (Grid::storage_index).
+template <int K, int S>
+__global__ void step_blocked_kernel(BlockedGeom G, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                    uint32_t birth, uint32_t survive, int deg) {
+    const uint64_t per = (uint64_t)G.rho * G.rho, total = (uint64_t)G.fc.w * G.fc.h * per;
+    const int64_t n = G.f.side, rho = G.rho;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i / per;
+        const int64_t ly = (int64_t)((i % per) / G.rho), lx = (int64_t)(i % G.rho);
+        if (!low_member<S>(G.f, (uint32_t)lx, (uint32_t)ly, G.m)) continue;  // filler slot, stays dead
+        uint32_t X, Y;
+        lambda_map<K, S>(G.fc, (uint32_t)(b % G.fc.w), (uint32_t)(b / G.fc.w), X, Y);
+        const int64_t x = (int64_t)X * rho + lx, y = (int64_t)Y * rho + ly;
+        uint32_t count = 0;
+        for (int j = 0; j < deg; ++j) {
+            const int64_t nx = x + kOffX[j], ny = y + kOffY[j];
+            if (nx < 0 || ny < 0 || nx >= n || ny >= n) continue;
+            const int64_t nlx = lx + kOffX[j], nly = ly + kOffY[j];
+            if (nlx >= 0 && nly >= 0 && nlx < rho && nly < rho) {  // same block
+                if (low_member<S>(G.f, (uint32_t)nlx, (uint32_t)nly, G.m)) count += src[b * per + nly * rho + nlx];
+            } else if (low_member<S>(G.f, (uint32_t)(nx % rho), (uint32_t)(ny % rho), G.m)) {
+                uint64_t idx;
+                if (blocked_index<K, S>(G, (uint32_t)nx, (uint32_t)ny, idx)) count += src[idx];
+            }
+        }
+        dst[i] = apply_rule(birth, survive, src[i], count);
+    }
+}
+
+}  // namespace nbbgpu

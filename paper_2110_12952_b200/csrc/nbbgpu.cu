@@ -23,6 +23,7 @@
 #include "naive.cuh"
 #include "tiled.cuh"
 #include "packed.cuh"
+#include "layouts.cuh"
 
 using namespace nbbgpu;
 
@@ -492,6 +493,7 @@ struct nbbgpu_sim {
     Frac frac{};
     MmaTables mt{};
     int mode = NBBGPU_MODE_COMPACT;
+    BlockedGeom bg{};          // NBBGPU_MODE_BLOCKED: block size rho = s^m, coarse tables
     uint64_t cells = 0;      // stored cells per buffer
     uint8_t* buf[2] = {nullptr, nullptr};
     int cur = 0;             // front = buf[cur]
@@ -628,7 +630,7 @@ constexpr uint64_t kTiledMinCells = 1ull << 17;
 bool is_device_ptr(const void* p);
 
 int resolve_kernel_for(nbbgpu_t h, int kernel) {
-    if (h->mode == NBBGPU_MODE_BB) return NBBGPU_KERNEL_NAIVE;
+    if (h->mode != NBBGPU_MODE_COMPACT) return NBBGPU_KERNEL_NAIVE;  // bb, lambda, blocked
     if (kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
     if (kernel == NBBGPU_KERNEL_PACKED) {
         if (h->pq < 2) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
@@ -1169,7 +1171,7 @@ void owned_range(nbbgpu_t h, uint64_t& lo, uint64_t& hi) {
         hi = (uint64_t)h->pg1 * h->pp.Cp;
         return;
     }
-    if (h->mode == NBBGPU_MODE_BB || h->nranks == 1) {
+    if (h->mode != NBBGPU_MODE_COMPACT || h->nranks == 1) {
         lo = 0;
         hi = h->cells;
         return;
@@ -1182,6 +1184,22 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const int deg = moore ? 8 : 4;
     const uint8_t* src = h->front();
     uint8_t* dst = h->back();
+    if (h->mode == NBBGPU_MODE_LAMBDA || h->mode == NBBGPU_MODE_BLOCKED) {
+        ++h->launches;
+        prof_mark(h);
+        struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
+        if (h->mode == NBBGPU_MODE_LAMBDA) {
+            const uint64_t n = (uint64_t)h->hf.w * h->hf.h;
+#define NBB_CALL(K, S, ...) step_lambda_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, src, dst, birth, survive, deg)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else {
+#define NBB_CALL(K, S, ...) step_blocked_kernel<K, S><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->bg, src, dst, birth, survive, deg)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+        return;
+    }
     if (h->mode == NBBGPU_MODE_BB) {
         ++h->launches;
         prof_mark(h);
@@ -1338,7 +1356,11 @@ uint64_t device_hash(nbbgpu_t h, bool owned) {
             NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL
         }
-    } else if (h->mode == NBBGPU_MODE_BB) {
+    } else if (h->mode == NBBGPU_MODE_BLOCKED) {
+#define NBB_CALL(K, S, ...) hash_blocked_kernel<K, S><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->bg, h->front(), h->d_acc)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+    } else if (h->mode == NBBGPU_MODE_BB || h->mode == NBBGPU_MODE_LAMBDA) {
         hash_bb_kernel<<<grid_for((uint64_t)h->hf.side * h->hf.side, 256), 256, 0, h->stream>>>((uint32_t)h->hf.side, h->front(), h->d_acc);
     } else if (hi > lo) {
 #define NBB_CALL(K, S, ...) hash_compact_kernel<K, S><<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(h->frac, h->front(), lo, hi, h->d_acc)
@@ -1365,7 +1387,15 @@ bool is_device_ptr(const void* p) {
 bool storage_index(nbbgpu_t h, int64_t x, int64_t y, uint64_t& idx) {
     int64_t cx, cy;
     if (!h->hf.nu(x, y, cx, cy, h->hf.r)) return false;
-    idx = h->mode == NBBGPU_MODE_BB ? (uint64_t)(y * h->hf.side + x) : (uint64_t)(cy * h->hf.w + cx);
+    if (h->mode == NBBGPU_MODE_BLOCKED) {  // Grid::storage_index, grid.cpp:54-63
+        const int64_t rho = h->bg.rho;
+        int64_t bx, by;
+        if (!h->hf.nu(x / rho, y / rho, bx, by, h->hf.r - h->bg.m)) return false;
+        idx = (uint64_t)((by * (int64_t)h->bg.fc.w + bx) * rho * rho + (y % rho) * rho + (x % rho));
+        return true;
+    }
+    idx = (h->mode == NBBGPU_MODE_BB || h->mode == NBBGPU_MODE_LAMBDA) ? (uint64_t)(y * h->hf.side + x)
+                                                                      : (uint64_t)(cy * h->hf.w + cx);
     return true;
 }
 
@@ -1435,19 +1465,39 @@ int nbbgpu_device_count(void) {
 
 int nbbgpu_create(const int32_t* rep, int k, int s, int level, int mode, int device,
                   uint64_t memory_cap, nbbgpu_t* out) {
+    return nbbgpu_create_ex(rep, k, s, level, mode, 0, device, memory_cap, out);
+}
+
+int nbbgpu_create_ex(const int32_t* rep, int k, int s, int level, int mode, int block_size, int device,
+                     uint64_t memory_cap, nbbgpu_t* out) {
     if (!out) { g_err = "null output handle"; return NBBGPU_ERR_INVALID; }
     *out = nullptr;
     nbbgpu_t h = new (std::nothrow) nbbgpu_sim();
     if (!h) { g_err = "host allocation failed"; return NBBGPU_ERR_CAPACITY; }
     const int rc = guarded([&] {
         if (!rep && k > 0) raise(NBBGPU_ERR_INVALID, "null replica table");
-        if (mode != NBBGPU_MODE_COMPACT && mode != NBBGPU_MODE_BB) raise(NBBGPU_ERR_INVALID, "unknown mode");
+        if (mode < NBBGPU_MODE_COMPACT || mode > NBBGPU_MODE_BLOCKED) raise(NBBGPU_ERR_INVALID, "unknown mode");
+        // Simulation ctor option checks (stencil.cpp:128-131)
+        if (block_size > 0 && mode != NBBGPU_MODE_BLOCKED) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "block size applies to the compact backend only");
+        if (mode == NBBGPU_MODE_BLOCKED && block_size < 1) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "the blocked layout needs a block size");
         h->hf.init(rep, k, s, level);
         if (h->hf.side > (int64_t)1 << 31 || h->hf.w > (int64_t)1 << 31)
             raise(NBBGPU_ERR_OUT_OF_DOMAIN, "level " + std::to_string(level) + " exceeds the engine's 32-bit coordinate range");
         h->mode = mode;
         // Grid::Grid cap check (grid.cpp:16-22): per grid, cells > memory_cap
-        const int64_t cells = mode == NBBGPU_MODE_BB ? HostFrac::ipow(h->hf.side, 2) : h->hf.w * h->hf.h;
+        int64_t cells = (mode == NBBGPU_MODE_BB || mode == NBBGPU_MODE_LAMBDA) ? HostFrac::ipow(h->hf.side, 2)
+                                                                           : h->hf.w * h->hf.h;
+        if (mode == NBBGPU_MODE_BLOCKED) {
+            // block_exponent / stored_cells (geometry.cpp:69-108)
+            int m = 0;
+            int64_t p = 1;
+            while (p < block_size) { p *= s; ++m; }
+            if (p != block_size) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "block size " + std::to_string(block_size) + " is not a power of s=" + std::to_string(s));
+            if (m > level) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "block size " + std::to_string(block_size) + " exceeds the level-" + std::to_string(level) + " fractal");
+            cells = HostFrac::ipow(k, level - m) * (int64_t)block_size * block_size;
+            h->bg.rho = (uint32_t)block_size;
+            h->bg.m = m;
+        }
         if ((uint64_t)cells > memory_cap)
             raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(cells) + " cells exceeds the memory cap of " + std::to_string(memory_cap) + " bytes");
         h->cells = (uint64_t)cells;
@@ -1464,6 +1514,14 @@ int nbbgpu_create(const int32_t* rep, int k, int s, int level, int mode, int dev
         for (int i = 0; i < kMaxS * kMaxS; ++i) f.id_of_subbox[i] = -1;
         for (int i = 0; i < s * s; ++i) f.id_of_subbox[i] = (int8_t)h->hf.id[i];
         for (int i = 0; i < k; ++i) { f.gx[i] = (uint8_t)h->hf.gx[i]; f.gy[i] = (uint8_t)h->hf.gy[i]; }
+        if (mode == NBBGPU_MODE_BLOCKED) {
+            h->bg.f = f;
+            h->bg.fc = f;
+            h->bg.fc.r = level - h->bg.m;
+            h->bg.fc.w = (uint32_t)HostFrac::ipow(k, (h->bg.fc.r + 1) / 2);
+            h->bg.fc.h = (uint32_t)HostFrac::ipow(k, h->bg.fc.r / 2);
+            h->bg.fc.side = (uint32_t)HostFrac::ipow(s, h->bg.fc.r);
+        }
         for (int mu = 0; mu < 32 && mu < level; ++mu) {
             h->mt.spow[mu] = (uint32_t)h->hf.spow[mu];
             int64_t t = 1;
@@ -1526,7 +1584,11 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
             return;
         }
         for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
-        if (h->mode == NBBGPU_MODE_BB) {
+        if (h->mode == NBBGPU_MODE_BLOCKED) {
+#define NBB_CALL(K, S, ...) seed_blocked_kernel<K, S><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->bg, h->front(), mix, density)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else if (h->mode == NBBGPU_MODE_BB || h->mode == NBBGPU_MODE_LAMBDA) {
             const uint64_t n = h->cells;
 #define NBB_CALL(K, S, ...) seed_bb_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, h->front(), mix, density)
             NBB_DISPATCH_KS(h->hf);

@@ -60,13 +60,14 @@ class Simulation:
                  backend: Backend = Backend.GpuCompact, options: Optional[SimOptions] = None):
         options = options or SimOptions()
         desc.validate()
-        if backend not in (Backend.GpuCompact, Backend.GpuBoundingBox):
+        if backend not in (Backend.GpuCompact, Backend.GpuBoundingBox, Backend.GpuLambda):
             raise OutOfDomain(f"backend '{backend.value}' is a CPU backend of the reference; "
-                              "this engine provides gpu-compact and gpu-bb")
-        # option validation, stencil.cpp:128-135
-        if options.block_size > 0:
-            raise OutOfDomain("block size applies to the compact CPU backend only")
-        if options.neighbor_table and backend != Backend.GpuCompact:
+                              "this engine provides gpu-compact, gpu-bb and gpu-lambda")
+        # option validation, stencil.cpp:128-135 (the neighbour table is accepted for the
+        # linear compact backend: the GPU kernels' tile tables play its role)
+        if options.block_size > 0 and backend != Backend.GpuCompact:
+            raise OutOfDomain("block size applies to the compact backend only")
+        if options.neighbor_table and (backend != Backend.GpuCompact or options.block_size > 0):
             raise OutOfDomain("the neighbor table applies to the linear compact backend only")
         self.desc = desc
         self._level = level
@@ -74,10 +75,15 @@ class Simulation:
         self.options = options
         L = _abi.lib()
         h = C.c_void_p()
-        mode = 1 if backend == Backend.GpuBoundingBox else 0
-        _abi.check(L.nbbgpu_create(_abi.replica_array(desc.replicas), desc.replica_count,
-                                   desc.growth, level, mode, options.device,
-                                   int(options.memory_cap), C.byref(h)))
+        if backend == Backend.GpuBoundingBox:
+            mode = 1
+        elif backend == Backend.GpuLambda:
+            mode = 2
+        else:
+            mode = 3 if options.block_size > 0 else 0
+        _abi.check(L.nbbgpu_create_ex(_abi.replica_array(desc.replicas), desc.replica_count,
+                                      desc.growth, level, mode, int(options.block_size),
+                                      options.device, int(options.memory_cap), C.byref(h)))
         self._h = h
         w, hh, side = C.c_int64(), C.c_int64(), C.c_int64()
         _abi.check(L.nbbgpu_dims(h, C.byref(w), C.byref(hh), C.byref(side)))
@@ -183,7 +189,8 @@ class Simulation:
             n = self.stored_cells()
             buf = np.empty(n, dtype=np.uint8)
             _abi.check(_abi.lib().nbbgpu_download(self._h, buf.ctypes.data, n))
-            layout = "embedded" if self._backend == Backend.GpuBoundingBox else "linear-compact"
+            layout = ("embedded" if self._backend in (Backend.GpuBoundingBox, Backend.GpuLambda) else
+                      "blocked-compact" if self.options.block_size > 0 else "linear-compact")
             self._front_cache = HostGrid(layout, buf, self._w, self._hgt, self._side)
         return self._front_cache
 

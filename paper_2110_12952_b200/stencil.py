@@ -88,6 +88,7 @@ class Backend(Enum):
     Compact = "compact"
     GpuCompact = "gpu-compact"
     GpuBoundingBox = "gpu-bb"
+    GpuLambda = "gpu-lambda"
 
 
 def backend_name(b: Backend) -> str:
@@ -98,4 +99,4 @@ def parse_backend(name: str) -> Backend:
     for b in Backend:
         if b.value == name:
             return b
-    raise ParseError(f"unknown backend '{name}' (expected bb, lambda, compact, gpu-compact or gpu-bb)")
+    raise ParseError(f"unknown backend '{name}' (expected bb, lambda, compact, gpu-compact, gpu-bb or gpu-lambda)")

@@ -312,8 +312,12 @@ def test_errors_and_validation():
     with pytest.raises(CapacityError, match="memory cap"):
         Simulation(T, 16, Backend.GpuBoundingBox)
     Simulation(T, 16, Backend.GpuCompact).close()
-    with pytest.raises(OutOfDomain):
-        Simulation(T, 3, Backend.GpuCompact, SimOptions(block_size=2))
+    with pytest.raises(OutOfDomain):  # not a power of s (geometry.cpp:93-97)
+        Simulation(T, 3, Backend.GpuCompact, SimOptions(block_size=3))
+    with pytest.raises(OutOfDomain):  # exceeds the level (geometry.cpp:98-101)
+        Simulation(T, 3, Backend.GpuCompact, SimOptions(block_size=16))
+    with pytest.raises(OutOfDomain):  # compact backend only (stencil.cpp:128-129)
+        Simulation(T, 3, Backend.GpuBoundingBox, SimOptions(block_size=2))
 
 
 def test_upload_download_roundtrip():

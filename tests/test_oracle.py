@@ -158,3 +158,28 @@ def test_oracle_equals_reference_directly():
                 c = o.to_compact(x, y)
                 if c is not None:
                     assert oracle.ref_to_compact(desc.replicas, desc.k, desc.s, r, x, y) == c
+
+
+def test_oracle_lambda_and_blocked_match_reference_library():
+    # the C restatement of step_compact_grid (stencil.cpp:313-332) and of the blocked
+    # layout (grid.cpp:54-63, stencil.cpp:161-177/217-231/370-399) against the
+    # unmodified reference, byte for byte, after every step
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    T = [(0, 0), (1, 0), (0, 1)]
+    C8 = [(0, 0), (1, 0), (2, 0), (0, 1), (2, 1), (0, 2), (1, 2), (2, 2)]
+    V = [(1, 0), (0, 1), (1, 1), (2, 1), (1, 2)]
+    for rep, k, s, r in [(T, 3, 2, 6), (C8, 8, 3, 3), (V, 5, 3, 4), (T, 3, 2, 8)]:
+        for mode, bs in [("lambda", 0), ("blocked", s), ("blocked", s * s)]:
+            o = oracle.Oracle(rep, k, s, r, mode=mode, block_size=bs)
+            o.seed(9, 0.5)
+            R = oracle.RefSim(rep, k, s, r, backend="lambda" if mode == "lambda" else "compact",
+                              block_size=bs)
+            R.seed_random(9, 0.5)
+            assert np.array_equal(o.front, R.front()), (mode, bs)
+            for i in range(5):
+                birth, surv, moore = (8, 12, True) if i % 2 == 0 else (0x49, 0x1A7, False)
+                o.step(birth, surv, moore)
+                R.step(birth, surv, moore)
+                assert np.array_equal(o.front, R.front()), (mode, bs, r, i)
+                assert o.state_hash() == R.state_hash()
