@@ -132,6 +132,15 @@ int nbbgpu_upload(nbbgpu_t h, const uint8_t* src, uint64_t bytes);
 int nbbgpu_get_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t* out);
 int nbbgpu_set_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t state);
 
+/* The embedded n x n view of the front state, Simulation::cell for every (x, y)
+ * (stencil.cpp:182-188), computed on the device for any layout: `bytes` must be
+ * side^2; dst is host or device memory. */
+int nbbgpu_embedded_view(nbbgpu_t h, uint8_t* dst, uint64_t bytes);
+/* write_pbm (pbm.cpp:9-23) rendered on the device: plain PBM "P1\n<n> <n>\n" + n
+ * rows of '0'/'1' + '\n'.  side > render_cap -> NBBGPU_ERR_CAPACITY (the
+ * reference's CapacityError).  dst == NULL returns the size in *written. */
+int nbbgpu_render_pbm(nbbgpu_t h, char* dst, uint64_t capacity, int64_t render_cap, uint64_t* written);
+
 /* Device bytes held by the handle (both state buffers + tables + scratch). */
 int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out);
 

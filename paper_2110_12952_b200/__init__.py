@@ -12,6 +12,8 @@ from .errors import (NbbError, ParseError, NotInFractal, OutOfDomain,  # noqa: F
 from .stencil import (StencilRule, Neighborhood, Backend, conway_rule,  # noqa: F401
                       neighbor_offsets, backend_name, parse_backend)
 from .simulation import Simulation, SimOptions, RunResult, run_simulation  # noqa: F401
+from .output import (write_pbm, render_pbm, embedded_view, verify_stencil,  # noqa: F401
+                     VerifyReport)
 
 
 def device_count() -> int:

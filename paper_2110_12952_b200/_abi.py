@@ -40,6 +40,8 @@ SIGNATURES = {
     "nbbgpu_get_cell": (C.c_int, [_H, C.c_int64, C.c_int64, _P(C.c_uint8)]),
     "nbbgpu_set_cell": (C.c_int, [_H, C.c_int64, C.c_int64, C.c_uint8]),
     "nbbgpu_peak_bytes": (C.c_int, [_H, _P(C.c_uint64)]),
+    "nbbgpu_embedded_view": (C.c_int, [_H, C.c_void_p, C.c_uint64]),
+    "nbbgpu_render_pbm": (C.c_int, [_H, C.c_void_p, C.c_uint64, C.c_int64, _P(C.c_uint64)]),
     "nbbgpu_set_kernel": (C.c_int, [_H, C.c_int]),
     "nbbgpu_set_map_variant": (C.c_int, [_H, C.c_int]),
     "nbbgpu_active_kernel": (C.c_int, [_H, _P(C.c_int), _P(C.c_int)]),

@@ -130,4 +130,45 @@ __global__ void step_blocked_kernel(BlockedGeom G, const uint8_t* __restrict__ s
     }
 }
 
+// ---- the embedded n x n view of any layout (Simulation::cell for every (x, y),
+// stencil.cpp:182-188): bytes 0/1, or the rows of a plain PBM (write_pbm,
+// pbm.cpp:9-23: '1'/'0' per cell, '\n' after each row) -------------------------
+struct ViewSrc {
+    int mode;               // NBBGPU_MODE_*
+    bool packed;            // compact mode, packed layout
+    const uint8_t* bytes;   // byte layouts
+    const uint32_t* words;  // packed layout
+    uint32_t wq, Wc, Cp;    // packed geometry
+    BlockedGeom bg;         // blocked layout
+};
+
+template <int K, int S>
+__device__ __forceinline__ uint8_t view_cell(const Frac& f, const ViewSrc& v, uint32_t x, uint32_t y) {
+    if (v.mode == 1 || v.mode == 2) return v.bytes[(uint64_t)y * f.side + x];  // bb / lambda: holes are 0
+    uint32_t cx, cy;
+    if (!nu_map<K, S>(f, x, y, cx, cy)) return 0;  // not a fractal cell
+    if (v.mode == 3) {
+        uint64_t idx;
+        if (!blocked_index<K, S>(v.bg, x, y, idx)) return 0;
+        return v.bytes[idx];
+    }
+    if (!v.packed) return v.bytes[(uint64_t)cy * f.w + cx];
+    const uint32_t X = cx / v.wq, c = cx % v.wq, Y = cy / v.wq, a = cy % v.wq;
+    const uint64_t t = (uint64_t)Y * v.Wc + X;
+    return (uint8_t)((v.words[(t / 32) * v.Cp + (uint64_t)a * v.wq + c] >> (t % 32)) & 1u);
+}
+
+// PBM: row stride n + 1 with '\n' at the end, characters '0' / '1'; else bytes 0 / 1
+template <int K, int S>
+__global__ void embedded_view_kernel(Frac f, ViewSrc v, uint8_t* __restrict__ out, int pbm) {
+    const uint64_t n = f.side, stride = pbm ? n + 1 : n, total = n * stride;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t y = i / stride, x = i - y * stride;
+        if (x == n) { out[i] = '\n'; continue; }
+        const uint8_t c = view_cell<K, S>(f, v, (uint32_t)x, (uint32_t)y);
+        out[i] = pbm ? (uint8_t)(c ? '1' : '0') : c;
+    }
+}
+
 }  // namespace nbbgpu

@@ -1827,6 +1827,70 @@ int nbbgpu_set_cell(nbbgpu_t h, int64_t x, int64_t y, uint8_t state) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+// the embedded n x n view (bytes, or PBM rows) of the front state into dst (host or device)
+void render_view(nbbgpu_t h, uint8_t* dst, int pbm) {
+    ViewSrc v{};
+    v.mode = h->mode;
+    v.packed = h->layout == 1;
+    v.bytes = h->layout == 1 ? nullptr : h->front();
+    v.words = h->layout == 1 ? h->pk[h->cur] : nullptr;
+    if (h->layout == 1) {
+        v.wq = (uint32_t)h->pp.wq;
+        v.Wc = (uint32_t)h->pp.Wc;
+        v.Cp = (uint32_t)h->pp.Cp;
+    }
+    v.bg = h->bg;
+    const uint64_t n = (uint64_t)h->hf.side, total = n * (pbm ? n + 1 : n);
+    uint8_t* out = dst;
+    const bool dev = is_device_mem(dst);
+    if (!dev) dmalloc_cap(out, total, "render buffer");
+#define NBB_CALL(K, S, ...) embedded_view_kernel<K, S><<<grid_for(total, 256), 256, 0, h->stream>>>(h->frac, v, out, pbm)
+    NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+    CK(cudaGetLastError());
+    if (!dev) {
+        CK(cudaMemcpyAsync(dst, out, total, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(out);
+    } else {
+        CK(cudaStreamSynchronize(h->stream));
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int nbbgpu_embedded_view(nbbgpu_t h, uint8_t* dst, uint64_t bytes) {
+    return guarded([&] {
+        check_handle(h);
+        if (!dst) raise(NBBGPU_ERR_INVALID, "null destination");
+        const uint64_t n = (uint64_t)h->hf.side;
+        if (bytes != n * n) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "view size " + std::to_string(bytes) + " != side^2 " + std::to_string(n * n));
+        render_view(h, dst, 0);
+    });
+}
+
+int nbbgpu_render_pbm(nbbgpu_t h, char* dst, uint64_t capacity, int64_t render_cap, uint64_t* written) {
+    return guarded([&] {
+        check_handle(h);
+        if (!written) raise(NBBGPU_ERR_INVALID, "null size output");
+        const int64_t n = h->hf.side;
+        // write_pbm (pbm.cpp:11-15)
+        if (n > render_cap)
+            raise(NBBGPU_ERR_CAPACITY, "side " + std::to_string(n) + " exceeds the render cap of " + std::to_string(render_cap));
+        const std::string header = "P1\n" + std::to_string(n) + " " + std::to_string(n) + "\n";
+        const uint64_t body = (uint64_t)n * (uint64_t)(n + 1), total = header.size() + body;
+        *written = total;
+        if (!dst) return;
+        if (capacity < total) raise(NBBGPU_ERR_INVALID, "PBM buffer too small");
+        std::memcpy(dst, header.data(), header.size());
+        render_view(h, reinterpret_cast<uint8_t*>(dst) + header.size(), 1);
+    });
+}
+
 int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out) {
     return guarded([&] {
         if (!h || !out) raise(NBBGPU_ERR_INVALID, "null argument");
