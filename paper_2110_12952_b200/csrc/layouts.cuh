@@ -98,33 +98,73 @@ __global__ void hash_blocked_kernel(BlockedGeom G, const uint8_t* __restrict__ f
     block_sum_atomic(acc, out);
 }
 
-// Simulation::step_compact_blocked (stencil.cpp:370-399): one thread per slot;
-// neighbours inside the block are a local offset, the others go through the coarse
-// nu of the neighbouring block (Grid::storage_index).
+// Static per-block table (built once per handle): [0..8] the block index in every
+// direction (dy+1)*3 + dx+1 (4 = the block itself; kNoBlock outside the box or on a
+// coarse hole, via the coarse nu), [9], [10] the block's coarse corner
+// (lambda at level r - m), [11] unused -- 48 B per block, 3 x 16-B loads.
+constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
+constexpr int kBlockTab = 12;
+
 template <int K, int S>
-__global__ void step_blocked_kernel(BlockedGeom G, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                    uint32_t birth, uint32_t survive, int deg) {
+__global__ void build_blocktab_kernel(BlockedGeom G, uint32_t* __restrict__ tab) {
+    const uint64_t nblocks = (uint64_t)G.fc.w * G.fc.h;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nblocks;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t X, Y;
+        lambda_map<K, S>(G.fc, (uint32_t)(b % G.fc.w), (uint32_t)(b / G.fc.w), X, Y);
+        uint32_t* t = tab + b * kBlockTab;
+        for (int d = 0; d < 9; ++d) {
+            const int64_t nx = (int64_t)X + d % 3 - 1, ny = (int64_t)Y + d / 3 - 1;
+            uint32_t v = kNoBlock, cx, cy;
+            if (d == 4) v = (uint32_t)b;
+            else if (nx >= 0 && ny >= 0 && nx < (int64_t)G.fc.side && ny < (int64_t)G.fc.side &&
+                     nu_map<K, S>(G.fc, (uint32_t)nx, (uint32_t)ny, cx, cy))
+                v = cy * G.fc.w + cx;
+            t[d] = v;
+        }
+        t[9] = X;
+        t[10] = Y;
+        t[11] = 0;
+    }
+}
+
+__device__ __forceinline__ bool low_mask_bit(const uint32_t* lm, uint32_t lx, uint32_t ly, uint32_t rho) {
+    const uint32_t i = ly * rho + lx;
+    return (__ldg(lm + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+// Simulation::step_compact_blocked (stencil.cpp:370-399): one thread per slot; the
+// block's neighbour indices come from the static block table, the in-block filler
+// pattern from low_mask (the same for every block) -- no per-cell digit loops.
+__global__ void step_blocked_kernel(BlockedGeom G, const uint32_t* __restrict__ low_mask,
+                                    const uint32_t* __restrict__ btab, const uint8_t* __restrict__ src,
+                                    uint8_t* __restrict__ dst, uint32_t birth, uint32_t survive, int deg) {
     const uint64_t per = (uint64_t)G.rho * G.rho, total = (uint64_t)G.fc.w * G.fc.h * per;
-    const int64_t n = G.f.side, rho = G.rho;
+    const uint32_t rho = G.rho;
+    const int64_t n = G.f.side;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = i / per;
-        const int64_t ly = (int64_t)((i % per) / G.rho), lx = (int64_t)(i % G.rho);
-        if (!low_member<S>(G.f, (uint32_t)lx, (uint32_t)ly, G.m)) continue;  // filler slot, stays dead
-        uint32_t X, Y;
-        lambda_map<K, S>(G.fc, (uint32_t)(b % G.fc.w), (uint32_t)(b / G.fc.w), X, Y);
-        const int64_t x = (int64_t)X * rho + lx, y = (int64_t)Y * rho + ly;
+        const int32_t ly = (int32_t)((i % per) / rho), lx = (int32_t)(i % rho);
+        if (!low_mask_bit(low_mask, lx, ly, rho)) continue;  // filler slot, stays dead
+        const uint4* t4 = reinterpret_cast<const uint4*>(btab + b * kBlockTab);
+        const uint4 q0 = __ldg(t4), q1 = __ldg(t4 + 1), q2 = __ldg(t4 + 2);
+        const uint32_t nbk[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+        const int64_t x = (int64_t)q2.y * rho + lx, y = (int64_t)q2.z * rho + ly;
         uint32_t count = 0;
-        for (int j = 0; j < deg; ++j) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= deg) break;
             const int64_t nx = x + kOffX[j], ny = y + kOffY[j];
             if (nx < 0 || ny < 0 || nx >= n || ny >= n) continue;
-            const int64_t nlx = lx + kOffX[j], nly = ly + kOffY[j];
-            if (nlx >= 0 && nly >= 0 && nlx < rho && nly < rho) {  // same block
-                if (low_member<S>(G.f, (uint32_t)nlx, (uint32_t)nly, G.m)) count += src[b * per + nly * rho + nlx];
-            } else if (low_member<S>(G.f, (uint32_t)(nx % rho), (uint32_t)(ny % rho), G.m)) {
-                uint64_t idx;
-                if (blocked_index<K, S>(G, (uint32_t)nx, (uint32_t)ny, idx)) count += src[idx];
-            }
+            int32_t nlx = lx + kOffX[j], nly = ly + kOffY[j];
+            const int dx = nlx < 0 ? -1 : (nlx >= (int32_t)rho ? 1 : 0);
+            const int dy = nly < 0 ? -1 : (nly >= (int32_t)rho ? 1 : 0);
+            nlx -= dx * (int32_t)rho;
+            nly -= dy * (int32_t)rho;
+            if (!low_mask_bit(low_mask, nlx, nly, rho)) continue;
+            const uint32_t nb2 = nbk[(dy + 1) * 3 + dx + 1];
+            if (nb2 != kNoBlock) count += src[(uint64_t)nb2 * per + (uint64_t)nly * rho + nlx];
         }
         dst[i] = apply_rule(birth, survive, src[i], count);
     }

@@ -494,6 +494,8 @@ struct nbbgpu_sim {
     MmaTables mt{};
     int mode = NBBGPU_MODE_COMPACT;
     BlockedGeom bg{};          // NBBGPU_MODE_BLOCKED: block size rho = s^m, coarse tables
+    uint32_t* d_lowmask = nullptr;  // filler mask of one block (rho^2 bits)
+    uint32_t* d_blocktab = nullptr; // per block: neighbour blocks + coarse corner
     uint64_t cells = 0;      // stored cells per buffer
     uint8_t* buf[2] = {nullptr, nullptr};
     int cur = 0;             // front = buf[cur]
@@ -1194,9 +1196,7 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
             NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL
         } else {
-#define NBB_CALL(K, S, ...) step_blocked_kernel<K, S><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->bg, src, dst, birth, survive, deg)
-            NBB_DISPATCH_KS(h->hf);
-#undef NBB_CALL
+            step_blocked_kernel<<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->bg, h->d_lowmask, h->d_blocktab, src, dst, birth, survive, deg);
         }
         return;
     }
@@ -1330,6 +1330,8 @@ void free_all(nbbgpu_t h) {
     if (h->d_pbtab) cudaFree(h->d_pbtab);
     if (h->d_phalo) cudaFree(h->d_phalo);
     if (h->d_gbar) cudaFree(h->d_gbar);
+    if (h->d_lowmask) cudaFree(h->d_lowmask);
+    if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
     if (h->d_send_all) cudaFree(h->d_send_all);
@@ -1515,12 +1517,29 @@ int nbbgpu_create_ex(const int32_t* rep, int k, int s, int level, int mode, int 
         for (int i = 0; i < s * s; ++i) f.id_of_subbox[i] = (int8_t)h->hf.id[i];
         for (int i = 0; i < k; ++i) { f.gx[i] = (uint8_t)h->hf.gx[i]; f.gy[i] = (uint8_t)h->hf.gy[i]; }
         if (mode == NBBGPU_MODE_BLOCKED) {
+            if (block_size > 64) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "the GPU blocked layout supports block sizes up to 64");
+            const int rho = block_size;
+            std::vector<uint32_t> lmask(((size_t)rho * rho + 31) / 32, 0u);
+            for (int ly = 0; ly < rho; ++ly)
+                for (int lx = 0; lx < rho; ++lx) {
+                    int64_t a, c;
+                    if (h->hf.nu(lx, ly, a, c, h->bg.m)) lmask[(ly * rho + lx) / 32] |= 1u << ((ly * rho + lx) % 32);
+                }
+            dmalloc_cap(h->d_lowmask, lmask.size() * 4, "filler mask");
+            CK(cudaMemcpy(h->d_lowmask, lmask.data(), lmask.size() * 4, cudaMemcpyHostToDevice));
             h->bg.f = f;
             h->bg.fc = f;
             h->bg.fc.r = level - h->bg.m;
             h->bg.fc.w = (uint32_t)HostFrac::ipow(k, (h->bg.fc.r + 1) / 2);
             h->bg.fc.h = (uint32_t)HostFrac::ipow(k, h->bg.fc.r / 2);
             h->bg.fc.side = (uint32_t)HostFrac::ipow(s, h->bg.fc.r);
+            const uint64_t nblocks = (uint64_t)h->bg.fc.w * h->bg.fc.h;
+            dmalloc_cap(h->d_blocktab, nblocks * kBlockTab * 4, "block table");
+            h->bytes_held += nblocks * kBlockTab * 4;
+#define NBB_CALL(K, S, ...) build_blocktab_kernel<K, S><<<grid_for(nblocks, 256), 256, 0, h->stream>>>(h->bg, h->d_blocktab)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+            CK(cudaGetLastError());
         }
         for (int mu = 0; mu < 32 && mu < level; ++mu) {
             h->mt.spow[mu] = (uint32_t)h->hf.spow[mu];
