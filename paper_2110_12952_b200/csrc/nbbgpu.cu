@@ -939,6 +939,24 @@ void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t&
     bit = (uint32_t)(t % 32);
 }
 
+// launch with programmatic stream serialisation (PDL): the kernel may begin while
+// its predecessor on the stream drains and synchronises in-kernel (pdl_wait)
+template <class... KArgs, class... Args>
+void launch_pdl(nbbgpu_t h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    static const bool off = getenv("NBBGPU_NO_PDL") != nullptr;  // comparison knob
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <bool CONWAY, int DEG, bool WIDE>
 void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
     constexpr int NT = kPackedThreads;
@@ -991,7 +1009,8 @@ void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCHUNK * NGRP + 2) * 32, smem));
     const uint64_t groups = p.g1 - p.g0;
     const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
-    kern<<<(unsigned)blocks, (NCHUNK * NGRP + 2) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
+    launch_pdl(h, kern, dim3((unsigned)blocks), dim3((NCHUNK * NGRP + 2) * 32), smem, p,
+               (const uint32_t*)h->pk[h->cur], h->pk[h->cur ^ 1], (const uint32_t*)h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
 template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
@@ -1087,7 +1106,8 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     // the step kernel bulk-loads them with each group record
     if (P.nH > 0) {
         const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0);
-        halo_words_kernel<<<grid_for(warps * 32, 256), 256, 0, h->stream>>>(p, h->bnd[h->cur], h->d_phalo);
+        launch_pdl(h, halo_words_kernel, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
+                   (const uint32_t*)h->bnd[h->cur], h->d_phalo);
         CK(cudaGetLastError());
         ++h->launches;
     }

@@ -30,6 +30,13 @@ namespace nbbgpu {
 constexpr int kPackedThreads = 256;
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic
+// stream-serialisation attribute may start while its predecessor drains; it must
+// wait here before touching the predecessor's output (full completion + flush).
+// A no-op when launched normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct PackedGeom {
     Frac f;
     uint32_t q, WQ, C, Cp;   // tile level, tile width, local cells, padded words per group
@@ -152,6 +159,8 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
+    pdl_wait();     // bsrc comes from the previous step kernel
+    pdl_trigger();  // the step kernel may launch and run its prologue
     const uint64_t nw = halo_tasks(p.nH, p.g1 - p.g0);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5)
@@ -526,6 +535,8 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * rec_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
     fence_proxy_async_smem();
     __syncthreads();
+    pdl_wait();     // the prologue above overlapped the previous kernel's tail (PDL)
+    pdl_trigger();
 
     if (warp == NCW) {  // ---- producer -------------------------------------------------
         if (lane == 0) {
