@@ -1038,15 +1038,13 @@ void launch_packed_fused_t(nbbgpu_t h, const PackedStepParams& p, int nsteps) {
 }
 
 // the fused multi-step kernel exists for the ws3 micro-block configurations
-// Used for small states (<= 8 MB), where launch gaps dominate (T r=16: 11.9 vs 13.3 us per
-// step); large states keep the halo kernel + ws3 pair, whose halo pass runs at full
-// occupancy (T r=20: 0.153 vs 0.162 ms).  NBBGPU_FUSE=0/1 forces either (comparisons).
+// Opt-in (NBBGPU_FUSE=1): with programmatic dependent launch the halo + step kernel
+// pair is faster at every measured level (T r=16: 8.4 vs 12.1 us per step; r=20:
+// 0.148 vs 0.162 ms), so the cooperative multi-step kernel is kept as a variant.
 bool packed_fusable(nbbgpu_t h) {
     static const char* env = getenv("NBBGPU_FUSE");
     const PackedPlan& P = h->pp;
-    if (P.wide) return false;
-    if (env && env[0] == '0') return false;
-    if (!(env && env[0] == '1') && packed_words(P) * 4 > (8ull << 20)) return false;
+    if (P.wide || !(env && env[0] == '1')) return false;
     return (P.tag == kTagTriangle && (P.wq == 81 || P.wq == 27)) || (P.tag == kTagCarpet && P.wq == 64) ||
            (P.tag == kTagVicsek && P.wq == 25) || (P.tag == kTagH && P.wq == 49);
 }
