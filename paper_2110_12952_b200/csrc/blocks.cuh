@@ -131,4 +131,5 @@ __device__ __forceinline__ void static_for(F&& f) {
     static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
+
 }  // namespace nbbgpu

@@ -308,7 +308,7 @@ struct PackedPlan {
     int nH = 0, nHp = 0, nD = 0, nSrc = 0;
     int8_t dlist[8] = {0};
     std::vector<uint8_t> slotD;     // per slot: direction D = (dy+1)*3 + dx+1
-    std::vector<uint32_t> slot;     // per slot: (direction slot << 16) | boundary source m
+    std::vector<uint32_t> slot;     // per slot: (D << 24) | (direction slot << 16) | boundary source m
     std::vector<uint32_t> srcidx;   // per boundary source: local cell
     std::vector<uint32_t> loc;      // per local cell: (yl << 16) | xl  (level-q lambda)
     std::vector<uint32_t> nbr[2];   // [moore] C x 8 stage byte offsets
@@ -405,7 +405,7 @@ PackedPlan build_packed_plan(const HostFrac& F, int q) {
         int m;
         if (it == m_of.end()) { m = (int)PP.srcidx.size(); m_of[cell] = m; PP.srcidx.push_back((uint32_t)cell); }
         else m = it->second;
-        PP.slot.push_back(((uint32_t)P8.hDslot[j] << 16) | (uint32_t)m);
+        PP.slot.push_back(((uint32_t)P8.hD[j] << 24) | ((uint32_t)P8.hDslot[j] << 16) | (uint32_t)m);
         PP.slotD.push_back(P8.hD[j]);
         key8[std::make_tuple((int)P8.hD[j], (int)P8.ha[j], (int)P8.hc[j])] = j;
     }
@@ -1058,7 +1058,7 @@ PackedStepParams packed_params(nbbgpu_t h, uint16_t birth, uint16_t survive, int
     p.nD = P.nD;
     for (int ds = 0; ds <= 8; ++ds) {
         int cnt = 0;
-        for (int j = 0; j < P.nH; ++j) cnt += (int)(P.slot[j] >> 16) < ds;
+        for (int j = 0; j < P.nH; ++j) cnt += (int)((P.slot[j] >> 16) & 0xFFu) < ds;
         p.dfirst[ds] = (uint16_t)cnt;
     }
     p.T = (uint32_t)P.T; p.NG = (uint32_t)P.NG;
@@ -1104,6 +1104,8 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     // the step kernel bulk-loads them with each group record
     if (P.nH > 0) {
         const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0);
+        // (the neighbour tile comes from the static ntab: an ALU carry walk with
+        //  compile-time tables measured slower, T r=20 0.178 vs 0.148 ms per step)
         launch_pdl(h, halo_words_kernel, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
                    (const uint32_t*)h->bnd[h->cur], h->d_phalo);
         CK(cudaGetLastError());

@@ -53,7 +53,7 @@ struct PackedStepParams {
     uint32_t lastmask;       // valid tile bits of group NG - 1
     uint32_t birth, survive;
     const void* nbr;         // [C][8] u16 (u32 when WIDE) byte offsets into the stage
-    const uint32_t* slot;    // per halo slot: (direction slot << 16) | boundary source m
+    const uint32_t* slot;    // per halo slot: (D << 24) | (direction slot << 16) | boundary source m
     const uint32_t* ntab;    // [nD][T] linear neighbour tile or kNoTile
     const uint32_t* srcidx;  // per boundary source m: its local cell
     const uint32_t* btab;    // micro-block kernels: per block NEP stage byte offsets of its externals
@@ -89,7 +89,7 @@ __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint
         sl[u] = 0;
         if (j < p.nH) {
             sl[u] = __ldg(p.slot + j);
-            if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)(sl[u] >> 16) * p.T + t);
+            if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)((sl[u] >> 16) & 0xFFu) * p.T + t);
         }
     }
     uint32_t mine = 0;
