@@ -60,50 +60,75 @@ def ncu_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed region, in
+    process through NVML (pynvml): no nvidia-smi process is spawned next to the
+    timed kernels.  Falls back to nvidia-smi when pynvml is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device]) if vis and vis.split(",")[device].strip().isdigit() else device
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            try:
+                reasons = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                reasons = n.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            self.rows.append((float(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)),
+                              float(n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)), int(reasons)))
+            return
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        if out.returncode == 0 and out.stdout.strip():
+            c = [x.strip() for x in out.stdout.strip().split(",")]
+            bits = sum(v for (name, v), f in zip(self.REASONS.items(), c[2:6]) if f.lower() == "active")
+            self.rows.append((float(c[0]), float(c[1]), bits))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+                self._sample()
             except Exception:
                 return
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nvml is not None else 0.2)
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
 
     def stop(self):
+        try:
+            self._sample()  # one sample at the end of the region too
+        except Exception:
+            pass
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
-        mx = max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"]}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({name for r in self.rows for name, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def dist_env():

@@ -1106,8 +1106,12 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
         const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0);
         // (the neighbour tile comes from the static ntab: an ALU carry walk with
         //  compile-time tables measured slower, T r=20 0.178 vs 0.148 ms per step)
-        launch_pdl(h, halo_words_kernel, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
-                   (const uint32_t*)h->bnd[h->cur], h->d_phalo);
+        if (halo_use_wide((uint32_t)P.nH, p.g1 - p.g0))
+            launch_pdl(h, halo_words_kernel<true>, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
+                       (const uint32_t*)h->bnd[h->cur], h->d_phalo);
+        else
+            launch_pdl(h, halo_words_kernel<false>, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
+                       (const uint32_t*)h->bnd[h->cur], h->d_phalo);
         CK(cudaGetLastError());
         ++h->launches;
     }

@@ -156,6 +156,9 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
     else halo4_task<NC>(p, bsrc, H, wi, lane);
 }
 
+// WIDE_HALO is compile-time so the small-halo variant keeps its 30 registers
+// (full occupancy: this kernel is latency-bound)
+template <bool WIDE_HALO>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
@@ -163,8 +166,10 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
     pdl_trigger();  // the step kernel may launch and run its prologue
     const uint64_t nw = halo_tasks(p.nH, p.g1 - p.g0);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
-         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5)
-        halo_task<true>(p, bsrc, H, wi, lane);
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        if constexpr (WIDE_HALO) halo_wide_task<true>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
+        else halo4_task<true>(p, bsrc, H, wi, lane);
+    }
 }
 
 // ---- mbarrier + 1-D bulk copy (TMA engine) -----------------------------------
