@@ -75,33 +75,36 @@ __device__ __forceinline__ uint32_t ld_bnd(const uint32_t* p) {
 // cell of slot j in the neighbour tile of tile 32 g + b (0 when there is none),
 // read from the boundary plane of the front state.  Task wi = (group, 4 slots), one
 // warp each; fully parallel, so the step never waits on a dependent gather.
-template <bool NC>
+template <bool NC, int SPW = 4>
 __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
                                            uint64_t wi, uint32_t lane) {
-    const uint32_t spw = (p.nH + 3) / 4;
-    const uint32_t g = p.g0 + (uint32_t)(wi / spw), j0 = (uint32_t)(wi % spw) * 4;
+    const uint32_t spw = (p.nH + SPW - 1) / SPW, w32 = (uint32_t)wi;  // tasks < 2^32
+    const uint32_t gi = w32 / spw;
+    const uint32_t g = p.g0 + gi, j0 = (w32 - gi * spw) * SPW;
     const uint32_t t = g * 32 + lane;
-    uint32_t t2[4], sl[4];
+    uint32_t t2[SPW], sl[SPW];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < SPW; ++u) {
         const uint32_t j = j0 + u;
         t2[u] = kNoTile;
         sl[u] = 0;
         if (j < p.nH) {
             sl[u] = __ldg(p.slot + j);
-            if (t < p.T) t2[u] = __ldg(p.ntab + (uint64_t)((sl[u] >> 16) & 0xFFu) * p.T + t);
+            if (t < p.T) t2[u] = __ldg(p.ntab + ((size_t)((sl[u] >> 16) & 0xFFu) * p.T + t));
         }
     }
+    uint32_t v[SPW];
+#pragma unroll
+    for (int u = 0; u < SPW; ++u)
+        v[u] = t2[u] != kNoTile ? ld_bnd<NC>(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)
+                                : 0u;
     uint32_t mine = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const uint32_t v = t2[u] != kNoTile
-                               ? (ld_bnd<NC>(bsrc + (uint64_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)) & 1u
-                               : 0u;
-        const uint32_t word = __ballot_sync(0xFFFFFFFFu, v != 0);
+    for (int u = 0; u < SPW; ++u) {
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
         if (lane == (uint32_t)u) mine = word;
     }
-    if (lane < 4 && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
+    if (lane < SPW && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
 }
 
 // Large halos (carpet, H: ~200-330 slots per tile): one task per group walking the
@@ -158,17 +161,17 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
 
 // WIDE_HALO is compile-time so the small-halo variant keeps its 30 registers
 // (full occupancy: this kernel is latency-bound)
-template <bool WIDE_HALO>
+template <bool WIDE_HALO, int SPW = 4>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
     pdl_wait();     // bsrc comes from the previous step kernel
     pdl_trigger();  // the step kernel may launch and run its prologue
-    const uint64_t nw = halo_tasks(p.nH, p.g1 - p.g0);
+    const uint64_t nw = WIDE_HALO ? (uint64_t)(p.g1 - p.g0) : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         if constexpr (WIDE_HALO) halo_wide_task<true>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
-        else halo4_task<true>(p, bsrc, H, wi, lane);
+        else halo4_task<true, SPW>(p, bsrc, H, wi, lane);
     }
 }
 
