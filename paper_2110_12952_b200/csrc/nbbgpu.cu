@@ -976,28 +976,13 @@ void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
     kern<<<(unsigned)blocks, NT, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NCW, int NS, bool STAB>
-void launch_packed_ws_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_ws_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NCW, NS, STAB>;
-    const size_t smem = 16 * NS + (STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0) + (size_t)NS * p.SW * 4;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
-    if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: warp-specialised stage ring exceeds shared memory");
-    int sms = 148;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    const uint64_t groups = p.g1 - p.g0;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)sms));
-    kern<<<(unsigned)blocks, (NCW + 1) * 32, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
-}
-
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1>
 void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_ws3_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO>;
-    constexpr int NCHUNK = (BlockGeom<FT, P, WQ>::NBLK + 31) / 32;
-    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * p.Cp * 4;
+    auto kern = step_packed_ws3_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO, SPLIT>;
+    constexpr int NCHUNK = WsGeom<FT, P, WQ, SPLIT>::NCHUNK;
+    constexpr int NT = (NCHUNK * NGRP + 2) * 32;
+    const size_t out_bytes = SPLIT == 1 ? (size_t)p.Cp * 4 : (size_t)WsGeom<FT, P, WQ, SPLIT>::ROWS * WQ * 4;
+    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * out_bytes;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1006,10 +991,10 @@ void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
     if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: stage rings exceed shared memory");
     int sms = 148, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCHUNK * NGRP + 2) * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     const uint64_t groups = p.g1 - p.g0;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
-    launch_pdl(h, kern, dim3((unsigned)blocks), dim3((NCHUNK * NGRP + 2) * 32), smem, p,
+    const uint64_t pairs = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms / SPLIT));
+    launch_pdl(h, kern, dim3((unsigned)(pairs * SPLIT)), dim3(NT), smem, p,
                (const uint32_t*)h->pk[h->cur], h->pk[h->cur ^ 1], (const uint32_t*)h->bnd[h->cur], h->bnd[h->cur ^ 1]);
 }
 
@@ -1122,14 +1107,7 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     if (P.tag != kTagNone) {
         const int dg = moore ? 8 : 4;
     // Micro-block kernels: the persistent TMA-in/TMA-out warp-specialised kernel
-    // (ws3) where a group's chunks fit one CTA, else the chunk-rotating ws kernel.
-#define NBB_WS(TAG, FT, BP, W, WD, NCW, NS, ST)                                                         \
-    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
-        if (conway && dg == 8) return launch_packed_ws_t<true, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);    \
-        if (conway) return launch_packed_ws_t<true, 4, WD, FT, BP, W, NCW, NS, ST>(h, p);               \
-        if (dg == 8) return launch_packed_ws_t<false, 8, WD, FT, BP, W, NCW, NS, ST>(h, p);             \
-        return launch_packed_ws_t<false, 4, WD, FT, BP, W, NCW, NS, ST>(h, p);                          \
-    }
+    // (ws3); groups with more chunks than a CTA has warps run on CTA pairs (SPLIT).
 #define NBB_WS3(TAG, FT, BP, W, WD, NGRP, NS, NO)                                                        \
     if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
         if (conway && dg == 8) return launch_packed_ws3_t<true, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);  \
@@ -1142,8 +1120,13 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
         NBB_WS3(kTagCarpet, CarpetTag, 1, 64, false, 1, 4, 2)
         NBB_WS3(kTagVicsek, VicsekTag, 2, 25, false, 16, 24, 16)
         NBB_WS3(kTagH, HTag, 1, 49, false, 2, 6, 4)
-        NBB_WS(kTagCandy, CandyTag, 1, 144, true, 27, 2, false)
-#undef NBB_WS
+        if (P.tag == kTagCandy && P.wq == 144 && P.wide) {
+            // 54 chunks per group: CTA pairs, each computing half the rows
+            if (conway && dg == 8) return launch_packed_ws3_t<true, 8, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
+            if (conway) return launch_packed_ws3_t<true, 4, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
+            if (dg == 8) return launch_packed_ws3_t<false, 8, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
+            return launch_packed_ws3_t<false, 4, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
+        }
 #undef NBB_WS3
         raise(NBBGPU_ERR_CUDA, "internal: micro-block plan without a kernel");
     }

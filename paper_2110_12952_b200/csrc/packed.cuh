@@ -231,55 +231,6 @@ __device__ __forceinline__ uint32_t cell_word(const uint8_t* Sb, const void* nbr
     return apply_rule_bits<CONWAY>(cnt, own, KB, KS);
 }
 
-// The bit-sliced step of every cell of micro-block `blk` (blocks.cuh): NB own
-// words and NE external words in registers, compile-time wiring, results to Dg.
-template <class FT, int P, int WQ, bool CONWAY, int DEG, bool STAB>
-__device__ __forceinline__ void block_words(const uint8_t* Sb, const uint32_t* btab, uint32_t blk,
-                                            uint32_t* Dg, uint32_t vmask, const uint32_t (&KB)[9],
-                                            const uint32_t (&KS)[9]) {
-    using W = Wiring<FT, P>;
-    constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
-    constexpr int BPR = WQ / BW;
-    const uint32_t by = blk / BPR, bx = blk - by * BPR;
-    const uint32_t base = by * (BH * WQ) + bx * BW;
-    const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
-    uint32_t own[NB];
-    static_for<NB>([&](auto n) {
-        constexpr int N = decltype(n)::value;
-        own[N] = Sw[(N / BW) * WQ + N % BW];
-    });
-    uint32_t ext[NEP];
-    const uint4* t4 = reinterpret_cast<const uint4*>(btab) + (size_t)blk * (NEP / 4);
-    static_for<NEP / 4>([&](auto e4) {
-        constexpr int E = decltype(e4)::value;
-        uint4 v;
-        if constexpr (STAB) v = t4[E];  // table staged in shared memory
-        else v = __ldg(t4 + E);
-        ext[4 * E + 0] = *reinterpret_cast<const uint32_t*>(Sb + v.x);
-        ext[4 * E + 1] = *reinterpret_cast<const uint32_t*>(Sb + v.y);
-        ext[4 * E + 2] = *reinterpret_cast<const uint32_t*>(Sb + v.z);
-        ext[4 * E + 3] = *reinterpret_cast<const uint32_t*>(Sb + v.w);
-    });
-    uint32_t* Dw = Dg + base;
-    static_for<NB>([&](auto n) {
-        constexpr int N = decltype(n)::value;
-        uint32_t x[8];
-        static_for<8>([&](auto j) {
-            constexpr int J = decltype(j)::value;
-            constexpr int SJ = W::d.src[N][J];
-            if constexpr (J >= DEG || SJ == kWireAbsent) x[J] = 0u;
-            else if constexpr (SJ >= 0) x[J] = own[SJ];
-            else x[J] = ext[-SJ - 2];
-        });
-        const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
-        Dw[(N / BW) * WQ + N % BW] = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
-    });
-}
-
-// One step over the owned groups.  Per CTA a 2-stage ring: the record + halo words
-// of the next group are in flight (cp.async.bulk, mbarrier completion) while the C
-// words of the current one are computed; results go straight to HBM with
-// coalesced 32-bit stores.
 template <class FT, int P, int WQ>
 struct BlockGeom {
     static constexpr int NBLK = (WQ / Wiring<FT, P>::BW) * (WQ / Wiring<FT, P>::BH);
@@ -374,84 +325,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 
-// Warp-specialised persistent variant of the micro-block step (one CTA per SM):
-// a producer warp streams group records + halo words into an NS-stage ring with
-// cp.async.bulk (full barriers carry the transaction bytes); NCW consumer warps
-// each take 32-block chunks of every group and release a stage through its empty
-// barrier -- no CTA-wide barrier in the loop, so warps drift up to NS-1 groups
-// apart instead of waiting for the slowest one.  The micro-block table is staged in
-// shared memory once (STAB) or read through L1.
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NCW, int NS, bool STAB>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1)
-step_packed_ws_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                      const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
-    (void)bsrc;
-    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
-    constexpr int NCHUNK = (NBLK + 31) / 32;
-    constexpr uint32_t TABB = STAB ? BlockGeom<FT, P, WQ>::TAB_BYTES : 0u;
-    extern __shared__ __align__(16) uint8_t sm[];
-    const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
-    const uint32_t* tab = STAB ? reinterpret_cast<const uint32_t*>(sm + 16 * NS) : p.btab;
-    uint8_t* st = sm + 16 * NS + TABB;
-    const uint32_t stage_bytes = p.SW * 4;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-    uint32_t KB[9], KS[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-    }
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, NCW);
-        }
-        mbar_fence_init();
-    }
-    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
-    if constexpr (STAB) {
-        for (uint32_t i = tid; i < TABB / 16; i += (NCW + 1) * 32)
-            reinterpret_cast<uint4*>(sm + 16 * NS)[i] = __ldg(reinterpret_cast<const uint4*>(p.btab) + i);
-    }
-    __syncthreads();
-
-    const uint32_t rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
-    if (warp == NCW) {  // ---- producer -------------------------------------------------
-        if (lane == 0) {
-            uint32_t i = 0;
-            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
-                const uint32_t s = i % NS;
-                if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
-                const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
-                mbar_expect_tx(bar, rec_bytes + halo_bytes);
-                bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
-                if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
-            }
-        }
-        return;
-    }
-    // ---- consumers -----------------------------------------------------------------
-    uint32_t i = 0;
-    for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
-        const uint32_t s = i % NS;
-        mbar_wait(full0 + 8 * s, (i / NS) & 1u);
-        const uint8_t* Sb = st + s * stage_bytes;
-        const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
-        uint32_t* D = dst + (uint64_t)g * p.Cp;
-        // chunk c of this group -> warp (c + i) mod NCW: the odd chunks rotate
-        for (int c = (int)((warp + NCW - (i % NCW)) % NCW); c < NCHUNK; c += NCW) {
-            const uint32_t blk = (uint32_t)c * 32 + lane;
-            if (blk < (uint32_t)NBLK) block_words<FT, P, WQ, CONWAY, DEG, STAB>(Sb, tab, blk, D, vmask, KB, KS);
-        }
-        if ((uint32_t)warp == i % NCW)  // boundary plane of the new state
-            for (uint32_t m = lane; m < p.nSrc; m += 32)
-                bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * s);
-    }
-}
-
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -510,13 +383,27 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
 //                   results go to an NO-deep shared output ring;
 //   storer warp   : one cp.async.bulk shared->global store per finished group.
 // No CTA-wide barrier in the loop; stores leave as whole 26 KB records.
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
-__global__ void __launch_bounds__(((BlockGeom<FT, P, WQ>::NBLK + 31) / 32 * NGRP + 2) * 32, 1)
+// SPLIT > 1 (groups with more chunks than a CTA has warps, e.g. candy: 54): SPLIT
+// consecutive CTAs share a group, CTA half h loading the whole record but computing
+// and storing only its 1/SPLIT of the micro-block rows (a contiguous slice of the
+// output record).
+template <class FT, int P, int WQ, int SPLIT>
+struct WsGeom {
+    static constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK / SPLIT;  // blocks per CTA
+    static constexpr int NCHUNK = (NBLK + 31) / 32;
+    static constexpr int ROWS = WQ / SPLIT;                          // cell rows per CTA
+    static_assert(SPLIT == 1 || (Wiring<FT, P>::BH == 1 && WQ % SPLIT == 0), "SPLIT needs P = 1 row blocks");
+};
+
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1>
+__global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2) * 32, 1)
 step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                        const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
+    (void)bsrc;
     using W = Wiring<FT, P>;
-    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
-    constexpr int NCHUNK = (NBLK + 31) / 32;
+    using WG = WsGeom<FT, P, WQ, SPLIT>;
+    constexpr int NBLK = WG::NBLK;
+    constexpr int NCHUNK = WG::NCHUNK;
     constexpr int NCW = NCHUNK * NGRP;
     constexpr int NEP = W::NEP;
     extern __shared__ __align__(16) uint8_t sm[];
@@ -524,6 +411,11 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
     uint8_t* st = sm + 16 * (NS + NO);
     const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4;
+    // output slice of this CTA: the whole record (SPLIT = 1), or rows [half*ROWS, ...)
+    const uint32_t half = blockIdx.x % SPLIT, pair = blockIdx.x / SPLIT, npairs = gridDim.x / SPLIT;
+    const uint32_t out_words = SPLIT == 1 ? p.Cp : (uint32_t)(WG::ROWS * WQ);
+    const uint32_t out_off = SPLIT == 1 ? 0u : half * out_words;
+    const uint32_t out_bytes = out_words * 4;
     uint8_t* outs = st + NS * stage_bytes;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -539,8 +431,9 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         mbar_fence_init();
     }
     if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
-    for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
-        reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * rec_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
+    if (SPLIT == 1)
+        for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
+            reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * out_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
     fence_proxy_async_smem();
     __syncthreads();
     pdl_wait();     // the prologue above overlapped the previous kernel's tail (PDL)
@@ -549,7 +442,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     if (warp == NCW) {  // ---- producer -------------------------------------------------
         if (lane == 0) {
             uint32_t i = 0;
-            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+            for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
                 const uint32_t s = i % NS;
                 if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
                 const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
@@ -564,10 +457,10 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     if (warp == NCW + 1) {  // ---- storer ---------------------------------------------------
         if (lane == 0) {
             uint32_t i = 0;
-            for (uint32_t g = p.g0 + blockIdx.x; g < p.g1; g += gridDim.x, ++i) {
+            for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
                 const uint32_t o = i % NO;
                 mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);
-                bulk_s2g(dst + (uint64_t)g * p.Cp, smem_u32(outs + o * rec_bytes), rec_bytes);
+                bulk_s2g(dst + (uint64_t)g * p.Cp + out_off, smem_u32(outs + o * out_bytes), out_bytes);
                 bulk_wait_read_all();  // the output record may be rewritten
                 mbar_arrive(oempty0 + 8 * o);
             }
@@ -583,8 +476,9 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
     const int set = warp / NCHUNK, c = warp - set * NCHUNK;
-    const uint32_t blk = (uint32_t)c * 32 + lane;
-    const bool active = blk < (uint32_t)NBLK;
+    const uint32_t lblk = (uint32_t)c * 32 + lane;
+    const bool active = lblk < (uint32_t)NBLK;
+    const uint32_t blk = half * (uint32_t)NBLK + lblk;
     uint32_t toff[NEP];
     {
         const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
@@ -595,15 +489,16 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         });
     }
     uint32_t i = (uint32_t)set;
-    for (uint32_t g = p.g0 + blockIdx.x + (uint32_t)set * gridDim.x; g < p.g1; g += NGRP * gridDim.x, i += NGRP) {
+    for (uint32_t g = p.g0 + pair + (uint32_t)set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
         const uint32_t s = i % NS, o = i % NO;
         mbar_wait(full0 + 8 * s, (i / NS) & 1u);
         if (i >= NO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
         const uint8_t* Sb = st + s * stage_bytes;
-        uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * rec_bytes);
+        // block_words_r indexes the whole record: shift the slice base back by out_off
+        uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * out_bytes) - out_off;
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
         if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
-        if (c == 0)  // boundary plane of the new state
+        if (c == 0 && half == 0)  // boundary plane of the new state
             for (uint32_t m = lane; m < p.nSrc; m += 32)
                 bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
         fence_proxy_async_smem();  // the bulk store reads Do through the async proxy
