@@ -1088,7 +1088,7 @@ void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore)
     // halo words of every owned group from the boundary plane (separate kernel);
     // the step kernel bulk-loads them with each group record
     if (P.nH > 0) {
-        const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0);
+        const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0, P.nD);
         // (the neighbour tile comes from the static ntab: an ALU carry walk with
         //  compile-time tables measured slower, T r=20 0.178 vs 0.148 ms per step)
         if (halo_use_wide((uint32_t)P.nH, p.g1 - p.g0))

@@ -107,55 +107,70 @@ __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint
     if (lane < SPW && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
 }
 
-// Large halos (carpet, H: ~200-330 slots per tile): one task per group walking the
-// used directions.  ONE coalesced load gives every lane its neighbour tile in a
-// direction; the direction's slots (contiguous: the plan sorts slots by direction)
-// then cost one load + shift + ballot each, 16 loads in flight per round trip.
+// Large halos (carpet, H: ~200-330 slots per tile): one task per (group, used
+// direction).  A direction with many slots (a tile edge) is gathered TRANSPOSED:
+// lane = slot, and a loop over the 32 tiles b reads B[t2_b][m_slot] (coalesced over
+// the slots) and sets bit b -- ~7 instructions per tile for 32 slots, instead of a
+// warp-wide load + ballot per slot.  Directions with a few slots (corners) keep the
+// lane = tile ballot form.
 template <bool NC>
 __device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
-                                               uint32_t g, uint32_t lane) {
+                                               uint32_t g, int ds, uint32_t lane) {
     const uint32_t t = g * 32 + lane;
     uint32_t* Hg = H + (uint64_t)g * p.nHp;
-    for (int ds = 0; ds < p.nD; ++ds) {
-        const uint32_t t2 = t < p.T ? __ldg(p.ntab + (uint64_t)ds * p.T + t) : kNoTile;
-        const bool valid = t2 != kNoTile;
-        const uint32_t* base = bsrc + (uint64_t)(valid ? t2 >> 5 : 0) * p.nSrc;
-        const uint32_t sh = t2 & 31;
-        const uint32_t j_end = p.dfirst[ds + 1];
-        for (uint32_t j0 = p.dfirst[ds]; j0 < j_end; j0 += 32) {
-            uint32_t mine = 0;
-            const uint32_t my_m = j0 + lane < j_end ? (__ldg(p.slot + j0 + lane) & 0xFFFFu) : 0u;
-            for (uint32_t j1 = 0; j1 < 32 && j0 + j1 < j_end; j1 += 16) {
-                uint32_t v[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_m, j1 + u);
-                    v[u] = (j0 + j1 + u < j_end && valid) ? ld_bnd<NC>(base + m) >> sh : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
-                    if (lane == j1 + u) mine = word;
+    const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)ds * p.T + t)) : kNoTile;  // lane = tile
+    const uint32_t j_beg = p.dfirst[ds], j_end = p.dfirst[ds + 1];
+    if (j_end - j_beg >= 8) {
+        for (uint32_t j0 = j_beg; j0 < j_end; j0 += 32) {
+            const uint32_t j = j0 + lane;  // lane = slot
+            const uint32_t my_m = j < j_end ? (__ldg(p.slot + j) & 0xFFFFu) : 0u;
+            uint32_t h = 0;
+#pragma unroll 8
+            for (int b = 0; b < 32; ++b) {
+                const uint32_t tb = __shfl_sync(0xFFFFFFFFu, t2, b);
+                if (tb != kNoTile) {  // warp-uniform
+                    const uint32_t w = ld_bnd<NC>(bsrc + (size_t)(tb >> 5) * p.nSrc + my_m);
+                    h |= ((w >> (tb & 31)) & 1u) << b;
                 }
             }
-            if (j0 + lane < j_end) Hg[j0 + lane] = mine;
+            if (j < j_end) Hg[j] = h;
         }
+        return;
     }
+    const bool valid = t2 != kNoTile;
+    const uint32_t* base = bsrc + (size_t)(valid ? t2 >> 5 : 0) * p.nSrc;
+    const uint32_t sh = t2 & 31;
+    const uint32_t my_m = j_beg + lane < j_end ? (__ldg(p.slot + j_beg + lane) & 0xFFFFu) : 0u;
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_m, u);
+        v[u] = (j_beg + u < j_end && valid) ? ld_bnd<NC>(base + m) >> sh : 0u;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
+        if (lane == (uint32_t)u) mine = word;
+    }
+    if (j_beg + lane < j_end) Hg[j_beg + lane] = mine;
 }
 
-// large halo and enough groups for latency hiding -> one warp per group walking the
-// directions (measured: H r=11 0.357 vs 0.408 ms/step); else 4 slots per warp
+// large halos -> tasks per (group, direction) with transposed edge gathers; small
+// halos (triangle, Vicsek: 4-8 slots) -> tasks of 4 slots, lane = tile
 __host__ __device__ __forceinline__ bool halo_use_wide(uint32_t nH, uint32_t groups) {
-    return nH > 32 && groups >= 8192;
+    (void)groups;
+    return nH > 32;
 }
-__host__ __device__ __forceinline__ uint64_t halo_tasks(uint32_t nH, uint32_t groups) {
-    return halo_use_wide(nH, groups) ? (uint64_t)groups : (uint64_t)groups * ((nH + 3) / 4);
+__host__ __device__ __forceinline__ uint64_t halo_tasks(uint32_t nH, uint32_t groups, int nD) {
+    return halo_use_wide(nH, groups) ? (uint64_t)groups * (uint32_t)nD : (uint64_t)groups * ((nH + 3) / 4);
 }
 
 template <bool NC>
 __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
                                           uint64_t wi, uint32_t lane) {
-    if (halo_use_wide(p.nH, p.g1 - p.g0)) halo_wide_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
+    if (halo_use_wide(p.nH, p.g1 - p.g0))
+        halo_wide_task<NC>(p, bsrc, H, p.g0 + (uint32_t)(wi / (uint32_t)p.nD), (int)(wi % (uint32_t)p.nD), lane);
     else halo4_task<NC>(p, bsrc, H, wi, lane);
 }
 
@@ -167,11 +182,16 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
     const uint32_t lane = threadIdx.x & 31;
     pdl_wait();     // bsrc comes from the previous step kernel
     pdl_trigger();  // the step kernel may launch and run its prologue
-    const uint64_t nw = WIDE_HALO ? (uint64_t)(p.g1 - p.g0) : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
+    const uint64_t nw = WIDE_HALO ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
+                                  : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        if constexpr (WIDE_HALO) halo_wide_task<true>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
-        else halo4_task<true, SPW>(p, bsrc, H, wi, lane);
+        if constexpr (WIDE_HALO) {
+            const uint32_t w32 = (uint32_t)wi, gi = w32 / (uint32_t)p.nD;
+            halo_wide_task<true>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
+        } else {
+            halo4_task<true, SPW>(p, bsrc, H, wi, lane);
+        }
     }
 }
 
@@ -582,7 +602,7 @@ step_packed_fused_kernel(const PackedStepParams p, uint32_t* P0, uint32_t* P1, u
     const uint32_t n_mine = blockIdx.x < ng ? (ng - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
     const uint64_t nwarps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    const uint64_t htasks = p.nH ? halo_tasks(p.nH, ng) : 0;
+    const uint64_t htasks = p.nH ? halo_tasks(p.nH, ng, p.nD) : 0;
 
     uint32_t KB[9], KS[9];
 #pragma unroll
