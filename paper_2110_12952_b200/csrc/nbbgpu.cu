@@ -296,189 +296,7 @@ int choose_tile_level(const HostFrac& F) {
 }
 
 
-// ---------------------------------------------------------------------------
-// Packed plan (packed.cuh): one halo-slot set (Moore; von Neumann's is a subset),
-// boundary sources, [C][8] stage byte offsets for both neighbourhoods.
-// ---------------------------------------------------------------------------
-constexpr int kPackedMaxCells = 24576;  // two smem stages of <= 96 KB
-
-struct PackedPlan {
-    int q = -1, wq = 1, C = 1, Cp = 4, L = 0;
-    int64_t Wc = 0, Hc = 0, T = 0, NG = 0, sq = 1;
-    int nH = 0, nHp = 0, nD = 0, nSrc = 0;
-    int8_t dlist[8] = {0};
-    std::vector<uint8_t> slotD;     // per slot: direction D = (dy+1)*3 + dx+1
-    std::vector<uint32_t> slot;     // per slot: (D << 24) | (direction slot << 16) | boundary source m
-    std::vector<uint32_t> srcidx;   // per boundary source: local cell
-    std::vector<uint32_t> loc;      // per local cell: (yl << 16) | xl  (level-q lambda)
-    std::vector<uint32_t> nbr[2];   // [moore] C x 8 stage byte offsets
-    bool wide = false;              // offsets do not fit 16 bits
-    uint32_t SW = 0;                // words per smem stage
-    uint32_t lastmask = 0xFFFFFFFFu;
-    int tag = 0;                    // micro-block descriptor (kTag*), 0 = generic program
-    int bP = 0;                     // micro-block level
-    std::vector<uint32_t> btab;     // micro-block external offsets (blocks.cuh)
-};
-
-// descriptors with compile-time micro-block wiring (blocks.cuh)
-enum { kTagNone = 0, kTagTriangle = 1, kTagCarpet = 2, kTagVicsek = 3, kTagH = 4, kTagCandy = 5 };
-
-template <class FT>
-bool matches_tag(const HostFrac& F) {
-    if (F.k != FT::K || F.s != FT::S) return false;
-    for (int i = 0; i < FT::K; ++i)
-        if (F.gx[i] != FT::GX[i] || F.gy[i] != FT::GY[i]) return false;
-    return true;
-}
-
-int descriptor_tag(const HostFrac& F) {
-    if (matches_tag<TriangleTag>(F)) return kTagTriangle;
-    if (matches_tag<CarpetTag>(F)) return kTagCarpet;
-    if (matches_tag<VicsekTag>(F)) return kTagVicsek;
-    if (matches_tag<HTag>(F)) return kTagH;
-    if (matches_tag<CandyTag>(F)) return kTagCandy;
-    return kTagNone;
-}
-
-// (tag, tile width) pairs with an instantiated micro-block kernel, and their block level
-int block_level_for(int tag, int wq) {
-    switch (tag) {
-        case kTagTriangle: return (wq == 27 || wq == 81) ? 2 : 0;
-        case kTagCarpet: return wq == 64 ? 1 : 0;
-        case kTagVicsek: return wq == 25 ? 2 : 0;
-        case kTagH: return wq == 49 ? 1 : 0;
-        case kTagCandy: return wq == 144 ? 1 : 0;
-        default: return 0;
-    }
-}
-
-// per micro-block: stage byte offsets of its NE external positions (blocks.cuh)
-template <class FT, int P>
-std::vector<uint32_t> build_block_table(const HostFrac& F, int q, int wq, int Cp, int nHp,
-                                        const std::map<std::tuple<int, int, int>, int>& key8) {
-    using W = Wiring<FT, P>;
-    const int bpr = wq / W::BW, bpc = wq / W::BH;
-    const int64_t tside = F.spow[q];
-    const uint32_t zero = 4u * (uint32_t)(Cp + nHp);
-    std::vector<uint32_t> t((size_t)bpr * bpc * W::NEP, zero);
-    for (int by = 0; by < bpc; ++by)
-        for (int bx = 0; bx < bpr; ++bx) {
-            // embedded origin of the block's s^P box = lambda(cell 0) - its in-box position
-            int64_t lx0, ly0;
-            F.lambda(bx * W::BW, by * W::BH, lx0, ly0, q);
-            lx0 -= W::d.ex[0];
-            ly0 -= W::d.ey[0];
-            for (int e = 0; e < W::NE; ++e) {
-                const int64_t X = lx0 + W::d.epx[e], Y = ly0 + W::d.epy[e];
-                const int Dx = X < 0 ? -1 : (X >= tside ? 1 : 0), Dy = Y < 0 ? -1 : (Y >= tside ? 1 : 0);
-                int64_t ncx, ncy;
-                uint32_t off = zero;
-                if (F.nu(X - Dx * tside, Y - Dy * tside, ncx, ncy, q)) {
-                    if (Dx == 0 && Dy == 0) {
-                        off = 4u * (uint32_t)(ncy * wq + ncx);
-                    } else {
-                        auto it = key8.find(std::make_tuple((Dy + 1) * 3 + Dx + 1, (int)ncy, (int)ncx));
-                        if (it == key8.end()) raise(NBBGPU_ERR_CUDA, "internal: micro-block external without a halo slot");
-                        off = 4u * (uint32_t)(Cp + it->second);
-                    }
-                }
-                t[((size_t)by * bpr + bx) * W::NEP + e] = off;
-            }
-        }
-    return t;
-}
-
-PackedPlan build_packed_plan(const HostFrac& F, int q) {
-    if (q < 2 || (q & 1) || q > F.r) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "packed tile level must be even, 2 <= q <= level");
-    const TilePlan P8 = build_plan(F, q, 8), P4 = build_plan(F, q, 4);
-    PackedPlan PP;
-    PP.q = q; PP.wq = P8.wq; PP.C = P8.C; PP.Cp = (P8.C + 3) & ~3; PP.L = P8.L;
-    PP.Wc = P8.Wc; PP.Hc = P8.Hc; PP.T = P8.Wc * P8.Hc; PP.NG = (PP.T + 31) / 32;
-    PP.sq = F.spow[q];
-    PP.nH = P8.nH; PP.nD = P8.nD;
-    for (int i = 0; i < 8; ++i) PP.dlist[i] = P8.dlist[i];
-    std::map<int, int> m_of;
-    std::map<std::tuple<int, int, int>, int> key8;
-    for (int j = 0; j < P8.nH; ++j) {
-        const int cell = P8.ha[j] * P8.wq + P8.hc[j];
-        auto it = m_of.find(cell);
-        int m;
-        if (it == m_of.end()) { m = (int)PP.srcidx.size(); m_of[cell] = m; PP.srcidx.push_back((uint32_t)cell); }
-        else m = it->second;
-        PP.slot.push_back(((uint32_t)P8.hD[j] << 24) | ((uint32_t)P8.hDslot[j] << 16) | (uint32_t)m);
-        PP.slotD.push_back(P8.hD[j]);
-        key8[std::make_tuple((int)P8.hD[j], (int)P8.ha[j], (int)P8.hc[j])] = j;
-    }
-    PP.nSrc = (int)PP.srcidx.size();
-    // stage: [0, Cp) record | [Cp, Cp + nHp) halo words | zero word at Cp + nHp
-    PP.nHp = (PP.nH + 3) & ~3;
-    const uint32_t zero = (uint32_t)(PP.Cp + PP.nHp);
-    PP.wide = 4ull * zero > 0xFFFFull;
-    PP.SW = zero + 4;
-    PP.nbr[1].resize((size_t)PP.C * 8);
-    PP.nbr[0].resize((size_t)PP.C * 8);
-    for (size_t e = 0; e < PP.nbr[1].size(); ++e) {
-        const uint32_t v = P8.nbr[e] / 4;
-        const uint32_t word = v < (uint32_t)PP.C ? v : (v == (uint32_t)(P8.C + P8.nH) ? zero : (uint32_t)PP.Cp + v - PP.C);
-        PP.nbr[1][e] = 4 * word;
-    }
-    for (size_t e = 0; e < PP.nbr[0].size(); ++e) {
-        const uint32_t v = P4.nbr[e] / 4;
-        uint32_t word;
-        if (v < (uint32_t)PP.C) word = v;
-        else if (v == (uint32_t)(P4.C + P4.nH)) word = zero;
-        else {
-            const int j4 = (int)(v - PP.C);
-            auto it = key8.find(std::make_tuple((int)P4.hD[j4], (int)P4.ha[j4], (int)P4.hc[j4]));
-            if (it == key8.end()) raise(NBBGPU_ERR_CUDA, "internal: von Neumann halo slot missing from the Moore plan");
-            word = (uint32_t)PP.Cp + (uint32_t)it->second;
-        }
-        PP.nbr[0][e] = 4 * word;
-    }
-    if (PP.T % 32) PP.lastmask = (1u << (PP.T % 32)) - 1u;
-    // micro-block program for descriptors with compile-time wiring
-    // (NBBGPU_GENERIC=1 forces the table-driven program, for comparisons)
-    const int tag = getenv("NBBGPU_GENERIC") ? kTagNone : descriptor_tag(F);
-    if (block_level_for(tag, PP.wq) > 0) {
-        PP.tag = tag;
-        switch (tag) {
-            case kTagTriangle: PP.btab = build_block_table<TriangleTag, 2>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
-            case kTagCarpet: PP.btab = build_block_table<CarpetTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
-            case kTagVicsek: PP.btab = build_block_table<VicsekTag, 2>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
-            case kTagH: PP.btab = build_block_table<HTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
-            case kTagCandy: PP.btab = build_block_table<CandyTag, 1>(F, q, PP.wq, PP.Cp, PP.nHp, key8); break;
-        }
-    }
-    PP.loc.resize(PP.C);
-    for (int i = 0; i < PP.C; ++i) {
-        int64_t xl, yl;
-        F.lambda(i % PP.wq, i / PP.wq, xl, yl, q);
-        PP.loc[i] = ((uint32_t)yl << 16) | (uint32_t)xl;
-    }
-    return PP;
-}
-
-// Tile level of the packed kernel: the largest even q whose group record fits the
-// smem ring and still leaves >= 4 groups per SM; else the smallest feasible q.
-// NBBGPU_PACKED_Q overrides (tuning).
-int choose_packed_level(const HostFrac& F) {
-    if (const char* e = getenv("NBBGPU_PACKED_Q")) {
-        const int q = atoi(e);
-        if (q >= 2 && !(q & 1) && q <= F.r) return q;
-    }
-    int best = -1, fallback = -1;
-    for (int q = 2; q <= F.r; q += 2) {
-        const int64_t wq = HostFrac::ipow(F.k, q / 2);
-        if (wq * wq > kPackedMaxCells) break;
-        if (F.spow[q] > 65535) break;
-        const int64_t T = (F.w / wq) * (F.h / wq);
-        if (T >= ((int64_t)1 << 32) - 64) continue;
-        const int64_t NG = (T + 31) / 32;
-        if (fallback < 0) fallback = q;
-        if (NG >= 4 * 148) best = q;
-    }
-    return best >= 0 ? best : fallback;
-}
+#include "packed_plan.inc"
 
 }  // namespace
 
@@ -653,488 +471,7 @@ void prof_mark(nbbgpu_t h) {
 }
 int layout_of_kernel(int k) { return k == NBBGPU_KERNEL_PACKED ? 1 : 0; }
 
-// ---------------------------------------------------------------------------
-// packed layout: tables, buffers, conversions (packed.cuh)
-// ---------------------------------------------------------------------------
-PackedGeom packed_geom(nbbgpu_t h) {
-    const PackedPlan& P = h->pp;
-    PackedGeom G{};
-    G.f = h->frac;
-    G.q = (uint32_t)P.q; G.WQ = (uint32_t)P.wq; G.C = (uint32_t)P.C; G.Cp = (uint32_t)P.Cp;
-    G.Wc = (uint32_t)P.Wc; G.Hc = (uint32_t)P.Hc; G.L = (uint32_t)P.L;
-    G.T = (uint32_t)P.T; G.NG = (uint32_t)P.NG; G.sq = (uint32_t)P.sq;
-    G.w = (uint64_t)h->hf.w;
-    return G;
-}
-
-uint64_t packed_words(const PackedPlan& P) { return (uint64_t)P.NG * P.Cp; }
-uint64_t bnd_words(const PackedPlan& P) { return std::max<uint64_t>(1, (uint64_t)P.NG * P.nSrc); }
-
-template <class T>
-void dmalloc_cap(T*& p, size_t bytes, const char* what) {
-    if (cudaMalloc((void**)&p, std::max<size_t>(bytes, 4)) != cudaSuccess) {
-        cudaGetLastError();
-        p = nullptr;
-        raise(NBBGPU_ERR_CAPACITY, std::string(what) + " exceeds the device memory (memory cap)");
-    }
-}
-
-// plan tables on the device (once per handle)
-void ensure_packed_tables(nbbgpu_t h) {
-    if (h->pp_built) return;
-    if (h->pq < 2) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
-    PackedPlan P = build_packed_plan(h->hf, h->pq);
-    uint64_t tb = 0;
-    for (int m = 0; m < 2; ++m) {
-        if (P.wide) {
-            dmalloc_cap(h->d_pnbr[m], P.nbr[m].size() * 4, "neighbour table");
-            CK(cudaMemcpy(h->d_pnbr[m], P.nbr[m].data(), P.nbr[m].size() * 4, cudaMemcpyHostToDevice));
-            tb += P.nbr[m].size() * 4;
-        } else {
-            std::vector<uint16_t> n16(P.nbr[m].begin(), P.nbr[m].end());
-            dmalloc_cap(h->d_pnbr[m], n16.size() * 2, "neighbour table");
-            CK(cudaMemcpy(h->d_pnbr[m], n16.data(), n16.size() * 2, cudaMemcpyHostToDevice));
-            tb += n16.size() * 2;
-        }
-    }
-    dmalloc_cap(h->d_pslot, P.slot.size() * 4, "halo table");
-    if (!P.slot.empty()) CK(cudaMemcpy(h->d_pslot, P.slot.data(), P.slot.size() * 4, cudaMemcpyHostToDevice));
-    dmalloc_cap(h->d_psrc, P.srcidx.size() * 4, "halo table");
-    if (!P.srcidx.empty()) CK(cudaMemcpy(h->d_psrc, P.srcidx.data(), P.srcidx.size() * 4, cudaMemcpyHostToDevice));
-    if (!P.btab.empty()) {
-        dmalloc_cap(h->d_pbtab, P.btab.size() * 4, "micro-block table");
-        CK(cudaMemcpy(h->d_pbtab, P.btab.data(), P.btab.size() * 4, cudaMemcpyHostToDevice));
-        tb += P.btab.size() * 4;
-    }
-    dmalloc_cap(h->d_ploc, P.loc.size() * 4, "lambda table");
-    CK(cudaMemcpy(h->d_ploc, P.loc.data(), P.loc.size() * 4, cudaMemcpyHostToDevice));
-    dmalloc_cap(h->d_gbar, 16, "grid barrier");
-    CK(cudaMemsetAsync(h->d_gbar, 0, 16, h->stream));
-    dmalloc_cap(h->d_phalo, (uint64_t)P.NG * P.nHp * 4, "halo words");
-    CK(cudaMemsetAsync(h->d_phalo, 0, std::max<uint64_t>(4, (uint64_t)P.NG * P.nHp * 4), h->stream));
-    tb += (uint64_t)P.NG * P.nHp * 4;
-    const uint64_t nt = (uint64_t)P.nD * P.T;
-    dmalloc_cap(h->d_pntab, nt * 4, "coarse neighbour table");
-    tb += (P.slot.size() + P.srcidx.size() + P.loc.size() + nt) * 4;
-    if (P.nD > 0) {
-        const int8_t* d = P.dlist;
-#define NBB_CALL(K, S, ...) build_ntab_linear_kernel<K, S><<<grid_for(P.T, 256), 256, 0, h->stream>>>(h->frac, P.L, (uint32_t)P.Wc, (uint32_t)P.Hc, P.nD, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], h->d_pntab)
-        NBB_DISPATCH_KS(h->hf);
-#undef NBB_CALL
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(h->stream));
-    }
-    h->pp = std::move(P);
-    h->pp_built = true;
-    h->packed_table_bytes = tb;
-    h->bytes_held += tb;
-    h->pg0 = 0;
-    h->pg1 = h->pp.NG;
-}
-
-void free_packed_state(nbbgpu_t h) {
-    for (int b = 0; b < 2; ++b) {
-        if (h->pk[b]) { cudaFree(h->pk[b]); h->pk[b] = nullptr; h->bytes_held -= packed_words(h->pp) * 4; }
-        if (h->bnd[b]) { cudaFree(h->bnd[b]); h->bnd[b] = nullptr; h->bytes_held -= bnd_words(h->pp) * 4; }
-    }
-}
-
-void free_byte_state(nbbgpu_t h) {
-    for (int b = 0; b < 2; ++b)
-        if (h->buf[b]) { cudaFree(h->buf[b]); h->buf[b] = nullptr; h->bytes_held -= h->cells + 64; }
-}
-
-void alloc_byte_state(nbbgpu_t h) {
-    for (int b = 0; b < 2; ++b) {
-        if (h->buf[b]) continue;
-        if (cudaMalloc(&h->buf[b], h->cells + 64) != cudaSuccess) {
-            cudaGetLastError();
-            raise(NBBGPU_ERR_CAPACITY, "grid of " + std::to_string(h->cells) + " cells exceeds the device memory (memory cap)");
-        }
-        h->bytes_held += h->cells + 64;
-        CK(cudaMemsetAsync(h->buf[b], 0, h->cells + 64, h->stream));
-    }
-}
-
-void alloc_packed_state(nbbgpu_t h) {
-    ensure_packed_tables(h);
-    for (int b = 0; b < 2; ++b) {
-        if (!h->pk[b]) {
-            dmalloc_cap(h->pk[b], packed_words(h->pp) * 4, "packed grid");
-            h->bytes_held += packed_words(h->pp) * 4;
-            CK(cudaMemsetAsync(h->pk[b], 0, packed_words(h->pp) * 4, h->stream));
-        }
-        if (!h->bnd[b]) {
-            dmalloc_cap(h->bnd[b], bnd_words(h->pp) * 4, "boundary plane");
-            h->bytes_held += bnd_words(h->pp) * 4;
-            CK(cudaMemsetAsync(h->bnd[b], 0, bnd_words(h->pp) * 4, h->stream));
-        }
-    }
-}
-
-void bnd_refresh(nbbgpu_t h) {
-    const PackedPlan& P = h->pp;
-    if (P.nSrc == 0) return;
-    bnd_refresh_kernel<<<grid_for((uint64_t)P.NG * P.nSrc, 256), 256, 0, h->stream>>>(
-        h->pk[h->cur], (uint32_t)P.Cp, (uint32_t)P.NG, (uint32_t)P.nSrc, h->d_psrc, h->bnd[h->cur]);
-    CK(cudaGetLastError());
-}
-
-// coarse rows per staging chunk for byte <-> packed conversions (bounded device memory)
-// (NBBGPU_STAGE_BYTES overrides the 64 MB default; the tests force many chunks)
-int64_t chunk_rows(nbbgpu_t h) {
-    uint64_t stage = 64ull << 20;
-    if (const char* e = getenv("NBBGPU_STAGE_BYTES")) stage = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
-    const uint64_t row_bytes = (uint64_t)h->pp.wq * (uint64_t)h->hf.w;
-    return (int64_t)std::max<uint64_t>(1, stage / std::max<uint64_t>(1, row_bytes));
-}
-
-// device memory is converted in place; host memory (pinned or pageable) streams
-// through two staging chunks: DMA copies on a second stream overlap the
-// conversion kernels on the engine stream (PCIe-bound, ~55 GB/s pinned)
-bool is_device_mem(const void* p) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-struct StagePipe {
-    nbbgpu_t h;
-    cudaStream_t xs = nullptr;
-    cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
-    uint8_t* buf[2] = {nullptr, nullptr};
-    explicit StagePipe(nbbgpu_t hh, uint64_t bytes) : h(hh) {
-        CK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
-            CK(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
-            dmalloc_cap(buf[i], bytes, "staging buffer");
-        }
-    }
-    ~StagePipe() {
-        if (xs) cudaStreamSynchronize(xs);
-        if (h->stream) cudaStreamSynchronize(h->stream);
-        for (int i = 0; i < 2; ++i) {
-            if (buf[i]) cudaFree(buf[i]);
-            if (ready[i]) cudaEventDestroy(ready[i]);
-            if (done[i]) cudaEventDestroy(done[i]);
-        }
-        if (xs) cudaStreamDestroy(xs);
-    }
-};
-
-size_t conv_smem(nbbgpu_t h) { return (size_t)kConvWarps * 32 * h->pp.wq; }
-
-void launch_pack(nbbgpu_t h, const uint8_t* chunk, int64_t Y0, int64_t Y1, uint32_t* dstP) {
-    const PackedPlan& P = h->pp;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        CK(cudaFuncSetAttribute(unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        attr = true;
-    }
-    const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
-    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((warps + kConvWarps - 1) / kConvWarps, 148ull * 16));
-    pack_kernel<<<blocks, kConvWarps * 32, conv_smem(h), h->stream>>>(packed_geom(h), chunk, (uint32_t)Y0, (uint32_t)Y1, dstP, h->d_flag);
-    CK(cudaGetLastError());
-}
-
-void launch_unpack(nbbgpu_t h, const uint32_t* srcP, int64_t Y0, int64_t Y1, uint8_t* chunk) {
-    const PackedPlan& P = h->pp;
-    const uint64_t warps = ((uint64_t)(Y1 - Y0) * P.Wc / 32 + 2) * P.wq;
-    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((warps + kConvWarps - 1) / kConvWarps, 148ull * 16));
-    unpack_kernel<<<blocks, kConvWarps * 32, conv_smem(h), h->stream>>>(packed_geom(h), srcP, (uint32_t)Y0, (uint32_t)Y1, chunk);
-    CK(cudaGetLastError());
-}
-
-// bytes (reference layout; device or host) -> packed buffer dstP.  Returns false
-// if a byte > 1 was seen (dstP then holds garbage; callers restore).
-bool packed_from_bytes(nbbgpu_t h, const uint8_t* src, uint32_t* dstP) {
-    const PackedPlan& P = h->pp;
-    CK(cudaMemsetAsync(dstP, 0, packed_words(P) * 4, h->stream));
-    CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
-    if (is_device_mem(src)) {
-        launch_pack(h, src, 0, P.Hc, dstP);
-    } else {
-        const int64_t cr = chunk_rows(h);
-        const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
-        StagePipe sp(h, std::min<uint64_t>(h->cells, cr * row_bytes));
-        int k = 0;
-        for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr, k ^= 1) {
-            const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
-            CK(cudaStreamWaitEvent(sp.xs, sp.done[k], 0));  // previous pack of this buffer finished
-            CK(cudaMemcpyAsync(sp.buf[k], src + (uint64_t)Y0 * row_bytes, (uint64_t)(Y1 - Y0) * row_bytes,
-                               cudaMemcpyHostToDevice, sp.xs));
-            CK(cudaEventRecord(sp.ready[k], sp.xs));
-            CK(cudaStreamWaitEvent(h->stream, sp.ready[k], 0));
-            launch_pack(h, sp.buf[k], Y0, Y1, dstP);
-            CK(cudaEventRecord(sp.done[k], h->stream));
-        }
-    }
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    return flag == 0;
-}
-
-// packed buffer srcP -> bytes (reference layout; device or host)
-void packed_to_bytes(nbbgpu_t h, const uint32_t* srcP, uint8_t* dst) {
-    const PackedPlan& P = h->pp;
-    if (is_device_mem(dst)) {
-        launch_unpack(h, srcP, 0, P.Hc, dst);
-        CK(cudaStreamSynchronize(h->stream));
-        return;
-    }
-    const int64_t cr = chunk_rows(h);
-    const uint64_t row_bytes = (uint64_t)P.wq * (uint64_t)h->hf.w;
-    StagePipe sp(h, std::min<uint64_t>(h->cells, cr * row_bytes));
-    int k = 0;
-    for (int64_t Y0 = 0; Y0 < P.Hc; Y0 += cr, k ^= 1) {
-        const int64_t Y1 = std::min<int64_t>(P.Hc, Y0 + cr);
-        CK(cudaStreamWaitEvent(h->stream, sp.done[k], 0));  // previous copy-out of this buffer finished
-        launch_unpack(h, srcP, Y0, Y1, sp.buf[k]);
-        CK(cudaEventRecord(sp.ready[k], h->stream));
-        CK(cudaStreamWaitEvent(sp.xs, sp.ready[k], 0));
-        CK(cudaMemcpyAsync(dst + (uint64_t)Y0 * row_bytes, sp.buf[k], (uint64_t)(Y1 - Y0) * row_bytes,
-                           cudaMemcpyDeviceToHost, sp.xs));
-        CK(cudaEventRecord(sp.done[k], sp.xs));
-    }
-    CK(cudaStreamSynchronize(sp.xs));
-}
-
-// switch the state layout, converting the front state on the device
-void set_layout(nbbgpu_t h, int want) {
-    if (h->layout == want && (want == 1 ? h->pk[0] != nullptr : h->buf[0] != nullptr)) return;
-    if (want == 1) {
-        alloc_packed_state(h);
-        if (h->buf[h->cur]) {
-            if (!packed_from_bytes(h, h->buf[h->cur], h->pk[0])) raise(NBBGPU_ERR_CUDA, "internal: non-binary state");
-        }
-        CK(cudaMemsetAsync(h->pk[1], 0, packed_words(h->pp) * 4, h->stream));
-        h->cur = 0;
-        bnd_refresh(h);
-        CK(cudaStreamSynchronize(h->stream));
-        free_byte_state(h);
-        h->layout = 1;
-    } else {
-        alloc_byte_state(h);
-        if (h->pk[h->cur]) packed_to_bytes(h, h->pk[h->cur], h->buf[0]);
-        CK(cudaMemsetAsync(h->buf[1], 0, h->cells + 64, h->stream));
-        h->cur = 0;
-        CK(cudaStreamSynchronize(h->stream));
-        free_packed_state(h);
-        h->layout = 0;
-    }
-}
-
-// packed word index + bit of the compact cell (cx, cy)
-void packed_locate(nbbgpu_t h, int64_t cx, int64_t cy, uint64_t& word, uint32_t& bit) {
-    const PackedPlan& P = h->pp;
-    const int64_t X = cx / P.wq, c = cx % P.wq, Y = cy / P.wq, a = cy % P.wq;
-    const uint64_t t = (uint64_t)(Y * P.Wc + X);
-    word = (t / 32) * (uint64_t)P.Cp + (uint64_t)(a * P.wq + c);
-    bit = (uint32_t)(t % 32);
-}
-
-// launch with programmatic stream serialisation (PDL): the kernel may begin while
-// its predecessor on the stream drains and synchronises in-kernel (pdl_wait)
-template <class... KArgs, class... Args>
-void launch_pdl(nbbgpu_t h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
-    static const bool off = getenv("NBBGPU_NO_PDL") != nullptr;  // comparison knob
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = h->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, args...));
-}
-
-template <bool CONWAY, int DEG, bool WIDE>
-void launch_packed_t(nbbgpu_t h, const PackedStepParams& p) {
-    constexpr int NT = kPackedThreads;
-    auto kern = step_packed_kernel<CONWAY, DEG, WIDE>;
-    const size_t smem = 16 + 2 * (size_t)p.SW * 4;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr_set = true;
-    }
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    int sms = 148;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    const uint64_t groups = p.g1 - p.g0;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms));
-    kern<<<(unsigned)blocks, NT, smem, h->stream>>>(p, h->pk[h->cur], h->pk[h->cur ^ 1], h->bnd[h->cur], h->bnd[h->cur ^ 1]);
-}
-
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1>
-void launch_packed_ws3_t(nbbgpu_t h, const PackedStepParams& p) {
-    auto kern = step_packed_ws3_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO, SPLIT>;
-    constexpr int NCHUNK = WsGeom<FT, P, WQ, SPLIT>::NCHUNK;
-    constexpr int NT = (NCHUNK * NGRP + 2) * 32;
-    const size_t out_bytes = SPLIT == 1 ? (size_t)p.Cp * 4 : (size_t)WsGeom<FT, P, WQ, SPLIT>::ROWS * WQ * 4;
-    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * out_bytes;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
-    if (smem > 227 * 1024) raise(NBBGPU_ERR_CUDA, "internal: stage rings exceed shared memory");
-    int sms = 148, per_sm = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    const uint64_t groups = p.g1 - p.g0;
-    const uint64_t pairs = std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(1, per_sm) * sms / SPLIT));
-    launch_pdl(h, kern, dim3((unsigned)(pairs * SPLIT)), dim3(NT), smem, p,
-               (const uint32_t*)h->pk[h->cur], h->pk[h->cur ^ 1], (const uint32_t*)h->bnd[h->cur], h->bnd[h->cur ^ 1]);
-}
-
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
-void launch_packed_fused_t(nbbgpu_t h, const PackedStepParams& p, int nsteps) {
-    auto kern = step_packed_fused_kernel<CONWAY, DEG, WIDE, FT, P, WQ, NGRP, NS, NO>;
-    constexpr int NCHUNK = (BlockGeom<FT, P, WQ>::NBLK + 31) / 32;
-    constexpr int NT = (NCHUNK * NGRP + 2) * 32;
-    const size_t smem = 16 * (NS + NO) + (size_t)NS * p.SW * 4 + (size_t)NO * p.Cp * 4;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
-    int sms = 148, per_sm = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    if (per_sm < 1) raise(NBBGPU_ERR_CUDA, "internal: fused kernel does not fit an SM");
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)(p.g1 - p.g0), (uint64_t)per_sm * sms));
-    PackedStepParams pp = p;
-    uint32_t *P0 = h->pk[0], *P1 = h->pk[1], *B0 = h->bnd[0], *B1 = h->bnd[1];
-    int cur0 = h->cur;
-    unsigned* gbar = h->d_gbar;
-    void* args[] = {&pp, &P0, &P1, &B0, &B1, &cur0, &nsteps, &gbar};
-    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(NT), args, smem, h->stream));
-}
-
-// the fused multi-step kernel exists for the ws3 micro-block configurations
-// Opt-in (NBBGPU_FUSE=1): with programmatic dependent launch the halo + step kernel
-// pair is faster at every measured level (T r=16: 8.4 vs 12.1 us per step; r=20:
-// 0.148 vs 0.162 ms), so the cooperative multi-step kernel is kept as a variant.
-bool packed_fusable(nbbgpu_t h) {
-    static const char* env = getenv("NBBGPU_FUSE");
-    const PackedPlan& P = h->pp;
-    if (P.wide || !(env && env[0] == '1')) return false;
-    return (P.tag == kTagTriangle && (P.wq == 81 || P.wq == 27)) || (P.tag == kTagCarpet && P.wq == 64) ||
-           (P.tag == kTagVicsek && P.wq == 25) || (P.tag == kTagH && P.wq == 49);
-}
-
-PackedStepParams packed_params(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
-    const PackedPlan& P = h->pp;
-    PackedStepParams p{};
-    p.C = (uint32_t)P.C; p.Cp = (uint32_t)P.Cp; p.SW = P.SW;
-    p.nH = (uint32_t)P.nH; p.nHp = (uint32_t)P.nHp; p.nSrc = (uint32_t)P.nSrc;
-    p.halo = h->d_phalo;
-    p.nD = P.nD;
-    for (int ds = 0; ds <= 8; ++ds) {
-        int cnt = 0;
-        for (int j = 0; j < P.nH; ++j) cnt += (int)((P.slot[j] >> 16) & 0xFFu) < ds;
-        p.dfirst[ds] = (uint16_t)cnt;
-    }
-    p.T = (uint32_t)P.T; p.NG = (uint32_t)P.NG;
-    p.g0 = (uint32_t)h->pg0; p.g1 = (uint32_t)h->pg1;
-    p.lastmask = P.lastmask;
-    p.birth = birth; p.survive = survive;
-    p.nbr = h->d_pnbr[moore];
-    p.slot = h->d_pslot; p.ntab = h->d_pntab; p.srcidx = h->d_psrc; p.btab = h->d_pbtab;
-    return p;
-}
-
-// nsteps steps in one cooperative launch (packed_fusable configurations)
-void launch_steps_fused(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int nsteps) {
-    const PackedPlan& P = h->pp;
-    const PackedStepParams p = packed_params(h, birth, survive, moore);
-    if (p.g1 <= p.g0 || nsteps <= 0) return;
-    ++h->launches;
-    prof_mark(h);
-    struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
-    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
-    const int dg = moore ? 8 : 4;
-#define NBB_FU(TAG, FT, BP, W, NGRP, NS, NO)                                                                     \
-    if (P.tag == TAG && P.wq == W) {                                                                             \
-        if (conway && dg == 8) return launch_packed_fused_t<true, 8, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);  \
-        if (conway) return launch_packed_fused_t<true, 4, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);             \
-        if (dg == 8) return launch_packed_fused_t<false, 8, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);           \
-        return launch_packed_fused_t<false, 4, false, FT, BP, W, NGRP, NS, NO>(h, p, nsteps);                        \
-    }
-    NBB_FU(kTagTriangle, TriangleTag, 2, 81, 1, 4, 2)
-    NBB_FU(kTagTriangle, TriangleTag, 2, 27, 8, 16, 8)
-    NBB_FU(kTagCarpet, CarpetTag, 1, 64, 1, 4, 2)
-    NBB_FU(kTagVicsek, VicsekTag, 2, 25, 16, 24, 16)
-    NBB_FU(kTagH, HTag, 1, 49, 2, 6, 4)
-#undef NBB_FU
-    raise(NBBGPU_ERR_CUDA, "internal: no fused kernel for this plan");
-}
-
-void launch_step_packed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
-    const PackedPlan& P = h->pp;
-    const PackedStepParams p = packed_params(h, birth, survive, moore);
-    if (p.g1 <= p.g0) return;
-    // halo words of every owned group from the boundary plane (separate kernel);
-    // the step kernel bulk-loads them with each group record
-    if (P.nH > 0) {
-        const uint64_t warps = halo_tasks((uint32_t)P.nH, p.g1 - p.g0, P.nD);
-        // (the neighbour tile comes from the static ntab: an ALU carry walk with
-        //  compile-time tables measured slower, T r=20 0.178 vs 0.148 ms per step)
-        if (halo_use_wide((uint32_t)P.nH, p.g1 - p.g0))
-            launch_pdl(h, halo_words_kernel<true>, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
-                       (const uint32_t*)h->bnd[h->cur], h->d_phalo);
-        else
-            launch_pdl(h, halo_words_kernel<false>, dim3(grid_for(warps * 32, 256)), dim3(256), 0, p,
-                       (const uint32_t*)h->bnd[h->cur], h->d_phalo);
-        CK(cudaGetLastError());
-        ++h->launches;
-    }
-    ++h->launches;  // the step kernel below
-    prof_mark(h);
-    struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
-    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC;
-    if (P.tag != kTagNone) {
-        const int dg = moore ? 8 : 4;
-    // Micro-block kernels: the persistent TMA-in/TMA-out warp-specialised kernel
-    // (ws3); groups with more chunks than a CTA has warps run on CTA pairs (SPLIT).
-#define NBB_WS3(TAG, FT, BP, W, WD, NGRP, NS, NO)                                                        \
-    if (P.tag == TAG && P.wq == W && P.wide == WD) {                                                    \
-        if (conway && dg == 8) return launch_packed_ws3_t<true, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);  \
-        if (conway) return launch_packed_ws3_t<true, 4, WD, FT, BP, W, NGRP, NS, NO>(h, p);             \
-        if (dg == 8) return launch_packed_ws3_t<false, 8, WD, FT, BP, W, NGRP, NS, NO>(h, p);           \
-        return launch_packed_ws3_t<false, 4, WD, FT, BP, W, NGRP, NS, NO>(h, p);                        \
-    }
-        NBB_WS3(kTagTriangle, TriangleTag, 2, 81, false, 1, 4, 2)
-        NBB_WS3(kTagTriangle, TriangleTag, 2, 27, false, 8, 16, 8)
-        NBB_WS3(kTagCarpet, CarpetTag, 1, 64, false, 1, 4, 2)
-        NBB_WS3(kTagVicsek, VicsekTag, 2, 25, false, 16, 24, 16)
-        NBB_WS3(kTagH, HTag, 1, 49, false, 2, 6, 4)
-        if (P.tag == kTagCandy && P.wq == 144 && P.wide) {
-            // 54 chunks per group: CTA pairs, each computing half the rows
-            if (conway && dg == 8) return launch_packed_ws3_t<true, 8, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
-            if (conway) return launch_packed_ws3_t<true, 4, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
-            if (dg == 8) return launch_packed_ws3_t<false, 8, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
-            return launch_packed_ws3_t<false, 4, true, CandyTag, 1, 144, 1, 2, 1, 2>(h, p);
-        }
-#undef NBB_WS3
-        raise(NBBGPU_ERR_CUDA, "internal: micro-block plan without a kernel");
-    }
-#define NBB_PK(CW, DG, WD) if (conway == CW && (moore ? 8 : 4) == DG && P.wide == WD) return launch_packed_t<CW, DG, WD>(h, p)
-    NBB_PK(true, 8, false); NBB_PK(false, 8, false); NBB_PK(true, 4, false); NBB_PK(false, 4, false);
-    NBB_PK(true, 8, true); NBB_PK(false, 8, true); NBB_PK(true, 4, true); NBB_PK(false, 4, true);
-#undef NBB_PK
-}
+#include "packed_host.inc"
 
 template <int WQ, int K, int S, bool CONWAY>
 void launch_tiled_t(nbbgpu_t h, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
