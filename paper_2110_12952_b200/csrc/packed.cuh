@@ -107,12 +107,27 @@ __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint
     if (lane < SPW && j0 + lane < p.nHp) H[(uint64_t)g * p.nHp + j0 + lane] = j0 + lane < p.nH ? mine : 0u;
 }
 
+// 32 x 32 bit transpose across a warp: lane i holds row i (bit k = column k) ->
+// lane k holds column k (bit i = row i).  Five shuffle-xor block swaps.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                                 : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+
 // Large halos (carpet, H: ~200-330 slots per tile): one task per (group, used
-// direction).  A direction with many slots (a tile edge) is gathered TRANSPOSED:
-// lane = slot, and a loop over the 32 tiles b reads B[t2_b][m_slot] (coalesced over
-// the slots) and sets bit b -- ~7 instructions per tile for 32 slots, instead of a
-// warp-wide load + ballot per slot.  Directions with a few slots (corners) keep the
-// lane = tile ballot form.
+// direction).  A direction with many slots (a tile edge) is gathered as a BIT
+// PERMUTATION: for every source group G of the 32 neighbour tiles, lane = slot
+// loads its boundary word B[G][m_slot] (one coalesced load), a warp transpose turns
+// the 32 words into bit columns, lane = tile picks column (t2 & 31) with one
+// shuffle, and a final transpose turns the tiles' bits back into the 32 halo
+// words -- ~70 instructions per 32 slots (1-2 source groups) instead of a load +
+// ballot per slot.  Directions with a few slots (corners) keep the ballot form.
 template <bool NC>
 __device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
                                                uint32_t g, int ds, uint32_t lane) {
@@ -121,19 +136,24 @@ __device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const 
     const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)ds * p.T + t)) : kNoTile;  // lane = tile
     const uint32_t j_beg = p.dfirst[ds], j_end = p.dfirst[ds + 1];
     if (j_end - j_beg >= 8) {
+        const bool valid = t2 != kNoTile;
+        const uint32_t G2 = t2 >> 5, col_of_tile = t2 & 31;
         for (uint32_t j0 = j_beg; j0 < j_end; j0 += 32) {
             const uint32_t j = j0 + lane;  // lane = slot
             const uint32_t my_m = j < j_end ? (__ldg(p.slot + j) & 0xFFFFu) : 0u;
-            uint32_t h = 0;
-#pragma unroll 8
-            for (int b = 0; b < 32; ++b) {
-                const uint32_t tb = __shfl_sync(0xFFFFFFFFu, t2, b);
-                if (tb != kNoTile) {  // warp-uniform
-                    const uint32_t w = ld_bnd<NC>(bsrc + (size_t)(tb >> 5) * p.nSrc + my_m);
-                    h |= ((w >> (tb & 31)) & 1u) << b;
-                }
+            uint32_t out = 0;  // lane = tile: bit i = slot j0 + i
+            uint32_t remaining = __ballot_sync(0xFFFFFFFFu, valid);
+            while (remaining) {  // one pass per distinct source group (warp-uniform)
+                const uint32_t G = __shfl_sync(0xFFFFFFFFu, G2, __ffs(remaining) - 1);
+                const uint32_t members = __ballot_sync(0xFFFFFFFFu, valid && G2 == G);
+                const uint32_t w = j < j_end ? ld_bnd<NC>(bsrc + (size_t)G * p.nSrc + my_m) : 0u;
+                const uint32_t col = warp_transpose32(w, lane);        // lane c: bit i = bit c of word i
+                const uint32_t picked = __shfl_sync(0xFFFFFFFFu, col, col_of_tile);
+                if ((members >> lane) & 1u) out = picked;
+                remaining &= ~members;
             }
-            if (j < j_end) Hg[j] = h;
+            const uint32_t halo = warp_transpose32(out, lane);       // lane i: bit b = tile b, slot i
+            if (j < j_end) Hg[j] = halo;
         }
         return;
     }
