@@ -232,7 +232,9 @@ def run_ours(args):
     dsim = None
     if ws > 1:
         from paper_2110_12952_b200.distributed import DistributedSimulation
-        if args.dist_backend == "nccl" and args.transport == "nccl":
+        if args.transport in ("p2p", "auto"):
+            dsim = DistributedSimulation(sim, dist, rank, ws, transport=args.transport)
+        elif args.dist_backend == "nccl" and args.transport == "nccl":
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="nccl")
         elif args.dist_backend == "nccl":
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="torch")
@@ -273,7 +275,7 @@ def run_ours(args):
     # kernel per step; N > 1 adds the halo pack / NCCL send-recv / unpack on-stream)
     if ws == 1:
         sim.step(rule, args.steps)
-    elif dsim.transport == "nccl":
+    elif dsim.transport in ("nccl", "p2p"):
         sim.step(rule, args.steps)
     else:
         dsim.step(rule, args.steps)
@@ -285,7 +287,7 @@ def run_ours(args):
     n1 = C.c_uint64()
     _abi.check(L.nbbgpu_launch_count(h, C.byref(n1)))
     launches = n1.value - n0.value
-    if dsim is not None and dsim.transport != "nccl":
+    if dsim is not None and dsim.transport == "torch":
         launches += args.steps * dsim.launches_per_exchange
     # second pass of K steps with CUDA events around every main step kernel: its own
     # average duration for the roofline (per-kernel events add gaps, so the headline
@@ -363,7 +365,8 @@ def run_ours(args):
         "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore "
                                "(BASELINE.json configs[3]; north-star target)",
                    "level": args.level, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
-                   "parallelism": f"partitioned x{n}" if n > 1 else "single GPU",
+                   "parallelism": (f"partitioned x{n}, halo transport {dsim.transport}" if dsim is not None
+                                   else "single GPU"),
                    "state_bytes_per_buffer": (cells + 7) // 8 if packed else cells,
                    "l2": (f"state {((cells + 7) // 8 if packed else cells) / 1e9:.2f} GB per buffer vs 126 MB L2: "
                           "inputs larger than L2, no flush")},
@@ -407,9 +410,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--level", type=int, default=LEVEL, help="triangle level (default 20)")
     ap.add_argument("--device", type=int, default=None, help="test knob: force the CUDA device")
-    ap.add_argument("--transport", choices=["nccl", "torch"], default="nccl",
-                    help="halo transport: in-library NCCL on the engine stream (default) or "
-                         "torch.distributed point-to-point")
+    ap.add_argument("--transport", choices=["auto", "nccl", "p2p", "torch"], default="auto",
+                    help="halo transport: auto (default) = peer-memory pushes over NVLink (p2p, CUDA IPC) "
+                         "when every rank can map its peers, else the in-library NCCL send/recv on the "
+                         "engine stream; torch = torch.distributed point-to-point")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="test knob: gloo lets several ranks share one GPU")
     args = ap.parse_args()

@@ -202,6 +202,17 @@ int nbbgpu_comm_init(nbbgpu_t h, const uint8_t* unique_id, int bytes);
  * boundary-plane word). */
 int nbbgpu_halo_elem_bytes(nbbgpu_t h, int* out);
 
+/* Peer-memory halo transport for the PACKED kernel (NVLink, CUDA IPC), an
+ * alternative to nbbgpu_comm_init: every rank exports nbbgpu_p2p_handle_bytes()
+ * bytes of IPC handles (its boundary planes + an arrival counter), the caller
+ * all-gathers them in rank order and every rank attaches them.  From then on each
+ * step pushes the boundary words peers need straight into their planes (one small
+ * kernel, system-scope fence + counter), and the next halo kernel waits on this
+ * rank's counter: no NCCL call and no host synchronisation per step. */
+int nbbgpu_p2p_handle_bytes(void);
+int nbbgpu_p2p_export(nbbgpu_t h, uint8_t* out, int bytes);
+int nbbgpu_p2p_attach(nbbgpu_t h, const uint8_t* all_handles, int bytes_per_rank, int nranks);
+
 /* Raw device pointer of the front buffer (reference bytes, or packed words for
  * the PACKED kernel; for peer-to-peer transports). */
 int nbbgpu_front_device_ptr(nbbgpu_t h, void** out);

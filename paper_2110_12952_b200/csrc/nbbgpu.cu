@@ -346,6 +346,16 @@ struct nbbgpu_sim {
     std::vector<uint64_t> n_recvs;
     // in-library NCCL transport (nbbgpu_comm_init)
     ncclComm_t comm = nullptr;
+    // peer-memory halo transport (nbbgpu_p2p_export / nbbgpu_p2p_attach)
+    bool p2p = false;
+    uint32_t* d_pcnt = nullptr;             // my arrival counter (exported by IPC)
+    uint32_t p2p_epoch = 0, p2p_nsrc = 0, p2p_send_mask = 0;
+    uint64_t* d_p2p_elems = nullptr;        // boundary elements peers need from me
+    uint8_t* d_p2p_peer = nullptr;          // ... and which peer
+    uint64_t p2p_n = 0;
+    uint32_t** d_peer_bnd[2] = {nullptr, nullptr};  // per rank: mapped boundary planes
+    uint32_t** d_peer_cnt = nullptr;                // per rank: mapped arrival counters
+    std::vector<void*> ipc_opened;
     uint64_t* d_send_all = nullptr;             // concatenated per-peer send offsets
     uint64_t* d_recv_all = nullptr;
     uint8_t* d_sendbuf = nullptr;
@@ -682,6 +692,13 @@ void free_all(nbbgpu_t h) {
     if (h->d_recv_all) cudaFree(h->d_recv_all);
     if (h->d_sendbuf) cudaFree(h->d_sendbuf);
     if (h->d_recvbuf) cudaFree(h->d_recvbuf);
+    for (void* q : h->ipc_opened) cudaIpcCloseMemHandle(q);
+    h->ipc_opened.clear();
+    if (h->d_pcnt) cudaFree(h->d_pcnt);
+    if (h->d_p2p_elems) cudaFree(h->d_p2p_elems);
+    if (h->d_p2p_peer) cudaFree(h->d_p2p_peer);
+    for (auto*& q : h->d_peer_bnd) if (q) { cudaFree(q); q = nullptr; }
+    if (h->d_peer_cnt) cudaFree(h->d_peer_cnt);
     free_comm(h);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -985,7 +1002,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     const uint64_t l0 = h->launches;
     CK(cudaEventRecord(h->ev0, h->stream));
     try {
-        if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm) {
+        if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm && !h->p2p) {
             // every step in one cooperative launch (chunks bound the launch length)
             for (int64_t done = 0; done < nsteps;) {
                 const int n = (int)std::min<int64_t>(nsteps - done, 1 << 20);
@@ -1000,7 +1017,8 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
                 else launch_step(h, birth, survive, moore);
                 h->cur ^= 1;
                 ++h->iteration;
-                if (h->comm) exchange_on_stream(h);  // halo of the new front, on-stream
+                if (h->p2p) p2p_push(h);             // peer-memory halo of the new front
+                else if (h->comm) exchange_on_stream(h);  // NCCL halo of the new front, on-stream
             }
         }
     } catch (...) {

@@ -60,7 +60,31 @@ struct PackedStepParams {
     uint32_t* halo;          // [NG][nHp] halo words of the step (halo_words_kernel)
     int nD;                  // used directions (rows of ntab)
     uint16_t dfirst[9];      // slots of direction slot ds: [dfirst[ds], dfirst[ds + 1])
+    // peer-memory halo transport: the halo kernel first waits until the peers have
+    // pushed this step's boundary words (system-scope arrival counter >= target)
+    const uint32_t* wait_cnt;
+    uint32_t wait_target;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// one thread per CTA spins on the arrival counter (bounded: a lost peer traps the
+// kernel after ~2 s instead of hanging the device), then the CTA proceeds
+__device__ __forceinline__ void wait_peers(const PackedStepParams& p) {
+    if (!p.wait_cnt) return;
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        while ((int32_t)(ld_acquire_sys(p.wait_cnt) - p.wait_target) < 0) {
+            __nanosleep(64);
+            if (clock64() - t0 > 4000000000LL) __trap();
+        }
+    }
+    __syncthreads();
+}
 
 // Boundary-plane / halo loads: through the read-only path when the data was written
 // by an earlier launch (NC), L2-coherent (ld.global.cg) inside the fused multi-step
@@ -196,11 +220,12 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
 
 // WIDE_HALO is compile-time so the small-halo variant keeps its 30 registers
 // (full occupancy: this kernel is latency-bound)
-template <bool WIDE_HALO, int SPW = 4>
+template <bool WIDE_HALO, int SPW = 4, bool NC = true>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
     pdl_wait();     // bsrc comes from the previous step kernel
+    wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
     pdl_trigger();  // the step kernel may launch and run its prologue
     const uint64_t nw = WIDE_HALO ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
                                   : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
@@ -208,9 +233,9 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         if constexpr (WIDE_HALO) {
             const uint32_t w32 = (uint32_t)wi, gi = w32 / (uint32_t)p.nD;
-            halo_wide_task<true>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
+            halo_wide_task<NC>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
         } else {
-            halo4_task<true, SPW>(p, bsrc, H, wi, lane);
+            halo4_task<NC, SPW>(p, bsrc, H, wi, lane);
         }
     }
 }
@@ -704,6 +729,26 @@ step_packed_fused_kernel(const PackedStepParams p, uint32_t* P0, uint32_t* P1, u
             }
         }
         grid_barrier(gbar);  // records + boundary words of this step complete
+    }
+}
+
+// Peer-memory halo push (one CTA): after this rank's step kernel, write every
+// boundary-plane word a peer needs straight into that peer's boundary plane over
+// NVLink (CUDA IPC mappings), then -- after a system-scope fence -- add 1 to the
+// arrival counter of every peer it sends to.  The peer's next halo kernel waits on
+// that counter (wait_peers).  Element e has the same index in every rank's plane.
+__global__ void p2p_push_kernel(const uint32_t* __restrict__ bnd, const uint64_t* __restrict__ elems,
+                                const uint8_t* __restrict__ peer_of, uint64_t n, uint32_t* const* __restrict__ peer_bnd,
+                                uint32_t* const* __restrict__ peer_cnt, uint32_t send_mask) {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t e = elems[i];
+        peer_bnd[peer_of[i]][e] = bnd[e];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < 32 && ((send_mask >> threadIdx.x) & 1u)) {
+        __threadfence_system();
+        atomicAdd_system(peer_cnt[threadIdx.x], 1u);
     }
 }
 

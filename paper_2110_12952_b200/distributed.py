@@ -188,11 +188,15 @@ class DistributedSimulation:
       broadcast over torch.distributed); pack kernel -> grouped ncclSend/ncclRecv
       -> unpack kernel are enqueued on the engine stream after each step kernel,
       so K steps run without any host synchronisation.
+    transport="p2p" (packed kernel): CUDA IPC mappings of the peers' boundary
+      planes over NVLink; each step pushes the words peers need straight into their
+      planes with a system-scope arrival counter (no NCCL call per step); the IPC
+      handles are all-gathered over torch.distributed once.
     transport="torch": torch.distributed point-to-point on device tensors
       (host_staging=True: through host tensors, so gloo can drive several ranks
       that share one test GPU)."""
 
-    def __init__(self, sim, dist, rank: int, nranks: int, transport: str = "nccl",
+    def __init__(self, sim, dist, rank: int, nranks: int, transport: str = "auto",
                  host_staging: bool = False):
         import torch
         self.sim, self.dist, self.rank, self.nranks = sim, dist, rank, nranks
@@ -213,6 +217,46 @@ class DistributedSimulation:
             assert (lo.value, hi.value) == (self.plan.lo, self.plan.hi), "partition geometry mismatch"
         self.launches_per_exchange = (int(any(self.plan.send[p].size for p in self.plan.peers)) +
                                       int(any(self.plan.recv[p].size for p in self.plan.peers)))
+        if transport == "auto":
+            # peer-memory pushes for the packed kernel when every rank can map its
+            # peers' planes (CUDA IPC + NVLink peer access), else the NCCL transport;
+            # every collective below is reached by every rank
+            mine = None
+            if self.plan.packed:
+                try:
+                    nb = L.nbbgpu_p2p_handle_bytes()
+                    buf = (C.c_uint8 * nb)()
+                    _abi.check(L.nbbgpu_p2p_export(h, buf, nb))
+                    mine = bytes(buf)
+                except Exception:  # noqa: BLE001 -- IPC unavailable on this rank
+                    mine = None
+            allh = [None] * nranks
+            dist.all_gather_object(allh, mine)
+            if all(x is not None for x in allh):
+                ok = 1
+                try:
+                    nb = len(allh[0])
+                    blob = (C.c_uint8 * (nb * nranks)).from_buffer_copy(b"".join(allh))
+                    _abi.check(L.nbbgpu_p2p_attach(h, blob, nb, nranks))
+                except Exception:  # noqa: BLE001 -- peer mapping failed
+                    ok = 0
+                flags = [None] * nranks
+                dist.all_gather_object(flags, ok)
+                if not all(flags):
+                    raise RuntimeError("p2p halo transport could not map every peer; use transport='nccl'")
+                dist.barrier()
+                self.transport = "p2p"
+                self.launches_per_exchange = 1
+                return
+            self.transport = transport = "nccl"
+        if transport == "p2p":
+            if not self.plan.packed:
+                raise ValueError("the p2p transport needs the packed kernel")
+            self._attach_p2p(L, h, dist, rank, nranks)
+            self.launches_per_exchange = 1
+            return
+        if transport == "nccl":
+            uid = (C.c_uint8 * 128)()
         if transport == "nccl":
             uid = (C.c_uint8 * 128)()
             if rank == 0:
@@ -234,10 +278,22 @@ class DistributedSimulation:
         self.launches_per_exchange = sum(int(self.plan.send[p].size > 0) + int(self.plan.recv[p].size > 0)
                                          for p in self.plan.peers)
 
+    def _attach_p2p(self, L, h, dist, rank: int, nranks: int) -> None:
+        """All-gather the ranks' IPC handles (boundary planes + arrival counter) and
+        map the peers' into this process (nbbgpu_p2p_export / nbbgpu_p2p_attach)."""
+        nb = L.nbbgpu_p2p_handle_bytes()
+        mine = (C.c_uint8 * nb)()
+        _abi.check(L.nbbgpu_p2p_export(h, mine, nb))
+        allh = [None] * nranks
+        dist.all_gather_object(allh, bytes(mine))
+        blob = (C.c_uint8 * (nb * nranks)).from_buffer_copy(b"".join(allh))
+        _abi.check(L.nbbgpu_p2p_attach(h, blob, nb, nranks))
+        dist.barrier()
+
     def exchange(self) -> None:
         """torch transport only (the nccl transport exchanges inside every step)."""
         import torch
-        if self.transport == "nccl":
+        if self.transport in ("nccl", "p2p"):
             return
         L, h = _abi.lib(), self.sim.handle()
 
@@ -258,7 +314,7 @@ class DistributedSimulation:
         exchange(self.plan, self.dist, pack, recv_buffer, unpack)
 
     def step(self, rule, nsteps: int = 1) -> None:
-        if self.transport == "nccl":
+        if self.transport in ("nccl", "p2p"):
             self.sim.step(rule, nsteps)
             return
         for _ in range(nsteps):
@@ -267,7 +323,7 @@ class DistributedSimulation:
 
     def step_timed(self, rule, nsteps: int) -> float:
         """Device ms of nsteps steps (step kernels + halo exchanges, one event pair)."""
-        if self.transport == "nccl":
+        if self.transport in ("nccl", "p2p"):
             return self.sim.step_timed(rule, nsteps)
         ms = 0.0
         for _ in range(nsteps):
@@ -277,7 +333,7 @@ class DistributedSimulation:
 
     def step_profiled(self, rule, nsteps: int):
         """(total device ms, device ms of the main step kernels, engine kernel launches)."""
-        if self.transport == "nccl":
+        if self.transport in ("nccl", "p2p"):
             return self.sim.step_profiled(rule, nsteps)
         tot = main = 0.0
         launches = 0

@@ -14,13 +14,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _bench(nproc, level, port):
+def _bench(nproc, level, port, transport="torch"):
     args = ["bench.py", "--level", str(level), "--steps", "4", "--warmup", "3", "--no-e2e",
             "--no-cpu-baseline"]
     if nproc > 1:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
                "--master-addr", "127.0.0.1", "--master-port", str(port)] + args + [
-               "--gpus", str(nproc), "--dist-backend", "gloo", "--transport", "torch", "--device", "0"]
+               "--gpus", str(nproc), "--dist-backend", "gloo", "--transport", transport, "--device", "0"]
     else:
         cmd = [sys.executable] + args
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
@@ -30,8 +30,26 @@ def _bench(nproc, level, port):
 
 
 @pytest.mark.parametrize("nproc", [2, 3])
-def test_multirank_bench_matches_single(nproc):
+def test_multirank_bench_matches_single(nproc):  # torch.distributed point-to-point (gloo)
     single = _bench(1, 14, 0)
     multi = _bench(nproc, 14, 29517 + nproc)
     assert multi["final_state_hash"] == single["final_state_hash"]
     assert multi["n_gpus"] == nproc and "packed" in multi["config"]["kernel"]
+
+
+@pytest.mark.parametrize("nproc", [2, 3])
+def test_multirank_p2p_transport_matches_single(nproc):
+    # the peer-memory transport (CUDA IPC mappings of the boundary planes, pushes +
+    # system-scope arrival counters): several processes on ONE GPU exercise the
+    # same IPC / counter protocol the NVLink peers use
+    single = _bench(1, 14, 0)
+    multi = _bench(nproc, 14, 29617 + nproc, transport="p2p")
+    assert multi["final_state_hash"] == single["final_state_hash"]
+    multi20 = _bench(nproc, 16, 29717 + nproc, transport="p2p")
+    assert multi20["final_state_hash"] == _bench(1, 16, 0)["final_state_hash"]
+
+
+def test_multirank_auto_transport_picks_p2p():
+    out = _bench(2, 12, 29817, transport="auto")
+    assert "halo transport p2p" in out["config"]["parallelism"]
+    assert out["final_state_hash"] == _bench(1, 12, 0)["final_state_hash"]
