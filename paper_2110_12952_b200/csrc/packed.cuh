@@ -740,6 +740,8 @@ step_packed_fused_kernel(const PackedStepParams p, uint32_t* P0, uint32_t* P1, u
 __global__ void p2p_push_kernel(const uint32_t* __restrict__ bnd, const uint64_t* __restrict__ elems,
                                 const uint8_t* __restrict__ peer_of, uint64_t n, uint32_t* const* __restrict__ peer_bnd,
                                 uint32_t* const* __restrict__ peer_cnt, uint32_t send_mask) {
+    pdl_wait();  // the step kernel's boundary words are complete (PDL launch)
+    pdl_trigger();
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint64_t e = elems[i];
         peer_bnd[peer_of[i]][e] = bnd[e];
