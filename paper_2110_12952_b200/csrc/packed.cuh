@@ -460,11 +460,15 @@ struct WsGeom {
     static_assert(SPLIT == 1 || (Wiring<FT, P>::BH == 1 && WQ % SPLIT == 0), "SPLIT needs P = 1 row blocks");
 };
 
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1>
-__global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2) * 32, 1)
+// HW > 0: HW extra warps gather each group's halo words in-kernel (ntab rows +
+// boundary-plane words, two round trips per group, HW groups in flight) into the
+// stage and arrive on its full barrier -- no separate halo kernel.  Pays off when a
+// rank owns few groups (T r=18 / r=20 on 8 GPUs: the halo kernel's fixed latency).
+template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1,
+          int HW = 0>
+__global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2 + HW) * 32, 1)
 step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                        const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
-    (void)bsrc;
     using W = Wiring<FT, P>;
     using WG = WsGeom<FT, P, WQ, SPLIT>;
     constexpr int NBLK = WG::NBLK;
@@ -486,7 +490,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(full0 + 8 * s, 1);
+            mbar_init(full0 + 8 * s, HW > 0 ? 2 : 1);  // producer (+ bytes) [+ the halo warp]
             mbar_init(empty0 + 8 * s, NCHUNK);
         }
         for (int o = 0; o < NO; ++o) {
@@ -502,6 +506,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     fence_proxy_async_smem();
     __syncthreads();
     pdl_wait();     // the prologue above overlapped the previous kernel's tail (PDL)
+    if constexpr (HW > 0) wait_peers(p);  // in-kernel halo: the peers' pushes of this step
     pdl_trigger();
 
     if (warp == NCW) {  // ---- producer -------------------------------------------------
@@ -511,13 +516,53 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 const uint32_t s = i % NS;
                 if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
                 const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
-                const uint32_t halo_bytes = p.nHp * 4;
+                const uint32_t halo_bytes = HW > 0 ? 0u : p.nHp * 4;
                 mbar_expect_tx(bar, rec_bytes + halo_bytes);
                 bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
                 if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
             }
         }
         return;
+    }
+    if constexpr (HW > 0) {
+        if (warp >= NCW + 2) {  // ---- halo warps: group i = hw (mod HW) --------------------
+            const uint32_t hw = (uint32_t)(warp - NCW - 2);
+            uint32_t i = hw;
+            for (uint32_t g = p.g0 + pair + hw * npairs; g < p.g1; g += HW * npairs, i += HW) {
+                const uint32_t s = i % NS;
+                if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
+                uint32_t* Hs = reinterpret_cast<uint32_t*>(st + s * stage_bytes) + p.Cp;
+                const uint32_t t = g * 32 + lane;
+                for (uint32_t j0 = 0; j0 < p.nH; j0 += 8) {
+                    uint32_t t2[8], sl[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t j = j0 + u;
+                        t2[u] = kNoTile;
+                        sl[u] = 0;
+                        if (j < p.nH) {
+                            sl[u] = __ldg(p.slot + j);
+                            if (t < p.T) t2[u] = __ldg(p.ntab + ((size_t)((sl[u] >> 16) & 0xFFu) * p.T + t));
+                        }
+                    }
+                    uint32_t v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = t2[u] != kNoTile ? __ldcg(bsrc + (size_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)
+                                                : 0u;
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
+                        if (lane == (uint32_t)u) mine = word;
+                    }
+                    if (lane < 8 && j0 + lane < p.nH) Hs[j0 + lane] = mine;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full0 + 8 * s);  // release: the halo words are visible
+            }
+            return;
+        }
     }
     if (warp == NCW + 1) {  // ---- storer ---------------------------------------------------
         if (lane == 0) {

@@ -53,3 +53,11 @@ def test_multirank_auto_transport_picks_p2p():
     out = _bench(2, 12, 29817, transport="auto")
     assert "halo transport p2p" in out["config"]["parallelism"]
     assert out["final_state_hash"] == _bench(1, 12, 0)["final_state_hash"]
+
+
+def test_multirank_p2p_in_kernel_halo_r18():
+    # r=18 picks q=8 with <= 4096 groups per rank: the step kernel gathers the halo
+    # words itself after waiting on the peers' arrival counter
+    single = _bench(1, 18, 0)
+    multi = _bench(2, 18, 29917, transport="p2p")
+    assert multi["final_state_hash"] == single["final_state_hash"]

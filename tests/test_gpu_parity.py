@@ -420,3 +420,22 @@ def test_packed_multistep_fused_and_split(monkeypatch, fuse):
                 assert np.array_equal(sim.front().data, o.front), (desc.name, r, q, n, fuse)
             assert sim.iteration() == 12
             sim.close()
+
+
+@pytest.mark.parametrize("hw", ["0", "1"])
+def test_packed_in_kernel_halo_warps(monkeypatch, hw):
+    # T q=8 with the halo words gathered by warps of the step kernel (default when a
+    # handle owns <= 4096 groups) or by the separate halo kernel: same bytes
+    monkeypatch.setenv("NBBGPU_HALO_WARPS", hw)
+    monkeypatch.setenv("NBBGPU_PACKED_Q", "8")
+    for r in (8, 10, 13):
+        _lockstep_vs_oracle(T, r, conway_rule(), 21 + r, 0.5, 6, kernel="packed")
+    o = oracle.Oracle(T.replicas, T.k, T.s, 13)
+    o.seed(3, 0.5)
+    sim = Simulation(T, 13, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+    sim.seed_random(3, 0.5)
+    sim.step(conway_rule(), 9)
+    for _ in range(9):
+        o.step(conway_rule().birth, conway_rule().survive, conway_rule().moore)
+    assert np.array_equal(sim.front().data, o.front)
+    sim.close()

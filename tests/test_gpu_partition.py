@@ -90,3 +90,13 @@ def test_partitioned_packed(nranks):
     _run(T, 12, nranks, StencilRule(8, 12, Neighborhood.Moore), 5, kernel="packed")
     _run(T, 9, nranks, StencilRule(0x1C9, 0x6, Neighborhood.VonNeumann), 4, kernel="packed")
     _run(C8, 5, nranks, StencilRule(8, 12, Neighborhood.Moore), 4, kernel="packed")
+
+
+@pytest.mark.parametrize("hw", ["0", "1"])
+def test_partitioned_packed_q8_halo_warps(monkeypatch, hw):
+    # T q=8 partitions: halo words gathered in the step kernel (hw=1) or by the halo kernel
+    monkeypatch.setenv("NBBGPU_PACKED_Q", "8")
+    monkeypatch.setenv("NBBGPU_HALO_WARPS", hw)
+    T = builtin_descriptor("sierpinski-triangle")
+    for n in (2, 3, 8):
+        _run(T, 14, n, StencilRule(8, 12, Neighborhood.Moore), 4, kernel="packed")
