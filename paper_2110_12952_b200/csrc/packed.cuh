@@ -398,6 +398,8 @@ __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
@@ -475,6 +477,15 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     constexpr int NCHUNK = WG::NCHUNK;
     constexpr int NCW = NCHUNK * NGRP;
     constexpr int NEP = W::NEP;
+    // boundary words copied from the output record by the storer (large boundaries)
+    // or recomputed by consumer warp 0 (triangle, Vicsek: a few words per group)
+    constexpr bool BST = !std::is_same<FT, TriangleTag>::value && !std::is_same<FT, VicsekTag>::value;
+    // PWS: row micro-blocks (BH = 1) give every consumer warp a contiguous slice of
+    // the output record; each warp bulk-stores its own slice and copies the boundary
+    // words inside it (p.srcidx + nSrc = the sources sorted by cell) -- no storer
+    // round trip per group
+    constexpr bool PWS = BST && W::BH == 1;
+    static_assert(!PWS || NO % NGRP == 0, "per-warp stores reuse an output buffer every NO / NGRP groups");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
@@ -565,17 +576,31 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
     }
     if (warp == NCW + 1) {  // ---- storer ---------------------------------------------------
-        if (lane == 0) {
-            uint32_t i = 0;
-            for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
-                const uint32_t o = i % NO;
-                mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);
-                bulk_s2g(dst + (uint64_t)g * p.Cp + out_off, smem_u32(outs + o * out_bytes), out_bytes);
+        if constexpr (PWS) return;
+        // one bulk store per finished group; with BST the lanes also copy the group's
+        // new boundary words (the output words at the boundary source cells) into the
+        // boundary plane.
+        uint32_t i = 0;
+        for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
+            const uint32_t o = i % NO;
+            mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);
+            const uint32_t* Do = reinterpret_cast<const uint32_t*>(outs + o * out_bytes);
+            if (lane == 0) bulk_s2g(dst + (uint64_t)g * p.Cp + out_off, smem_u32(Do), out_bytes);
+            if constexpr (BST) {
+                for (uint32_t m = lane; m < p.nSrc; m += 32) {
+                    const uint32_t c = __ldg(p.srcidx + m) - out_off;  // (wraps when below this slice)
+                    if (SPLIT == 1 || c < out_words) bdst[(uint64_t)g * p.nSrc + m] = Do[c];
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                // (lagging this wait by one group measured slower: T r=20 0.176 vs
+                //  0.143 ms -- the consumers then wait a storer round trip per group)
                 bulk_wait_read_all();  // the output record may be rewritten
                 mbar_arrive(oempty0 + 8 * o);
             }
-            bulk_wait_all();
         }
+        if (lane == 0) bulk_wait_all();
         return;
     }
     // ---- consumers ---------------------------------------------------------------------
@@ -598,17 +623,54 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
         });
     }
+    // PWS: this warp's output slice [w_lo, w_hi) (slice words) and its boundary
+    // sources [k_lo, k_hi) of the cell-sorted list
+    uint32_t w_lo = 0, w_hi = 0, k_lo = 0, k_hi = 0;
+    if constexpr (PWS) {
+        w_lo = (uint32_t)c * 32 * W::BW;
+        w_hi = c == NCHUNK - 1 ? out_words : w_lo + 32 * W::BW;
+        const uint32_t* sorted = p.srcidx + p.nSrc;
+        for (uint32_t k = lane; k < p.nSrc; k += 32) {
+            const uint32_t cell = __ldg(p.srcidx + __ldg(sorted + k));
+            k_lo += cell < out_off + w_lo;
+            k_hi += cell < out_off + w_hi;
+        }
+        k_lo = __reduce_add_sync(0xFFFFFFFFu, k_lo);
+        k_hi = __reduce_add_sync(0xFFFFFFFFu, k_hi);
+    }
     uint32_t i = (uint32_t)set;
     for (uint32_t g = p.g0 + pair + (uint32_t)set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
         const uint32_t s = i % NS, o = i % NO;
         mbar_wait(full0 + 8 * s, (i / NS) & 1u);
-        if (i >= NO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
+        if constexpr (PWS) {
+            if (i >= NO) {  // this warp's store from NO groups ago has read its slice
+                if (lane == 0) bulk_wait_read<NO / NGRP - 1>();
+                __syncwarp();
+            }
+        } else if (i >= NO) {
+            mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
+        }
         const uint8_t* Sb = st + s * stage_bytes;
         // block_words_r indexes the whole record: shift the slice base back by out_off
         uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * out_bytes) - out_off;
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
         if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
-        if (c == 0 && half == 0)  // boundary plane of the new state
+        if constexpr (PWS) {
+            fence_proxy_async_smem();  // the bulk store reads this slice through the async proxy
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(empty0 + 8 * s);
+                bulk_s2g(dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
+                         (w_hi - w_lo) * 4);
+            }
+            const uint32_t* sorted = p.srcidx + p.nSrc;
+            for (uint32_t k = k_lo + lane; k < k_hi; k += 32) {
+                const uint32_t m = __ldg(sorted + k);
+                bdst[(uint64_t)g * p.nSrc + m] = Do[__ldg(p.srcidx + m)];
+            }
+            continue;
+        }
+        if (!BST && c == 0 && half == 0)  // boundary plane of the new state (few words)
             for (uint32_t m = lane; m < p.nSrc; m += 32)
                 bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
         fence_proxy_async_smem();  // the bulk store reads Do through the async proxy
@@ -618,6 +680,8 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             mbar_arrive(ofull0 + 8 * o);
         }
     }
+    if constexpr (PWS)
+        if (lane == 0) bulk_wait_all();
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() {

@@ -34,8 +34,12 @@ def main(cases):
         steps = int(os.environ.get("QB_STEPS", "20"))
         ms = sim.step_timed(rule, steps) / steps
         cells = d.k ** level
+        extra = ""
+        if os.environ.get("QB_PROF"):
+            tot, main, n = sim.step_profiled(rule, steps)
+            extra = f" | step kernel {main / steps * 1e3:.1f} us of {tot / steps * 1e3:.1f} us, {n / steps:.0f} launches/step"
         print(f"{case:14s} {sim.active_kernel()} {ms:9.4f} ms/step {cells * 1e3 / ms:10.3e} cell-updates/s "
-              f"hash={sim.state_hash():016x} held={sim.peak_bytes() / 1e9:.3f} GB", flush=True)
+              f"hash={sim.state_hash():016x} held={sim.peak_bytes() / 1e9:.3f} GB{extra}", flush=True)
         sim.close()
 
 
