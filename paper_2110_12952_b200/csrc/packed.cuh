@@ -64,6 +64,9 @@ struct PackedStepParams {
     // pushed this step's boundary words (system-scope arrival counter >= target)
     const uint32_t* wait_cnt;
     uint32_t wait_target;
+    // stream the group records through L2 as evict-first (TMA cache hint), so the
+    // small per-step tables (ntab, boundary planes, halo words) stay L2-resident
+    int stream_ef;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
@@ -134,12 +137,17 @@ __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint
 // 32 x 32 bit transpose across a warp: lane i holds row i (bit k = column k) ->
 // lane k holds column k (bit i = row i).  Five shuffle-xor block swaps.
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+    // per stage: shuffle, rotate (left by j in the low-half lanes, right by j in the
+    // high-half lanes: the wrapped-in bits fall under the mask) and a bit select
 #pragma unroll
     for (int j = 16; j > 0; j >>= 1) {
         const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
                                                  : j == 2 ? 0x33333333u : 0x55555555u;
+        const bool hi = (lane & j) != 0;
         const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
-        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+        const uint32_t r = __funnelshift_l(y, y, hi ? 32 - j : j);
+        const uint32_t K = hi ? ~m : m;
+        x = (x & K) | (r & ~K);
     }
     return x;
 }
@@ -152,32 +160,65 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) 
 // shuffle, and a final transpose turns the tiles' bits back into the 32 halo
 // words -- ~70 instructions per 32 slots (1-2 source groups) instead of a load +
 // ballot per slot.  Directions with a few slots (corners) keep the ballot form.
-template <bool NC>
-__device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
-                                               uint32_t g, int ds, uint32_t lane) {
-    const uint32_t t = g * 32 + lane;
-    uint32_t* Hg = H + (uint64_t)g * p.nHp;
-    const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)ds * p.T + t)) : kNoTile;  // lane = tile
+// one used direction ds of group g (Hg = its halo words); t2 = lane's neighbour tile
+template <bool NC, int NCH>
+__device__ __forceinline__ void halo_dir(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* Hg, int ds,
+                                         uint32_t t2, uint32_t lane) {
     const uint32_t j_beg = p.dfirst[ds], j_end = p.dfirst[ds + 1];
     if (j_end - j_beg >= 8) {
         const bool valid = t2 != kNoTile;
         const uint32_t G2 = t2 >> 5, col_of_tile = t2 & 31;
-        for (uint32_t j0 = j_beg; j0 < j_end; j0 += 32) {
-            const uint32_t j = j0 + lane;  // lane = slot
-            const uint32_t my_m = j < j_end ? (__ldg(p.slot + j) & 0xFFFFu) : 0u;
-            uint32_t out = 0;  // lane = tile: bit i = slot j0 + i
-            uint32_t remaining = __ballot_sync(0xFFFFFFFFu, valid);
-            while (remaining) {  // one pass per distinct source group (warp-uniform)
-                const uint32_t G = __shfl_sync(0xFFFFFFFFu, G2, __ffs(remaining) - 1);
-                const uint32_t members = __ballot_sync(0xFFFFFFFFu, valid && G2 == G);
-                const uint32_t w = j < j_end ? ld_bnd<NC>(bsrc + (size_t)G * p.nSrc + my_m) : 0u;
-                const uint32_t col = warp_transpose32(w, lane);        // lane c: bit i = bit c of word i
-                const uint32_t picked = __shfl_sync(0xFFFFFFFFu, col, col_of_tile);
-                if ((members >> lane) & 1u) out = picked;
-                remaining &= ~members;
+        // the distinct source groups of the 32 neighbour tiles, first up to 4 in
+        // registers (warp-uniform), so their boundary-word loads go out together
+        uint32_t Gs[4] = {0u, 0u, 0u, 0u};
+        int nG = 0;
+        uint32_t remaining = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (remaining) {
+                Gs[u] = __shfl_sync(0xFFFFFFFFu, G2, __ffs(remaining) - 1);
+                remaining &= ~__ballot_sync(0xFFFFFFFFu, valid && G2 == Gs[u]);
+                nG = u + 1;
             }
-            const uint32_t halo = warp_transpose32(out, lane);       // lane i: bit b = tile b, slot i
-            if (j < j_end) Hg[j] = halo;
+        // NCH chunks of 32 slots per round trip (more registers, fewer round trips)
+        for (uint32_t jc = j_beg; jc < j_end; jc += 32 * NCH) {
+            uint32_t mm[NCH], w[NCH][4];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const uint32_t j = jc + 32 * c + lane;
+                mm[c] = j < j_end ? (__ldg(p.slot + j) & 0xFFFFu) : 0u;
+            }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    w[c][u] = (u < nG && jc + 32 * c + lane < j_end) ? ld_bnd<NC>(bsrc + (size_t)Gs[u] * p.nSrc + mm[c])
+                                                                     : 0u;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const uint32_t j0 = jc + 32 * c, j = j0 + lane;  // lane = slot
+                if (j0 >= j_end) break;
+                uint32_t out = 0;  // lane = tile: bit i = slot j0 + i
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < nG) {
+                        const uint32_t col = warp_transpose32(w[c][u], lane);  // lane c: bit i = bit c of word i
+                        const uint32_t picked = __shfl_sync(0xFFFFFFFFu, col, col_of_tile);
+                        if (valid && G2 == Gs[u]) out = picked;
+                    }
+                uint32_t rem = remaining;  // more than 4 source groups (rare): one pass each
+                while (rem) {
+                    const uint32_t G = __shfl_sync(0xFFFFFFFFu, G2, __ffs(rem) - 1);
+                    const uint32_t members = __ballot_sync(0xFFFFFFFFu, valid && G2 == G);
+                    const uint32_t wx = j < j_end ? ld_bnd<NC>(bsrc + (size_t)G * p.nSrc + mm[c]) : 0u;
+                    const uint32_t col = warp_transpose32(wx, lane);
+                    const uint32_t picked = __shfl_sync(0xFFFFFFFFu, col, col_of_tile);
+                    if ((members >> lane) & 1u) out = picked;
+                    rem &= ~members;
+                }
+                const uint32_t halo = warp_transpose32(out, lane);  // lane i: bit b = tile b, slot i
+                if (j < j_end) Hg[j] = halo;
+            }
         }
         return;
     }
@@ -200,6 +241,33 @@ __device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const 
     if (j_beg + lane < j_end) Hg[j_beg + lane] = mine;
 }
 
+template <bool NC>
+__device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
+                                               uint32_t g, int ds, uint32_t lane) {
+    const uint32_t t = g * 32 + lane;
+    const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)ds * p.T + t)) : kNoTile;  // lane = tile
+    halo_dir<NC, 1>(p, bsrc, H + (uint64_t)g * p.nHp, ds, t2, lane);
+}
+
+// one task per group: the neighbour tiles of every direction are loaded up front
+// and each direction's loads go out in one round trip (fewer, longer tasks: for
+// many groups -- H r=11 halo 0.127 -> 0.115 ms; with ~1K groups too few warps)
+template <bool NC>
+__device__ __forceinline__ void halo_group_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
+                                                uint32_t g, uint32_t lane) {
+    const uint32_t t = g * 32 + lane;
+    const bool in = t < p.T;
+    // directions in a rolled loop (small code: the unrolled form stalled on the
+    // instruction cache) with the next direction's neighbour tile prefetched
+    uint32_t t2 = in ? __ldg(p.ntab + t) : kNoTile;
+#pragma unroll 1
+    for (int d = 0; d < p.nD; ++d) {
+        const uint32_t t2n = (d + 1 < p.nD && in) ? __ldg(p.ntab + ((size_t)(d + 1) * p.T + t)) : kNoTile;
+        halo_dir<NC, 3>(p, bsrc, H + (uint64_t)g * p.nHp, d, t2, lane);
+        t2 = t2n;
+    }
+}
+
 // large halos -> tasks per (group, direction) with transposed edge gathers; small
 // halos (triangle, Vicsek: 4-8 slots) -> tasks of 4 slots, lane = tile
 __host__ __device__ __forceinline__ bool halo_use_wide(uint32_t nH, uint32_t groups) {
@@ -218,20 +286,24 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
     else halo4_task<NC>(p, bsrc, H, wi, lane);
 }
 
-// WIDE_HALO is compile-time so the small-halo variant keeps its 30 registers
-// (full occupancy: this kernel is latency-bound)
-template <bool WIDE_HALO, int SPW = 4, bool NC = true>
+// HMODE is compile-time so the small-halo variant keeps its 30 registers (full
+// occupancy: this kernel is latency-bound).  0: tasks of SPW slots (small halos),
+// 1: (group, direction) tasks, 2: group tasks (all directions of a group)
+template <int HMODE, int SPW = 4, bool NC = true>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
     pdl_wait();     // bsrc comes from the previous step kernel
     wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
     pdl_trigger();  // the step kernel may launch and run its prologue
-    const uint64_t nw = WIDE_HALO ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
-                                  : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
+    const uint64_t nw = HMODE == 2 ? (uint64_t)(p.g1 - p.g0)
+                      : HMODE == 1 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
+                                   : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        if constexpr (WIDE_HALO) {
+        if constexpr (HMODE == 2) {
+            halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
+        } else if constexpr (HMODE == 1) {
             const uint32_t w32 = (uint32_t)wi, gi = w32 / (uint32_t)p.nD;
             halo_wide_task<NC>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
         } else {
@@ -393,6 +465,33 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, uint32_t src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(src), "r"(bytes), "l"(pol) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// record streams of the ws3 kernel: evict-first when p.stream_ef
+__device__ __forceinline__ void rec_g2s(const PackedStepParams& p, uint32_t dst, const void* src, uint32_t bytes,
+                                       uint32_t mbar) {
+    if (p.stream_ef) bulk_g2s_hint(dst, src, bytes, mbar, l2_evict_first_policy());
+    else bulk_g2s(dst, src, bytes, mbar);
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes);
+__device__ __forceinline__ void rec_s2g(const PackedStepParams& p, void* dst, uint32_t src, uint32_t bytes) {
+    if (p.stream_ef) bulk_s2g_hint(dst, src, bytes, l2_evict_first_policy());
+    else bulk_s2g(dst, src, bytes);
+}
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
                  : "memory");
@@ -415,16 +514,28 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
     const uint32_t by = blk / BPR, bx = blk - by * BPR;
     const uint32_t base = by * (BH * WQ) + bx * BW;
     const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
+    // row blocks with BW % 4 == 0 (carpet: BW = 8, candy: 12): 16-byte loads and
+    // stores -- lanes sit BW words apart, so single-word accesses conflict BW/gcd-way
+    constexpr bool VEC = BH == 1 && BW % 4 == 0;
     uint32_t own[NB], ext[NEP];
-    static_for<NB>([&](auto n) {
-        constexpr int N = decltype(n)::value;
-        own[N] = Sw[(N / BW) * WQ + N % BW];
-    });
+    if constexpr (VEC) {
+        static_for<NB / 4>([&](auto q) {
+            constexpr int Q = decltype(q)::value;
+            const uint4 v = reinterpret_cast<const uint4*>(Sw)[Q];
+            own[4 * Q] = v.x; own[4 * Q + 1] = v.y; own[4 * Q + 2] = v.z; own[4 * Q + 3] = v.w;
+        });
+    } else {
+        static_for<NB>([&](auto n) {
+            constexpr int N = decltype(n)::value;
+            own[N] = Sw[(N / BW) * WQ + N % BW];
+        });
+    }
     static_for<NEP>([&](auto e) {
         constexpr int E = decltype(e)::value;
         ext[E] = *reinterpret_cast<const uint32_t*>(Sb + toff[E]);
     });
     uint32_t* Dw = Do + base;
+    uint32_t res[VEC ? 4 : 1];
     static_for<NB>([&](auto n) {
         constexpr int N = decltype(n)::value;
         uint32_t x[8];
@@ -436,7 +547,14 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
             else x[J] = ext[-SJ - 2];
         });
         const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
-        Dw[(N / BW) * WQ + N % BW] = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
+        const uint32_t r = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
+        if constexpr (VEC) {
+            res[N % 4] = r;
+            if constexpr (N % 4 == 3)
+                reinterpret_cast<uint4*>(Dw)[N / 4] = make_uint4(res[0], res[1], res[2], res[3]);
+        } else {
+            Dw[(N / BW) * WQ + N % BW] = r;
+        }
     });
 }
 
@@ -529,7 +647,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
                 const uint32_t halo_bytes = HW > 0 ? 0u : p.nHp * 4;
                 mbar_expect_tx(bar, rec_bytes + halo_bytes);
-                bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
+                rec_g2s(p, dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
                 if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
             }
         }
@@ -585,7 +703,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             const uint32_t o = i % NO;
             mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);
             const uint32_t* Do = reinterpret_cast<const uint32_t*>(outs + o * out_bytes);
-            if (lane == 0) bulk_s2g(dst + (uint64_t)g * p.Cp + out_off, smem_u32(Do), out_bytes);
+            if (lane == 0) rec_s2g(p, dst + (uint64_t)g * p.Cp + out_off, smem_u32(Do), out_bytes);
             if constexpr (BST) {
                 for (uint32_t m = lane; m < p.nSrc; m += 32) {
                     const uint32_t c = __ldg(p.srcidx + m) - out_off;  // (wraps when below this slice)
@@ -660,7 +778,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(empty0 + 8 * s);
-                bulk_s2g(dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
+                rec_s2g(p, dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
                          (w_hi - w_lo) * 4);
             }
             const uint32_t* sorted = p.srcidx + p.nSrc;
