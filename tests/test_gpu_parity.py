@@ -424,12 +424,13 @@ def test_packed_multistep_fused_and_split(monkeypatch, fuse):
 
 @pytest.mark.parametrize("hw", ["0", "1"])
 def test_packed_in_kernel_halo_warps(monkeypatch, hw):
-    # T q=8 with the halo words gathered by warps of the step kernel (default when a
-    # handle owns <= 4096 groups) or by the separate halo kernel: same bytes
+    # T q=6 / q=8 with the halo words gathered by warps of the step kernel (default
+    # when a handle owns <= 4096 groups) or by the separate halo kernel: same bytes
     monkeypatch.setenv("NBBGPU_HALO_WARPS", hw)
-    monkeypatch.setenv("NBBGPU_PACKED_Q", "8")
-    for r in (8, 10, 13):
+    for q, r in ((6, 6), (6, 9), (6, 12), (8, 8), (8, 10)):
+        monkeypatch.setenv("NBBGPU_PACKED_Q", str(q))
         _lockstep_vs_oracle(T, r, conway_rule(), 21 + r, 0.5, 6, kernel="packed")
+    monkeypatch.setenv("NBBGPU_PACKED_Q", "8")
     o = oracle.Oracle(T.replicas, T.k, T.s, 13)
     o.seed(3, 0.5)
     sim = Simulation(T, 13, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
