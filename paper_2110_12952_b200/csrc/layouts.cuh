@@ -179,6 +179,7 @@ struct ViewSrc {
     const uint8_t* bytes;   // byte layouts
     const uint32_t* words;  // packed layout
     uint32_t wq, Wc, Cp;    // packed geometry
+    uint32_t ilv;           // interleaved record layout (rec_word)
     BlockedGeom bg;         // blocked layout
 };
 
@@ -195,7 +196,7 @@ __device__ __forceinline__ uint8_t view_cell(const Frac& f, const ViewSrc& v, ui
     if (!v.packed) return v.bytes[(uint64_t)cy * f.w + cx];
     const uint32_t X = cx / v.wq, c = cx % v.wq, Y = cy / v.wq, a = cy % v.wq;
     const uint64_t t = (uint64_t)Y * v.Wc + X;
-    return (uint8_t)((v.words[(t / 32) * v.Cp + (uint64_t)a * v.wq + c] >> (t % 32)) & 1u);
+    return (uint8_t)((v.words[(t / 32) * v.Cp + rec_word(v.ilv, v.wq, a, c)] >> (t % 32)) & 1u);
 }
 
 // PBM: row stride n + 1 with '\n' at the end, characters '0' / '1'; else bytes 0 / 1

@@ -1222,6 +1222,7 @@ void render_view(nbbgpu_t h, uint8_t* dst, int pbm) {
         v.wq = (uint32_t)h->pp.wq;
         v.Wc = (uint32_t)h->pp.Wc;
         v.Cp = (uint32_t)h->pp.Cp;
+        v.ilv = h->pp.ilv ? 1u : 0u;
     }
     v.bg = h->bg;
     const uint64_t n = (uint64_t)h->hf.side, total = n * (pbm ? n + 1 : n);

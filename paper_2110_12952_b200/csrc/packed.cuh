@@ -37,8 +37,20 @@ constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Record word of local cell (row a, column c).  Row-major, except the carpet at
+// WQ = 64 (ilv): its 8-cell row micro-blocks are interleaved so that the 32 blocks
+// of four rows -- one consumer warp -- sit in 32 consecutive words for every cell
+// position n: word = ((a / 4) * 8 + n) * 32 + (a % 4) * 8 + block, c = 8 * block + n.
+// Lane = block then reads and writes conflict-free (row-major blocks start 8 words
+// apart: every shared access of the step kernel conflicted 4- to 8-way).
+__host__ __device__ __forceinline__ uint32_t rec_word(uint32_t ilv, uint32_t wq, uint32_t a, uint32_t c) {
+    if (ilv) return (((a >> 2) * 8 + (c & 7)) << 5) + (a & 3) * 8 + (c >> 3);
+    return a * wq + c;
+}
+
 struct PackedGeom {
     Frac f;
+    uint32_t ilv;            // interleaved record layout (rec_word)
     uint32_t q, WQ, C, Cp;   // tile level, tile width, local cells, padded words per group
     uint32_t Wc, Hc, L;      // coarse dims, coarse level r - q
     uint32_t T, NG;          // tiles, groups
@@ -516,9 +528,18 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
     const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
     // row blocks with BW % 4 == 0 (carpet: BW = 8, candy: 12): 16-byte loads and
     // stores -- lanes sit BW words apart, so single-word accesses conflict BW/gcd-way
-    constexpr bool VEC = BH == 1 && BW % 4 == 0;
+    // interleaved carpet records (rec_word): cell n of block blk at word
+    // (blk / 32 * 8 + n) * 32 + blk % 32
+    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    constexpr bool VEC = BH == 1 && BW % 4 == 0 && !ILV;
     uint32_t own[NB], ext[NEP];
-    if constexpr (VEC) {
+    if constexpr (ILV) {
+        const uint32_t* Sq = reinterpret_cast<const uint32_t*>(Sb) + (blk >> 5) * (NB * 32) + (blk & 31);
+        static_for<NB>([&](auto n) {
+            constexpr int N = decltype(n)::value;
+            own[N] = Sq[N * 32];
+        });
+    } else if constexpr (VEC) {
         static_for<NB / 4>([&](auto q) {
             constexpr int Q = decltype(q)::value;
             const uint4 v = reinterpret_cast<const uint4*>(Sw)[Q];
@@ -534,7 +555,7 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
         constexpr int E = decltype(e)::value;
         ext[E] = *reinterpret_cast<const uint32_t*>(Sb + toff[E]);
     });
-    uint32_t* Dw = Do + base;
+    uint32_t* Dw = ILV ? Do + (blk >> 5) * (NB * 32) + (blk & 31) : Do + base;
     uint32_t res[VEC ? 4 : 1];
     static_for<NB>([&](auto n) {
         constexpr int N = decltype(n)::value;
@@ -548,7 +569,9 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
         });
         const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
         const uint32_t r = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
-        if constexpr (VEC) {
+        if constexpr (ILV) {
+            Dw[N * 32] = r;
+        } else if constexpr (VEC) {
             res[N % 4] = r;
             if constexpr (N % 4 == 3)
                 reinterpret_cast<uint4*>(Dw)[N / 4] = make_uint4(res[0], res[1], res[2], res[3]);
@@ -1154,7 +1177,7 @@ pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32
             const uint32_t t = g * 32 + lane;
             lanes = __ballot_sync(0xFFFFFFFFu, t >= tlo && t < thi && t < G.T);
         }
-        uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        uint32_t* R = P + (uint64_t)g * G.Cp;
         for (uint32_t c = lane; c < ((G.WQ + 31) & ~31u); c += 32) {
             uint32_t word = 0, over = 0;
             if (c < G.WQ) {
@@ -1167,7 +1190,8 @@ pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32
                 word &= lanes;
                 if (over) *bad = 1;
                 // groups shared with a neighbouring row chunk keep the other tiles' bits
-                R[c] = lanes == 0xFFFFFFFFu ? word : ((R[c] & ~lanes) | word);
+                uint32_t& Rw = R[rec_word(G.ilv, G.WQ, a, c)];
+                Rw = lanes == 0xFFFFFFFFu ? word : ((Rw & ~lanes) | word);
             }
         }
         __syncwarp();
@@ -1184,9 +1208,9 @@ unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_
     const uint64_t nw = (uint64_t)(ghi - glo) * G.WQ;
     for (uint64_t wi = blockIdx.x * (uint64_t)kConvWarps + wib; wi < nw; wi += (uint64_t)gridDim.x * kConvWarps) {
         const uint32_t g = glo + (uint32_t)(wi / G.WQ), a = (uint32_t)(wi % G.WQ);
-        const uint32_t* R = P + (uint64_t)g * G.Cp + (uint64_t)a * G.WQ;
+        const uint32_t* R = P + (uint64_t)g * G.Cp;
         for (uint32_t c = lane; c < G.WQ; c += 32) {
-            const uint32_t word = R[c];
+            const uint32_t word = R[rec_word(G.ilv, G.WQ, a, c)];
 #pragma unroll 8
             for (uint32_t b = 0; b < 32; ++b) sb[b * G.WQ + c] = (uint8_t)((word >> b) & 1u);
         }
