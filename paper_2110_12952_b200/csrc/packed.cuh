@@ -253,12 +253,12 @@ __device__ __forceinline__ void halo_dir(const PackedStepParams& p, const uint32
     if (j_beg + lane < j_end) Hg[j_beg + lane] = mine;
 }
 
-template <bool NC>
+template <bool NC, int NCH = 1>
 __device__ __forceinline__ void halo_wide_task(const PackedStepParams& p, const uint32_t* bsrc, uint32_t* H,
                                                uint32_t g, int ds, uint32_t lane) {
     const uint32_t t = g * 32 + lane;
     const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)ds * p.T + t)) : kNoTile;  // lane = tile
-    halo_dir<NC, 1>(p, bsrc, H + (uint64_t)g * p.nHp, ds, t2, lane);
+    halo_dir<NC, NCH>(p, bsrc, H + (uint64_t)g * p.nHp, ds, t2, lane);
 }
 
 // one task per group: the neighbour tiles of every direction are loaded up front
@@ -300,7 +300,8 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
 
 // HMODE is compile-time so the small-halo variant keeps its 30 registers (full
 // occupancy: this kernel is latency-bound).  0: tasks of SPW slots (small halos),
-// 1: (group, direction) tasks, 2: group tasks (all directions of a group)
+// 1: (group, direction) tasks, 2: group tasks (all directions of a group),
+// 3: (group, direction) tasks with 3 chunks of loads per round trip (few groups)
 template <int HMODE, int SPW = 4, bool NC = true>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
@@ -309,15 +310,15 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
     wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
     pdl_trigger();  // the step kernel may launch and run its prologue
     const uint64_t nw = HMODE == 2 ? (uint64_t)(p.g1 - p.g0)
-                      : HMODE == 1 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
+                      : HMODE == 1 || HMODE == 3 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
                                    : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         if constexpr (HMODE == 2) {
             halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
-        } else if constexpr (HMODE == 1) {
+        } else if constexpr (HMODE == 1 || HMODE == 3) {
             const uint32_t w32 = (uint32_t)wi, gi = w32 / (uint32_t)p.nD;
-            halo_wide_task<NC>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
+            halo_wide_task<NC, HMODE == 3 ? 3 : 1>(p, bsrc, H, p.g0 + gi, (int)(w32 - gi * (uint32_t)p.nD), lane);
         } else {
             halo4_task<NC, SPW>(p, bsrc, H, wi, lane);
         }
