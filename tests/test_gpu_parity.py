@@ -440,3 +440,18 @@ def test_packed_in_kernel_halo_warps(monkeypatch, hw):
         o.step(conway_rule().birth, conway_rule().survive, conway_rule().moore)
     assert np.array_equal(sim.front().data, o.front)
     sim.close()
+
+
+@pytest.mark.parametrize("env", [("NBBGPU_HALO_GROUP", "1"), ("NBBGPU_HALO_GROUP", "0"),
+                                 ("NBBGPU_HALO_NCH3", "1"), ("NBBGPU_HALO_NCH3", "0")])
+def test_large_halo_task_modes(monkeypatch, env):
+    # the wide-halo gathers (group tasks / direction tasks, 1 or 3 chunks of loads
+    # per round trip) give the same bytes on halo-heavy fractals
+    monkeypatch.setenv(*env)
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    for desc, r in ((CARPET, 5), (H, 5), (Y, 5)):
+        _lockstep_vs_oracle(desc, r, conway_rule(), 31 + r, 0.5, 4, kernel="packed")
+        _lockstep_vs_oracle(desc, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 32 + r, 0.5, 3,
+                            kernel="packed")
