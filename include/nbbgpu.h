@@ -94,6 +94,10 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density);
 /* nsteps x Simulation::step (stencil.cpp:262-289) with rule
  * StencilRule{birth, survive, moore ? Moore : VonNeumann} (stencil.hpp:18-31). */
 int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps);
+/* nbbgpu_step without the final host synchronisation (the steps are enqueued on
+ * the handle's stream; the state must not be read before nbbgpu_synchronize). */
+int nbbgpu_step_async(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps);
+int nbbgpu_synchronize(nbbgpu_t h);
 
 /* Same as nbbgpu_step, also returning the device time of the nsteps step
  * kernels measured with CUDA events on the handle's stream. */
@@ -212,6 +216,13 @@ int nbbgpu_halo_elem_bytes(nbbgpu_t h, int* out);
 int nbbgpu_p2p_handle_bytes(void);
 int nbbgpu_p2p_export(nbbgpu_t h, uint8_t* out, int bytes);
 int nbbgpu_p2p_attach(nbbgpu_t h, const uint8_t* all_handles, int bytes_per_rank, int nranks);
+/* The same transport for ONE process driving every rank (the proposed
+ * SimOptions::gpus: "one host thread drives all GPUs"): handles[i]
+ * is the packed partition rank i of nranks (nbbgpu_partition), one per device;
+ * peer access is enabled between the devices and the peers' planes are plain
+ * device pointers (no IPC).  Step the handles with nbbgpu_step_async, then
+ * nbbgpu_synchronize each. */
+int nbbgpu_p2p_attach_local(nbbgpu_t* handles, int nranks);
 
 /* Raw device pointer of the front buffer (reference bytes, or packed words for
  * the PACKED kernel; for peer-to-peer transports). */

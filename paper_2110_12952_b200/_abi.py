@@ -69,6 +69,9 @@ SIGNATURES = {
     "nbbgpu_p2p_handle_bytes": (C.c_int, []),
     "nbbgpu_p2p_export": (C.c_int, [_H, C.c_void_p, C.c_int]),
     "nbbgpu_p2p_attach": (C.c_int, [_H, C.c_void_p, C.c_int, C.c_int]),
+    "nbbgpu_p2p_attach_local": (C.c_int, [C.c_void_p, C.c_int]),
+    "nbbgpu_step_async": (C.c_int, [_H, C.c_uint16, C.c_uint16, C.c_int, C.c_int64]),
+    "nbbgpu_synchronize": (C.c_int, [_H]),
     "nbbgpu_plan_packed_level": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, _P(C.c_int)]),
     "nbbgpu_plan_packed": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, _P(C.c_int64)]),
     "nbbgpu_plan_packed_partition": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int,

@@ -985,7 +985,7 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
 }
 
 static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
-                      float* ms, float* main_ms = nullptr, uint64_t* launches = nullptr) {
+                      float* ms, float* main_ms = nullptr, uint64_t* launches = nullptr, bool sync = true) {
     check_handle(h);
     if (nsteps < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "steps must be >= 0");
     moore = moore ? 1 : 0;
@@ -1029,6 +1029,10 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     h->prof = nullptr;
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));
+    if (!sync) {  // nbbgpu_step_async: enqueued only
+        if (launches) *launches = h->launches - l0;
+        return;
+    }
     CK(cudaStreamSynchronize(h->stream));
     if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
     if (main_ms) {
@@ -1061,6 +1065,17 @@ int nbbgpu_step_profiled(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore
 
 int nbbgpu_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps) {
     return guarded([&] { step_impl(h, birth, survive, moore, nsteps, nullptr); });
+}
+
+int nbbgpu_step_async(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps) {
+    return guarded([&] { step_impl(h, birth, survive, moore, nsteps, nullptr, nullptr, nullptr, false); });
+}
+
+int nbbgpu_synchronize(nbbgpu_t h) {
+    return guarded([&] {
+        check_handle(h);
+        CK(cudaStreamSynchronize(h->stream));
+    });
 }
 
 int nbbgpu_step_timed(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,

@@ -15,6 +15,7 @@ exercised by both.  The partial state hashes add up to the global hash
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List
 
@@ -22,6 +23,8 @@ import numpy as np
 
 from . import _abi
 from .descriptor import FractalDescriptor
+from .errors import OutOfDomain
+from .stencil import Neighborhood, StencilRule
 
 
 def _needs(desc: FractalDescriptor, level: int, tile_level: int, rank: int, nranks: int,
@@ -361,3 +364,146 @@ class DistributedSimulation:
         parts = [torch.zeros_like(t) for _ in range(self.nranks)]
         self.dist.all_gather(parts, t)
         return wrap_u64_sum(int(q[0]) | (int(q[1]) << 32) for q in parts)
+
+
+class MultiGpuSimulation:
+    """Simulation(..., SimOptions(gpus=N)): ONE process drives N packed partitions,
+    one per device (SURVEY.md 8b "one host thread drives all GPUs"; 8e).  Rank i
+    owns groups [g0, g1) of the packed layout on devices[i]; the peer-memory
+    transport is attached in-process (nbbgpu_p2p_attach_local: the peers' boundary
+    planes are device pointers over NVLink, each step pushes the words a peer needs
+    and bumps its arrival counter).  step() enqueues every rank's steps (interleaved,
+    so no rank waits on a peer that is not queued yet) and then synchronises; ranks
+    sharing a device (tests on one GPU) step one at a time instead, since a spinning
+    kernel could then starve its peer of SMs.  Same methods as Simulation."""
+
+    def __init__(self, desc: FractalDescriptor, level: int, backend, options):
+        from dataclasses import replace
+        from .simulation import Simulation
+        from .stencil import Backend
+        if backend != Backend.GpuCompact or options.block_size > 0:
+            raise OutOfDomain("gpus > 1 applies to the linear compact backend")
+        n = int(options.gpus)
+        devices = list(options.devices) if options.devices is not None else list(range(n))
+        if len(devices) != n:
+            raise OutOfDomain("SimOptions.devices must list one device per gpu")
+        self.desc, self._level, self.options = desc, level, options
+        self.devices = devices
+        self.shared_device = len(set(devices)) < n
+        self.ranks = []
+        L = _abi.lib()
+        for r in range(n):
+            o = replace(options, gpus=1, devices=None, device=devices[r], kernel="packed")
+            sim = Simulation(desc, level, backend, o)
+            _abi.check(L.nbbgpu_partition(sim.handle(), r, n))
+            self.ranks.append(sim)
+        arr = (C.c_void_p * n)(*[s.handle().value for s in self.ranks])
+        _abi.check(L.nbbgpu_p2p_attach_local(arr, n))
+        q = self.ranks[0].active_kernel()[1]
+        self.plans = [PartitionPlan(desc, level, r, n, tile_level=q, packed=True) for r in range(n)]
+        self._front_cache = None
+
+    # -- lifetime ---------------------------------------------------------------
+    def close(self) -> None:
+        for s in getattr(self, "ranks", []):
+            s.close()
+        self.ranks = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- geometry -----------------------------------------------------------------
+    def level(self) -> int:
+        return self._level
+
+    def side(self) -> int:
+        return self.ranks[0].side()
+
+    def compact_dims(self):
+        return self.ranks[0].compact_dims()
+
+    def iteration(self) -> int:
+        return self.ranks[0].iteration()
+
+    def stored_cells(self) -> int:
+        return self.ranks[0].stored_cells()
+
+    def peak_bytes(self) -> int:
+        return sum(s.peak_bytes() for s in self.ranks)
+
+    def active_kernel(self):
+        return self.ranks[0].active_kernel()
+
+    # -- state --------------------------------------------------------------------
+    def seed_random(self, seed: int, density: float) -> None:
+        self._front_cache = None
+        for s in self.ranks:
+            s.seed_random(seed, density)
+
+    def step(self, rule: StencilRule, nsteps: int = 1) -> None:
+        self._front_cache = None
+        for s in self.ranks:
+            s._front_cache = None  # stepped below through the C ABI directly
+        L = _abi.lib()
+        args = (rule.birth & 0xFFFF, rule.survive & 0xFFFF, int(rule.neighborhood == Neighborhood.Moore))
+        for _ in range(int(nsteps)):
+            for s in self.ranks:
+                _abi.check(L.nbbgpu_step_async(s.handle(), *args, 1))
+                if self.shared_device:
+                    _abi.check(L.nbbgpu_synchronize(s.handle()))
+        for s in self.ranks:
+            _abi.check(L.nbbgpu_synchronize(s.handle()))
+
+    def step_timed(self, rule: StencilRule, nsteps: int) -> float:
+        """Wall-clock ms of nsteps on all ranks (enqueue + synchronise)."""
+        for s in self.ranks:
+            _abi.check(_abi.lib().nbbgpu_synchronize(s.handle()))
+        t0 = time.perf_counter()
+        self.step(rule, nsteps)
+        return (time.perf_counter() - t0) * 1e3
+
+    def state_hash(self) -> int:
+        parts = []
+        for s in self.ranks:
+            v = C.c_uint64()
+            _abi.check(_abi.lib().nbbgpu_state_hash_owned(s.handle(), C.byref(v)))
+            parts.append(v.value)
+        return wrap_u64_sum(parts)
+
+    def front(self):
+        if self._front_cache is None:
+            g = None
+            for s, plan in zip(self.ranks, self.plans):
+                f = s.front()
+                if g is None:
+                    g = f.data.copy()
+                m = plan.owned_cell_mask()
+                g[m] = f.data[m]
+            f0 = self.ranks[0].front()
+            self._front_cache = type(f0)(f0.layout, g, f0.width, f0.height, f0.side)
+        return self._front_cache
+
+    def upload(self, data: np.ndarray) -> None:
+        self._front_cache = None
+        for s in self.ranks:
+            s.upload(data)
+
+    def cell(self, e) -> int:
+        x, y = int(e[0]), int(e[1])
+        side = self.side()
+        if not (0 <= x < side and 0 <= y < side):
+            return self.ranks[0].cell(e)  # the reference's out-of-domain behaviour
+        comp, _ = self.ranks[0].nu_batch(np.array([[x, y]], dtype=np.int32))
+        cx, cy = int(comp[0][0]), int(comp[0][1])
+        if cx < 0 or cy < 0:
+            return 0  # not a fractal cell
+        w, _ = self.compact_dims()
+        return int(self.front().data[cy * w + cx])
+
+    def set_cell(self, e, state: int) -> None:
+        self._front_cache = None
+        for s in self.ranks:
+            s.set_cell(e, state)

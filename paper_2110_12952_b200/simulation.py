@@ -36,6 +36,10 @@ class SimOptions:
     device: int = 0
     kernel: str = "auto"
     map_variant: str = "digit"
+    # SimOptions::gpus (additive): > 1 -> one process drives `gpus`
+    # partitions (distributed.MultiGpuSimulation) on `devices` (default 0..gpus-1)
+    gpus: int = 1
+    devices: Optional[List[int]] = None
 
 
 @dataclass
@@ -56,6 +60,13 @@ class HostGrid:
 
 
 class Simulation:
+    def __new__(cls, desc: FractalDescriptor = None, level: int = 0, backend: Backend = Backend.GpuCompact,
+                options: Optional[SimOptions] = None):
+        if cls is Simulation and options is not None and options.gpus > 1:
+            from .distributed import MultiGpuSimulation
+            return MultiGpuSimulation(desc, level, backend, options)
+        return super().__new__(cls)
+
     def __init__(self, desc: FractalDescriptor, level: int,
                  backend: Backend = Backend.GpuCompact, options: Optional[SimOptions] = None):
         options = options or SimOptions()
