@@ -780,6 +780,16 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         k_lo = __reduce_add_sync(0xFFFFFFFFu, k_lo);
         k_hi = __reduce_add_sync(0xFFFFFFFFu, k_hi);
     }
+    // up to 64 boundary sources of the slice: (m, word) pairs held in registers
+    // (carpet r=9 0.0207 -> 0.0188 ms; candy, with few sources per warp, keeps the
+    // loop: 0.238 vs 0.244 ms)
+    constexpr bool REGB = PWS && !std::is_same<FT, CandyTag>::value;
+    uint32_t bm0 = 0, bw0 = 0, bm1 = 0, bw1 = 0;
+    if constexpr (REGB) {
+        const uint32_t* sorted = p.srcidx + p.nSrc;
+        if (k_lo + lane < k_hi) { bm0 = __ldg(sorted + k_lo + lane); bw0 = __ldg(p.srcidx + bm0); }
+        if (k_lo + 32 + lane < k_hi) { bm1 = __ldg(sorted + k_lo + 32 + lane); bw1 = __ldg(p.srcidx + bm1); }
+    }
     uint32_t i = (uint32_t)set;
     for (uint32_t g = p.g0 + pair + (uint32_t)set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
         const uint32_t s = i % NS, o = i % NO;
@@ -805,10 +815,15 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 rec_s2g(p, dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
                          (w_hi - w_lo) * 4);
             }
+            uint32_t* bg = bdst + (uint64_t)g * p.nSrc;
+            if constexpr (REGB) {
+                if (k_lo + lane < k_hi) bg[bm0] = Do[bw0];
+                if (k_lo + 32 + lane < k_hi) bg[bm1] = Do[bw1];
+            }
             const uint32_t* sorted = p.srcidx + p.nSrc;
-            for (uint32_t k = k_lo + lane; k < k_hi; k += 32) {
+            for (uint32_t k = k_lo + (REGB ? 64 : 0) + lane; k < k_hi; k += 32) {
                 const uint32_t m = __ldg(sorted + k);
-                bdst[(uint64_t)g * p.nSrc + m] = Do[__ldg(p.srcidx + m)];
+                bg[m] = Do[__ldg(p.srcidx + m)];
             }
             continue;
         }
