@@ -10,8 +10,9 @@ exchange (NCCL send/recv via torch.distributed), so scaling is strong.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Timing: W untimed steps, then K steps bracketed by barrier + synchronize, timed
-with CUDA events on the engine's stream, max over ranks.  The state (6.97 GB) is
-54x the 126 MB L2, so no flush is needed between steps.
+with CUDA events on the engine's stream, max over ranks.  The packed state (0.44 GB
+per buffer, 0.87 GB read + written per step) is 7x the 126 MB L2, so no flush is
+needed between steps.
 
 One JSON line on rank 0 (see DESIGN.md "Measurement" for every field).
 """
@@ -270,20 +271,22 @@ def run_ours(args):
     n0 = C.c_uint64()
     _abi.check(L.nbbgpu_launch_count(h, C.byref(n0)))
     t_wall = time.perf_counter()
-    ev0.record(ext)
     # K steps back to back on the engine stream (packed: halo-words kernel + step
-    # kernel per step; N > 1 adds the halo pack / NCCL send-recv / unpack on-stream)
-    if ws == 1:
-        sim.step(rule, args.steps)
-    elif dsim.transport in ("nccl", "p2p"):
-        sim.step(rule, args.steps)
+    # kernel per step; N > 1 adds the peer push or the NCCL exchange on-stream).
+    # The library records its CUDA events on the engine stream right around the K
+    # launches (nbbgpu_step_timed); torch events around the ctypes call would also
+    # count the host's call/return latency while the stream idles (~3 us/step at K=20)
+    if ws == 1 or dsim.transport in ("nccl", "p2p"):
+        step_ms = sim.step_timed(rule, args.steps)
     else:
+        ev0.record(ext)
         dsim.step(rule, args.steps)
-    ev1.record(ext)
+        ev1.record(ext)
     barrier()
     t_wall = time.perf_counter() - t_wall
     clk = clocks.stop()
-    step_ms = ev0.elapsed_time(ev1)
+    if not (ws == 1 or dsim.transport in ("nccl", "p2p")):
+        step_ms = ev0.elapsed_time(ev1)
     n1 = C.c_uint64()
     _abi.check(L.nbbgpu_launch_count(h, C.byref(n1)))
     launches = n1.value - n0.value
