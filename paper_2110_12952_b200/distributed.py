@@ -372,8 +372,9 @@ class MultiGpuSimulation:
     owns groups [g0, g1) of the packed layout on devices[i]; the peer-memory
     transport is attached in-process (nbbgpu_p2p_attach_local: the peers' boundary
     planes are device pointers over NVLink, each step pushes the words a peer needs
-    and bumps its arrival counter).  step() enqueues every rank's steps (interleaved,
-    so no rank waits on a peer that is not queued yet) and then synchronises; ranks
+    and bumps its arrival counter).  step() enqueues every rank's steps (interleaved in
+    chunks of 16, so no rank waits on a peer that is not queued yet) and then
+    synchronises; ranks
     sharing a device (tests on one GPU) step one at a time instead, since a spinning
     kernel could then starve its peer of SMs.  Same methods as Simulation."""
 
@@ -449,11 +450,18 @@ class MultiGpuSimulation:
             s._front_cache = None  # stepped below through the C ABI directly
         L = _abi.lib()
         args = (rule.birth & 0xFFFF, rule.survive & 0xFFFF, int(rule.neighborhood == Neighborhood.Moore))
-        for _ in range(int(nsteps)):
+        # distinct devices: chunks of 16 steps per rank, interleaved across ranks (a
+        # rank's queue never fills while a peer it waits on is not yet enqueued, and
+        # the host issues one call per 16 steps); shared device: one step at a time
+        chunk = 1 if self.shared_device else 16
+        left = int(nsteps)
+        while left > 0:
+            k = min(chunk, left)
             for s in self.ranks:
-                _abi.check(L.nbbgpu_step_async(s.handle(), *args, 1))
+                _abi.check(L.nbbgpu_step_async(s.handle(), *args, k))
                 if self.shared_device:
                     _abi.check(L.nbbgpu_synchronize(s.handle()))
+            left -= k
         for s in self.ranks:
             _abi.check(L.nbbgpu_synchronize(s.handle()))
 
