@@ -79,6 +79,11 @@ struct PackedStepParams {
     // stream the group records through L2 as evict-first (TMA cache hint), so the
     // small per-step tables (ntab, boundary planes, halo words) stay L2-resident
     int stream_ef;
+    // transposed halo gather (HMODE 5): the boundary plane transposed per 32 slots,
+    // Bt[(g * nHc + k) * 32 + b] bit i = boundary word 32k + i of tile 32g + b, and
+    // per chunk k and direction slot d the mask of chunk k's slots in direction d
+    const uint32_t* bt;
+    const uint32_t* dmask;  // [nHc][8]
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
@@ -298,6 +303,71 @@ __device__ __forceinline__ void halo_task(const PackedStepParams& p, const uint3
     else halo4_task<NC>(p, bsrc, H, wi, lane);
 }
 
+// Boundary plane -> Bt (see PackedStepParams::bt): warp per (group, 32 slots), one
+// coalesced load, a warp transpose, one coalesced store.
+__global__ void bnd_transpose_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
+                                     uint32_t* __restrict__ bt) {
+    const uint32_t lane = threadIdx.x & 31;
+    pdl_wait();     // bsrc comes from the previous step kernel
+    pdl_trigger();  // the halo kernel may launch and run its prologue
+    const uint32_t nHc = (p.nH + 31) / 32;
+    const uint64_t nw = (uint64_t)(p.g1 - p.g0) * nHc;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
+         wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t w32 = (uint32_t)wi, gi = w32 / nHc, k = w32 - gi * nHc, g = p.g0 + gi;
+        const uint32_t j = k * 32 + lane;
+        const uint32_t w = j < p.nH ? __ldg(bsrc + (uint64_t)g * p.nSrc + j) : 0u;
+        bt[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(w, lane);
+    }
+}
+
+// Halo words of group g from Bt: lane = tile b gathers, per chunk k of 32 slots,
+// the chunk's bits of its neighbour tile in every direction present in the chunk
+// (one load each, masked), and one transpose turns lane b's bits into the 32 halo
+// words (no per-source-group passes: the slots of a direction are bits of ONE word
+// of the neighbour tile).
+__device__ __forceinline__ void halo_bt_task(const PackedStepParams& p, uint32_t* H, uint32_t g, uint32_t lane) {
+    const uint32_t t = g * 32 + lane;
+    const bool in = t < p.T;
+    const uint32_t nHc = (p.nH + 31) / 32;
+    uint32_t t2[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) t2[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
+    uint32_t* Hg = H + (uint64_t)g * p.nHp;
+#pragma unroll 1
+    for (uint32_t k = 0; k < nHc; ++k) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            const uint32_t dm = __ldg(p.dmask + k * 8 + d);
+            if (dm && t2[d] != kNoTile)
+                word |= __ldcg(p.bt + ((uint64_t)(t2[d] >> 5) * nHc + k) * 32 + (t2[d] & 31)) & dm;
+        }
+        const uint32_t out = warp_transpose32(word, lane);  // lane i: bit b = slot 32k + i of tile b
+        if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
+    }
+}
+
+// (group, chunk) tasks for few groups: the chunk's directions only, more warps
+__device__ __forceinline__ void halo_bt_chunk_task(const PackedStepParams& p, uint32_t* H, uint32_t g, uint32_t k,
+                                                   uint32_t lane) {
+    const uint32_t t = g * 32 + lane;
+    const bool in = t < p.T;
+    const uint32_t nHc = (p.nH + 31) / 32;
+    uint32_t t2[8], dm[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+        dm[d] = __ldg(p.dmask + k * 8 + d);
+        t2[d] = (dm[d] && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d)
+        if (t2[d] != kNoTile) word |= __ldcg(p.bt + ((uint64_t)(t2[d] >> 5) * nHc + k) * 32 + (t2[d] & 31)) & dm[d];
+    const uint32_t out = warp_transpose32(word, lane);
+    if (k * 32 + lane < p.nH) H[(uint64_t)g * p.nHp + k * 32 + lane] = out;
+}
+
 // HMODE is compile-time so the small-halo variant keeps its 30 registers (full
 // occupancy: this kernel is latency-bound).  0: tasks of SPW slots (small halos),
 // 1: (group, direction) tasks, 2: group tasks (all directions of a group),
@@ -309,12 +379,18 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
     pdl_wait();     // bsrc comes from the previous step kernel
     wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
     pdl_trigger();  // the step kernel may launch and run its prologue
-    const uint64_t nw = HMODE == 2 ? (uint64_t)(p.g1 - p.g0)
+    const uint64_t nw = HMODE == 6 ? (uint64_t)(p.g1 - p.g0) * ((p.nH + 31) / 32)
+                      : HMODE == 2 || HMODE == 5 ? (uint64_t)(p.g1 - p.g0)
                       : HMODE == 1 || HMODE == 3 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
                                    : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        if constexpr (HMODE == 2) {
+        if constexpr (HMODE == 6) {
+            const uint32_t nHc = (p.nH + 31) / 32, w32 = (uint32_t)wi, gi = w32 / nHc;
+            halo_bt_chunk_task(p, H, p.g0 + gi, w32 - gi * nHc, lane);
+        } else if constexpr (HMODE == 5) {
+            halo_bt_task(p, H, p.g0 + (uint32_t)wi, lane);
+        } else if constexpr (HMODE == 2) {
             halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 1 || HMODE == 3) {
             const uint32_t w32 = (uint32_t)wi, gi = w32 / (uint32_t)p.nD;

@@ -443,10 +443,13 @@ def test_packed_in_kernel_halo_warps(monkeypatch, hw):
 
 
 @pytest.mark.parametrize("env", [("NBBGPU_HALO_GROUP", "1"), ("NBBGPU_HALO_GROUP", "0"),
-                                 ("NBBGPU_HALO_NCH3", "1"), ("NBBGPU_HALO_NCH3", "0")])
+                                 ("NBBGPU_HALO_NCH3", "1"), ("NBBGPU_HALO_NCH3", "0"),
+                                 ("NBBGPU_HALO_BT", "1")])
 def test_large_halo_task_modes(monkeypatch, env):
     # the wide-halo gathers (group tasks / direction tasks, 1 or 3 chunks of loads
-    # per round trip) give the same bytes on halo-heavy fractals
+    # per round trip; the transposed boundary plane) give the same bytes on
+    # halo-heavy fractals
+    monkeypatch.setenv("NBBGPU_HALO_BT", "0")
     monkeypatch.setenv(*env)
     H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
     Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
