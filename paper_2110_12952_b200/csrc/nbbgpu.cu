@@ -378,6 +378,8 @@ struct nbbgpu_sim {
     uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
     uint32_t* d_pbt = nullptr;              // transposed boundary plane (wide halos, single GPU)
     uint32_t* d_pdmask = nullptr;           // [nHc][8] direction masks per 32-slot chunk
+    uint32_t* d_phent = nullptr;            // nonzero (chunk, direction) masks, 2 words each
+    uint32_t n_hent = 0;
     unsigned* d_gbar = nullptr;             // grid barrier of the fused multi-step kernel
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
@@ -687,6 +689,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_phalo) cudaFree(h->d_phalo);
     if (h->d_pbt) cudaFree(h->d_pbt);
     if (h->d_pdmask) cudaFree(h->d_pdmask);
+    if (h->d_phent) cudaFree(h->d_phent);
     if (h->d_gbar) cudaFree(h->d_gbar);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
