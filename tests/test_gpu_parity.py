@@ -90,7 +90,7 @@ def test_kernel_selection():
     assert sim.active_kernel() == ("tiled", 6)
     sim2 = Simulation(T, 12, Backend.GpuCompact, SimOptions(kernel="naive"))
     assert sim2.active_kernel() == ("naive", 0)
-    assert Simulation(T, 16, Backend.GpuCompact).active_kernel() == ("packed", 6)
+    assert Simulation(T, 16, Backend.GpuCompact).active_kernel() == ("packed", 8)
     assert Simulation(T, 18, Backend.GpuCompact).active_kernel() == ("packed", 8)
     # the packed state is 1/8 of the reference bytes (+ tables)
     assert Simulation(T, 18, Backend.GpuCompact).peak_bytes() < 3 ** 18 // 3

@@ -30,7 +30,7 @@ def test_plans_build(desc, r, qs):
 
 def test_default_levels():
     assert plan_packed_level(T, 20) == 8
-    assert plan_packed_level(T, 16) == 6
+    assert plan_packed_level(T, 16) == 8
     assert plan_packed_level(CARPET, 9) == 4
     assert plan_packed_level(T, 1) == -1
 
