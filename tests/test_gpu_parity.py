@@ -444,7 +444,7 @@ def test_packed_in_kernel_halo_warps(monkeypatch, hw):
 
 @pytest.mark.parametrize("env", [("NBBGPU_HALO_GROUP", "1"), ("NBBGPU_HALO_GROUP", "0"),
                                  ("NBBGPU_HALO_NCH3", "1"), ("NBBGPU_HALO_NCH3", "0"),
-                                 ("NBBGPU_HALO_BT", "1")])
+                                 ("NBBGPU_HALO_BT", "1"), ("NBBGPU_HALO_LEAN", "1")])
 def test_large_halo_task_modes(monkeypatch, env):
     # the wide-halo gathers (group tasks / direction tasks, 1 or 3 chunks of loads
     # per round trip; the transposed boundary plane) give the same bytes on
@@ -454,7 +454,7 @@ def test_large_halo_task_modes(monkeypatch, env):
     H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
     Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
                                       (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
-    for desc, r in ((CARPET, 5), (H, 5), (Y, 5)):
+    for desc, r in ((CARPET, 5), (H, 5), (Y, 5), (T, 9), (VICSEK, 6)):
         _lockstep_vs_oracle(desc, r, conway_rule(), 31 + r, 0.5, 4, kernel="packed")
         _lockstep_vs_oracle(desc, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 32 + r, 0.5, 3,
                             kernel="packed")
