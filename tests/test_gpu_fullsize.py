@@ -73,3 +73,29 @@ def test_r22_packed_matches_tiled():
         assert p.state_hash() == t.state_hash()
     t.close()
     p.close()
+
+
+@pytest.mark.parametrize("case", ["h11", "c10", "y9"])
+def test_large_configs_kernel_agreement(monkeypatch, case):
+    # BASELINE configs 3 and 5 at full size: the packed micro-block kernel with its
+    # default large-halo path (transposed boundary plane: 4-chunk transposes +
+    # entry-list gather for >= 8192 groups) against the tiled byte-layout kernel
+    from paper_2110_12952_b200.descriptor import FractalDescriptor
+    desc, level = {
+        "h11": (FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)]), 11),
+        "c10": (builtin_descriptor("sierpinski-carpet"), 10),
+        "y9": (FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                              (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)]), 9),
+    }[case]
+    sims = {}
+    for k in ("packed", "tiled"):
+        s = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel=k, memory_cap=1 << 42))
+        s.seed_random(42, 0.5)
+        sims[k] = s
+    for n in (1, 3):
+        for rule in (conway_rule(), StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)):
+            for s in sims.values():
+                s.step(rule, n)
+            assert sims["packed"].state_hash() == sims["tiled"].state_hash(), (case, n)
+    for s in sims.values():
+        s.close()
