@@ -86,6 +86,9 @@ struct PackedStepParams {
     const uint32_t* dmask;  // [nHc][8]
     const uint32_t* hent;   // the nonzero (chunk, direction) masks: [2e] = k << 8 | d, [2e + 1] = mask
     uint32_t nhent;
+    // SPLIT = 2 (candy CTA pairs): the staged row window of half h is record words
+    // [win0[h], win0[h] + win_words)
+    uint32_t win0[2], win_words;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
@@ -691,13 +694,13 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 template <class FT, int P, int WQ, bool CONWAY, int DEG>
 __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t (&toff)[Wiring<FT, P>::NEP],
                                               uint32_t blk, uint32_t* Do, uint32_t vmask, const uint32_t (&KB)[9],
-                                              const uint32_t (&KS)[9]) {
+                                              const uint32_t (&KS)[9], uint32_t own_shift = 0) {
     using W = Wiring<FT, P>;
     constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
     constexpr int BPR = WQ / BW;
     const uint32_t by = blk / BPR, bx = blk - by * BPR;
     const uint32_t base = by * (BH * WQ) + bx * BW;
-    const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + base;
+    const uint32_t* Sw = reinterpret_cast<const uint32_t*>(Sb) + (base - own_shift);  // (row window)
     // row blocks with BW % 4 == 0 (carpet: BW = 8, candy: 12): 16-byte loads and
     // stores -- lanes sit BW words apart, so single-word accesses conflict BW/gcd-way
     // interleaved carpet records (rec_word): cell n of block blk at word
@@ -803,11 +806,16 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
     uint8_t* st = sm + 16 * (NS + NO);
-    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4;
+    // SPLIT = 2: each CTA stages only the rows its blocks read (the row window
+    // p.win0[half] + [0, p.win_words) of the record; the plan rebases the block
+    // tables to it)
+    const uint32_t win_words = SPLIT == 1 ? p.Cp : p.win_words;
+    const uint32_t stage_bytes = p.SW * 4, rec_bytes = win_words * 4;
     // output slice of this CTA: the whole record (SPLIT = 1), or rows [half*ROWS, ...)
     const uint32_t half = blockIdx.x % SPLIT, pair = blockIdx.x / SPLIT, npairs = gridDim.x / SPLIT;
     const uint32_t out_words = SPLIT == 1 ? p.Cp : (uint32_t)(WG::ROWS * WQ);
     const uint32_t out_off = SPLIT == 1 ? 0u : half * out_words;
+    const uint32_t win0 = SPLIT == 1 ? 0u : p.win0[half];  // words
     const uint32_t out_bytes = out_words * 4;
     uint8_t* outs = st + NS * stage_bytes;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -823,7 +831,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
         mbar_fence_init();
     }
-    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
+    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[win_words + p.nHp] = 0u;  // absent
     if (SPLIT == 1)
         for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
             reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * out_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
@@ -842,7 +850,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
                 const uint32_t halo_bytes = HW > 0 ? 0u : p.nHp * 4;
                 mbar_expect_tx(bar, rec_bytes + halo_bytes);
-                rec_g2s(p, dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
+                rec_g2s(p, dst_s, src + (uint64_t)g * p.Cp + win0, rec_bytes, bar);
                 if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
             }
         }
@@ -855,7 +863,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             for (uint32_t g = p.g0 + pair + hw * npairs; g < p.g1; g += HW * npairs, i += HW) {
                 const uint32_t s = i % NS;
                 if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
-                uint32_t* Hs = reinterpret_cast<uint32_t*>(st + s * stage_bytes) + p.Cp;
+                uint32_t* Hs = reinterpret_cast<uint32_t*>(st + s * stage_bytes) + win_words;
                 const uint32_t t = g * 32 + lane;
                 for (uint32_t j0 = 0; j0 < p.nH; j0 += 8) {
                     uint32_t t2[8], sl[8];
@@ -977,7 +985,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         // block_words_r indexes the whole record: shift the slice base back by out_off
         uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * out_bytes) - out_off;
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
-        if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
+        if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS, win0);
         if constexpr (PWS) {
             fence_proxy_async_smem();  // the bulk store reads this slice through the async proxy
             __syncwarp();
