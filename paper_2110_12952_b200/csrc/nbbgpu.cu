@@ -1009,7 +1009,9 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     const uint64_t l0 = h->launches;
     CK(cudaEventRecord(h->ev0, h->stream));
     try {
-        if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm && !h->p2p) {
+        if (rk == NBBGPU_KERNEL_PACKED && launch_resident(h, birth, survive, moore, nsteps)) {
+            // (all steps on-chip in one single-CTA launch)
+        } else if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm && !h->p2p) {
             // every step in one cooperative launch (chunks bound the launch length)
             for (int64_t done = 0; done < nsteps;) {
                 const int n = (int)std::min<int64_t>(nsteps - done, 1 << 20);

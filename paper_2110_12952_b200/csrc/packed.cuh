@@ -1043,6 +1043,82 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
     __syncthreads();
 }
 
+// Small levels whose whole packed state fits one SM's shared memory (triangle q=6,
+// r <= 12): ONE CTA runs all nsteps steps on-chip.  Shared memory holds both state
+// buffers in stage layout (per group: record | halo words | zero word) and, per
+// (group, halo slot, tile), the smem word + bit of its source cell (built once from
+// ntab).  Per step: halo words by ballots over smem, __syncthreads, every
+// micro-block chunk of every group (block_words_r) into the other buffer,
+// __syncthreads.  Global memory is touched only to load the first state and to
+// store the last one (+ its boundary plane).
+template <bool CONWAY, int DEG, class FT, int P, int WQ>
+__global__ void __launch_bounds__(1024, 1)
+step_packed_resident_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                            uint32_t* __restrict__ bdst, int nsteps) {
+    using W = Wiring<FT, P>;
+    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
+    constexpr int NCHUNK = (NBLK + 31) / 32;
+    constexpr int NEP = W::NEP;
+    extern __shared__ __align__(16) uint32_t rsm[];
+    const uint32_t NG = p.NG, SWg = p.SW, nH = p.nH;
+    uint32_t* S0 = rsm;
+    uint32_t* S1 = rsm + NG * SWg;
+    uint32_t* hix = rsm + 2 * NG * SWg;  // [NG][nH][32]: smem word << 5 | bit, or ~0u
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (uint32_t i = tid; i < 2 * NG * SWg; i += blockDim.x) {
+        const uint32_t g = (i / SWg) % NG, w = i % SWg;
+        rsm[i] = (i < NG * SWg && w < p.Cp) ? src[(uint64_t)g * p.Cp + w] : 0u;
+    }
+    for (uint32_t i = tid; i < NG * nH * 32; i += blockDim.x) {
+        const uint32_t l = i & 31, gj = i >> 5, g = gj / nH, j = gj - g * nH;
+        const uint32_t t = g * 32 + l, sl = __ldg(p.slot + j);
+        const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)((sl >> 16) & 0xFFu) * p.T + t)) : kNoTile;
+        hix[i] = t2 == kNoTile ? 0xFFFFFFFFu : (((t2 >> 5) * SWg + __ldg(p.srcidx + j)) << 5) | (t2 & 31);
+    }
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    __syncthreads();
+    for (int step = 0; step < nsteps; ++step) {
+        uint32_t* A = (step & 1) ? S1 : S0;
+        uint32_t* Bn = (step & 1) ? S0 : S1;
+        for (uint32_t task = warp; task < NG * nH; task += nwarps) {  // halo words of A
+            const uint32_t x = hix[task * 32 + lane];
+            const uint32_t bit = x == 0xFFFFFFFFu ? 0u : (A[x >> 5] >> (x & 31)) & 1u;
+            const uint32_t w = __ballot_sync(0xFFFFFFFFu, bit != 0);
+            if (lane == 0) {
+                const uint32_t g = task / nH;
+                A[g * SWg + p.Cp + (task - g * nH)] = w;
+            }
+        }
+        __syncthreads();
+        for (uint32_t item = warp; item < NG * NCHUNK; item += nwarps) {  // micro-blocks A -> Bn
+            const uint32_t g = item / NCHUNK, c = item - g * NCHUNK;
+            const uint32_t blk = c * 32 + lane;
+            if (blk < (uint32_t)NBLK) {
+                uint32_t toff[NEP];
+                const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)blk * (NEP / 4);
+                static_for<NEP / 4>([&](auto e4) {
+                    constexpr int E = decltype(e4)::value;
+                    const uint4 v = __ldg(t4 + E);
+                    toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
+                });
+                const uint32_t vmask = g == NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+                block_words_r<FT, P, WQ, CONWAY, DEG>(reinterpret_cast<const uint8_t*>(A + g * SWg), toff, blk,
+                                                      Bn + g * SWg, vmask, KB, KS);
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t* F = (nsteps & 1) ? S1 : S0;
+    for (uint32_t i = tid; i < NG * p.Cp; i += blockDim.x) dst[i] = F[(i / p.Cp) * SWg + i % p.Cp];
+    for (uint32_t i = tid; i < NG * p.nSrc; i += blockDim.x)
+        bdst[i] = F[(i / p.nSrc) * SWg + __ldg(p.srcidx + i % p.nSrc)];
+}
+
 // All nsteps steps in ONE cooperative launch (persistent, one CTA per SM): per step
 //   phase H: every warp of the grid gathers halo words (halo_task) into H,
 //   grid barrier,

@@ -458,3 +458,24 @@ def test_large_halo_task_modes(monkeypatch, env):
         _lockstep_vs_oracle(desc, r, conway_rule(), 31 + r, 0.5, 4, kernel="packed")
         _lockstep_vs_oracle(desc, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 32 + r, 0.5, 3,
                             kernel="packed")
+
+
+@pytest.mark.parametrize("resident", ["0", "1"])
+def test_packed_resident_small_levels(monkeypatch, resident):
+    # T q=6 with <= 8 groups: every step on-chip in one single-CTA launch (or the
+    # per-step kernels): bytes equal the oracle after each call, any rule
+    monkeypatch.setenv("NBBGPU_RESIDENT", resident)
+    for r in (6, 8, 10, 11):
+        _lockstep_vs_oracle(T, r, conway_rule(), 41 + r, 0.5, 5, kernel="packed")
+        _lockstep_vs_oracle(T, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 42 + r, 0.5, 4,
+                            kernel="packed")
+    o = oracle.Oracle(T.replicas, T.k, T.s, 10)
+    o.seed(9, 0.5)
+    sim = Simulation(T, 10, Backend.GpuCompact, SimOptions(kernel="packed"))
+    sim.seed_random(9, 0.5)
+    for n in (100, 1, 7):  # many steps per launch, odd and even counts
+        sim.step(conway_rule(), n)
+        for _ in range(n):
+            o.step(conway_rule().birth, conway_rule().survive, conway_rule().moore)
+        assert np.array_equal(sim.front().data, o.front)
+    sim.close()
