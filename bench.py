@@ -60,6 +60,25 @@ def ncu_traffic():
         return None, None
 
 
+def gpu_numa_affinity(device: int):
+    """Restrict this process to the CPUs NVML reports as local to the GPU; returns
+    the previous affinity (None when NVML or the call is unavailable)."""
+    try:
+        import pynvml as n
+        n.nvmlInit()
+        hdl = n.nvmlDeviceGetHandleByIndex(device)
+        words = n.nvmlDeviceGetCpuAffinity(hdl, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        old = os.sched_getaffinity(0)
+        cpus &= old
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return old
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled during the timed region, in
     process through NVML (pynvml): no nvidia-smi process is spawned next to the
@@ -318,6 +337,10 @@ def run_ours(args):
     # download the final state into pinned host memory.  All inside the region.
     e2e = None
     if not args.no_e2e:
+        # host buffers and the driving thread on the GPU's own NUMA node (NVML CPU
+        # affinity): pinned pages are placed by first touch, and PCIe DMA to a remote
+        # node's memory is slower and noisier; the previous affinity is restored after
+        old_aff = gpu_numa_affinity(device)
         host_in = torch.empty(cells, dtype=torch.uint8).pin_memory()
         host_out = torch.empty(cells, dtype=torch.uint8).pin_memory()
         _abi.check(L.nbbgpu_download(h, C.c_void_p(host_in.data_ptr()), cells))
@@ -334,6 +357,8 @@ def run_ours(args):
             if rep:
                 reps.append(time.perf_counter() - t0)
         e2e_s = sorted(reps)[len(reps) // 2]
+        if old_aff is not None:
+            os.sched_setaffinity(0, old_aff)
         if dist is not None:
             tt = torch.tensor([e2e_s], dtype=torch.float64,
                               device=f"cuda:{device}" if args.dist_backend == "nccl" else "cpu")
