@@ -478,4 +478,6 @@ def test_packed_resident_small_levels(monkeypatch, resident):
         for _ in range(n):
             o.step(conway_rule().birth, conway_rule().survive, conway_rule().moore)
         assert np.array_equal(sim.front().data, o.front)
+    _, _, launches = sim.step_profiled(conway_rule(), 50)  # one launch for all 50 steps
+    assert launches == (1 if resident == "1" else 50)
     sim.close()
