@@ -1119,6 +1119,106 @@ step_packed_resident_kernel(const PackedStepParams p, const uint32_t* __restrict
         bdst[i] = F[(i / p.nSrc) * SWg + __ldg(p.srcidx + i % p.nSrc)];
 }
 
+// Cluster version for states of up to 8 CTAs x 8 groups (T r=12): CTA c of the
+// cluster owns groups g = c (mod NC) in its shared memory; halo words read the
+// neighbour tiles' source words from the owning CTA's shared memory over the
+// cluster (distributed shared memory, mapa + ld.shared::cluster); one cluster
+// barrier per step.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_dsmem(uint32_t local_saddr, uint32_t rank) {
+    uint32_t ra, v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_saddr), "r"(rank));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <bool CONWAY, int DEG, class FT, int P, int WQ>
+__global__ void __launch_bounds__(1024, 1)
+step_packed_cluster_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                           uint32_t* __restrict__ bdst, int nsteps) {
+    using W = Wiring<FT, P>;
+    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
+    constexpr int NCHUNK = (NBLK + 31) / 32;
+    constexpr int NEP = W::NEP;
+    extern __shared__ __align__(16) uint32_t csm[];
+    const uint32_t NC = gridDim.x, me = cluster_rank();
+    const uint32_t NG = p.NG, SWg = p.SW, nH = p.nH;
+    const uint32_t LG = (NG + NC - 1) / NC;                // local group slots per CTA
+    const uint32_t nmine = me < NG ? (NG - me + NC - 1) / NC : 0u;
+    uint32_t* S0 = csm;
+    uint32_t* S1 = csm + LG * SWg;
+    uint32_t* hix = csm + 2 * LG * SWg;                    // [nmine][nH][32]: rank << 25 | word << 5 | bit
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (uint32_t i = tid; i < 2 * LG * SWg; i += blockDim.x) {
+        const uint32_t lg = (i / SWg) % LG, w = i % SWg, g = lg * NC + me;
+        csm[i] = (i < LG * SWg && g < NG && w < p.Cp) ? src[(uint64_t)g * p.Cp + w] : 0u;
+    }
+    for (uint32_t i = tid; i < nmine * nH * 32; i += blockDim.x) {
+        const uint32_t l = i & 31, gj = i >> 5, lg = gj / nH, j = gj - lg * nH, g = lg * NC + me;
+        const uint32_t t = g * 32 + l, sl = __ldg(p.slot + j);
+        const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)((sl >> 16) & 0xFFu) * p.T + t)) : kNoTile;
+        if (t2 == kNoTile) { hix[i] = 0xFFFFFFFFu; continue; }
+        const uint32_t G2 = t2 >> 5;
+        hix[i] = ((G2 % NC) << 25) | ((((G2 / NC) * SWg) + __ldg(p.srcidx + j)) << 5) | (t2 & 31);
+    }
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    cluster_sync_all();  // every CTA's first state is in place
+    for (int step = 0; step < nsteps; ++step) {
+        uint32_t* A = (step & 1) ? S1 : S0;
+        uint32_t* Bn = (step & 1) ? S0 : S1;
+        const uint32_t Abase = (uint32_t)__cvta_generic_to_shared(A);
+        for (uint32_t task = warp; task < nmine * nH; task += nwarps) {  // halo words of my groups
+            const uint32_t x = hix[task * 32 + lane];
+            uint32_t bit = 0u;
+            if (x != 0xFFFFFFFFu) bit = (ld_dsmem(Abase + ((x >> 5) & 0xFFFFFu) * 4, x >> 25) >> (x & 31)) & 1u;
+            const uint32_t w = __ballot_sync(0xFFFFFFFFu, bit != 0);
+            if (lane == 0) {
+                const uint32_t lg = task / nH;
+                A[lg * SWg + p.Cp + (task - lg * nH)] = w;
+            }
+        }
+        __syncthreads();
+        for (uint32_t item = warp; item < nmine * NCHUNK; item += nwarps) {
+            const uint32_t lg = item / NCHUNK, c = item - lg * NCHUNK, g = lg * NC + me;
+            const uint32_t blk = c * 32 + lane;
+            if (blk < (uint32_t)NBLK) {
+                uint32_t toff[NEP];
+                const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)blk * (NEP / 4);
+                static_for<NEP / 4>([&](auto e4) {
+                    constexpr int E = decltype(e4)::value;
+                    const uint4 v = __ldg(t4 + E);
+                    toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
+                });
+                const uint32_t vmask = g == NG - 1 ? p.lastmask : 0xFFFFFFFFu;
+                block_words_r<FT, P, WQ, CONWAY, DEG>(reinterpret_cast<const uint8_t*>(A + lg * SWg), toff, blk,
+                                                      Bn + lg * SWg, vmask, KB, KS);
+            }
+        }
+        cluster_sync_all();  // Bn complete everywhere; nobody still reads A
+    }
+    const uint32_t* F = (nsteps & 1) ? S1 : S0;
+    for (uint32_t i = tid; i < nmine * p.Cp; i += blockDim.x) {
+        const uint32_t lg = i / p.Cp, w = i - lg * p.Cp;
+        dst[(uint64_t)(lg * NC + me) * p.Cp + w] = F[lg * SWg + w];
+    }
+    for (uint32_t i = tid; i < nmine * p.nSrc; i += blockDim.x) {
+        const uint32_t lg = i / p.nSrc, m = i - lg * p.nSrc;
+        bdst[(uint64_t)(lg * NC + me) * p.nSrc + m] = F[lg * SWg + __ldg(p.srcidx + m)];
+    }
+}
+
 // All nsteps steps in ONE cooperative launch (persistent, one CTA per SM): per step
 //   phase H: every warp of the grid gathers halo words (halo_task) into H,
 //   grid barrier,
