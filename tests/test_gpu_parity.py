@@ -465,7 +465,7 @@ def test_packed_resident_small_levels(monkeypatch, resident):
     # T q=6 with <= 8 groups: every step on-chip in one single-CTA launch (or the
     # per-step kernels): bytes equal the oracle after each call, any rule
     monkeypatch.setenv("NBBGPU_RESIDENT", resident)
-    for r in (6, 8, 10, 11, 12):  # r=12: 23 groups on a cluster of 8 CTAs (DSMEM halos)
+    for r in (6, 8, 10, 11, 12, 13):  # r=12 / 13: 23 / 69 groups on clusters of 8 / 16 CTAs
         _lockstep_vs_oracle(T, r, conway_rule(), 41 + r, 0.5, 5, kernel="packed")
         _lockstep_vs_oracle(T, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 42 + r, 0.5, 4,
                             kernel="packed")
