@@ -229,7 +229,6 @@ def run_ours(args):
     from paper_2110_12952_b200 import (Backend, SimOptions, Simulation, builtin_descriptor,
                                        conway_rule, _abi)
     ws, rank, local = dist_env()
-    n = args.gpus if ws == 1 else ws
     dist = None
     device = (local if ws > 1 else 0) if args.device is None else args.device
     if ws > 1:
@@ -261,8 +260,13 @@ def run_ours(args):
         else:
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="torch", host_staging=True)
         owned = dsim.owned_cells()
+        devs = [None] * ws
+        dist.all_gather_object(devs, torch.cuda.get_device_properties(device).uuid.hex
+                               if hasattr(torch.cuda.get_device_properties(device), "uuid") else str(device))
+        n = len(set(devs))  # GPUs that actually stepped (ranks sharing a device count once)
     else:
         owned = cells
+        n = 1
 
     def exchange():
         if dsim is not None:
@@ -394,8 +398,9 @@ def run_ours(args):
         "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore "
                                "(BASELINE.json configs[3]; north-star target)",
                    "level": args.level, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
-                   "parallelism": (f"partitioned x{n}, halo transport {dsim.transport}" if dsim is not None
-                                   else "single GPU"),
+                   "parallelism": (f"partitioned x{ws} over {n} GPU(s), halo transport {dsim.transport}"
+                                   if dsim is not None else "single GPU"),
+                   "partitions": ws,
                    "state_bytes_per_buffer": (cells + 7) // 8 if packed else cells,
                    "l2": (f"state {((cells + 7) // 8 if packed else cells) / 1e9:.2f} GB per buffer vs 126 MB L2: "
                           "inputs larger than L2, no flush")},
@@ -450,7 +455,31 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    ws, _, _ = dist_env()
+    if ws == 1 and args.gpus > 1:
+        return relaunch_distributed(args)
     return run_ours(args)
+
+
+def relaunch_distributed(args):
+    """`python bench.py --gpus N` without torchrun: re-run this script as N ranks
+    (one process per GPU) exactly as the driver launches it, so the line always
+    measures N devices.  Refuses (exit 2, no line claiming N GPUs) when fewer than N
+    devices are visible, unless --device pins every rank to one device (test knob:
+    N partitions emulated on one GPU, reported as n_gpus 1, partitions N)."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if args.device is None and have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                                                     f"found {have}", "n_gpus": have}), flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 if __name__ == "__main__":

@@ -60,8 +60,12 @@ enum { NBBGPU_MODE_COMPACT = 0, NBBGPU_MODE_BB = 1, NBBGPU_MODE_LAMBDA = 2, NBBG
  * layout on the device; PACKED keeps it bit-sliced (1 bit per cell, groups of 32
  * level-q tiles, csrc/packed.cuh) and converts to / from the reference bytes on
  * download / upload.  Switching between the two families converts the state on
- * the device.  Results are identical for every kernel. */
-enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2, NBBGPU_KERNEL_PACKED = 3 };
+ * the device.  TABLE is SimOptions::neighbor_table (stencil.cpp:340-352, 401-414):
+ * the byte layout stepped through a per-slot neighbour table built on the device
+ * on the first step of a neighbourhood (deg x k^r slots, 32-bit below 2^32 cells).
+ * Results are identical for every kernel. */
+enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2, NBBGPU_KERNEL_PACKED = 3,
+       NBBGPU_KERNEL_TABLE = 4 };
 
 /* lambda / nu map variants: CUDA-core digit loop, or the paper's matrix form on
  * the tensor cores (exact integer MMA, u8 x u8 -> s32). */

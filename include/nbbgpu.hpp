@@ -93,6 +93,10 @@ public:
         check(nbbgpu_download(h_, buf.data(), n));
         return buf;
     }
+    // front().data() into a caller buffer of n = stored cells bytes (host or device)
+    void download(std::uint8_t* dst, std::uint64_t n) const { check(nbbgpu_download(h_, dst, n)); }
+    // NBBGPU_KERNEL_* (SimOptions::neighbor_table -> NBBGPU_KERNEL_TABLE)
+    void set_kernel(int kernel) { check(nbbgpu_set_kernel(h_, kernel)); }
     nbbgpu_t handle() const { return h_; }
 
 private:

@@ -96,6 +96,48 @@ __global__ void step_compact_naive_kernel(Frac f, const uint8_t* __restrict__ sr
     }
 }
 
+// Simulation::build_neighbor_table (stencil.cpp:401-414) on the device: per
+// compact slot and offset j the neighbour's slot, or kNoSlot (outside the box or
+// a hole).  The reference stores [i * deg + j] int64; here the table is laid out
+// offset-major, tab[j * n + i], so the step kernel's table reads coalesce, with
+// 32-bit slots while k^r < 2^32 (64-bit above).
+template <int K, int S, class IDX>
+__global__ void build_nbr_table_kernel(Frac f, uint64_t n, int deg, IDX* __restrict__ tab) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t ex, ey;
+        lambda_map<K, S>(f, (uint32_t)(i % f.w), (uint32_t)(i / f.w), ex, ey);
+        for (int j = 0; j < deg; ++j) {
+            const int nx = (int)ex + kOffX[j], ny = (int)ey + kOffY[j];
+            IDX slot = (IDX)~(IDX)0;
+            uint32_t cx, cy;
+            if (nx >= 0 && ny >= 0 && nx < (int)f.side && ny < (int)f.side &&
+                nu_map<K, S>(f, (uint32_t)nx, (uint32_t)ny, cx, cy))
+                slot = (IDX)((uint64_t)cy * f.w + cx);
+            tab[(uint64_t)j * n + i] = slot;
+        }
+    }
+}
+
+// Simulation::step_compact_linear with the neighbour table (stencil.cpp:340-352):
+// deg table reads + deg byte gathers per cell, no maps.
+template <class IDX, int DEG>
+__global__ void step_table_kernel(const IDX* __restrict__ tab, uint64_t n, const uint8_t* __restrict__ src,
+                                  uint8_t* __restrict__ dst, uint64_t i0, uint64_t i1, uint32_t birth,
+                                  uint32_t survive) {
+    for (uint64_t i = i0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < i1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        IDX slot[DEG];
+#pragma unroll
+        for (int j = 0; j < DEG; ++j) slot[j] = __ldcs(tab + (uint64_t)j * n + i);  // streamed once per step
+        uint32_t count = 0;
+#pragma unroll
+        for (int j = 0; j < DEG; ++j)
+            if (slot[j] != (IDX)~(IDX)0) count += src[slot[j]];
+        dst[i] = apply_rule(birth, survive, src[i], count);
+    }
+}
+
 // Simulation::step_bounding_box (stencil.cpp:291-311), one thread per embedded
 // cell: holes are skipped (never written), neighbours read straight from the box.
 template <int K, int S>

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <exception>
 #include <map>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -387,6 +389,10 @@ struct nbbgpu_sim {
     std::vector<cudaEvent_t>* prof = nullptr;  // pre-created pool
     size_t prof_idx = 0;
     uint64_t launches = 0;
+    // NBBGPU_KERNEL_TABLE: neighbour table tab[j * cells + i] (u32 or u64 slots)
+    void* d_tab = nullptr;
+    int tab_deg = 0;
+    int cluster_fit[2] = {-1, -1};          // 8- / 16-CTA resident clusters fit (-1: not queried)
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -466,6 +472,7 @@ bool is_device_ptr(const void* p);
 int resolve_kernel_for(nbbgpu_t h, int kernel) {
     if (h->mode != NBBGPU_MODE_COMPACT) return NBBGPU_KERNEL_NAIVE;  // bb, lambda, blocked
     if (kernel == NBBGPU_KERNEL_NAIVE) return NBBGPU_KERNEL_NAIVE;
+    if (kernel == NBBGPU_KERNEL_TABLE) return NBBGPU_KERNEL_TABLE;
     if (kernel == NBBGPU_KERNEL_PACKED) {
         if (h->pq < 2) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
         return NBBGPU_KERNEL_PACKED;
@@ -485,17 +492,29 @@ void prof_mark(nbbgpu_t h) {
 }
 int layout_of_kernel(int k) { return k == NBBGPU_KERNEL_PACKED ? 1 : 0; }
 
+// Kernel attributes (opt-in shared memory, non-portable clusters) are per device:
+// set them once per (kernel, device) pair.  Thread-safe; several handles on
+// several devices share the registry.
+bool attr_needed(const void* fn, int device) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> g(mu);
+    return done.insert({fn, device}).second;
+}
+template <class K>
+void smem_attr(nbbgpu_t h, K kern, int bytes, bool nonportable_cluster = false) {
+    if (!attr_needed((const void*)kern, h->device)) return;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    if (nonportable_cluster) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
 #include "packed_host.inc"
 
 template <int WQ, int K, int S, bool CONWAY>
 void launch_tiled_t(nbbgpu_t h, const TiledParams& p, const uint8_t* src, uint8_t* dst) {
     auto kern = step_tiled_kernel<WQ, K, S, CONWAY>;
     const size_t smem = (size_t)p.smem_per_warp * kTiledWarps;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
-    }
+    smem_attr(h, kern, 200 * 1024);
     const uint64_t groups = (uint64_t)(p.row1 - p.row0) * p.gpr;
     constexpr int G = (32 / WQ) > 0 ? 32 / WQ : 1;
     const uint64_t warps = (groups + G - 1) / G;
@@ -538,6 +557,41 @@ void owned_range(nbbgpu_t h, uint64_t& lo, uint64_t& hi) {
     }
     lo = (uint64_t)h->prow0 * h->unit_rows * h->hf.w;
     hi = (uint64_t)h->prow1 * h->unit_rows * h->hf.w;
+}
+
+// Simulation::build_neighbor_table (stencil.cpp:401-414): (re)built when the
+// neighbourhood's degree changes, like the reference's table_degree_ check
+// (stencil.cpp:276-280).  Not covered by the memory cap (the reference's table is
+// not either); device OOM -> CapacityError.
+void ensure_nbr_table(nbbgpu_t h, int deg) {
+    if (h->d_tab && h->tab_deg == deg) return;
+    const bool wide = h->cells > 0xFFFFFFFFull;
+    const uint64_t bytes = h->cells * (uint64_t)deg * (wide ? 8 : 4);
+    if (h->d_tab) {
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(h->d_tab);
+        h->bytes_held -= h->cells * (uint64_t)h->tab_deg * (wide ? 8 : 4);
+        h->d_tab = nullptr;
+        h->tab_deg = 0;
+    }
+    if (cudaMalloc(&h->d_tab, std::max<uint64_t>(bytes, 8)) != cudaSuccess) {
+        cudaGetLastError();
+        h->d_tab = nullptr;
+        raise(NBBGPU_ERR_CAPACITY, "neighbor table of " + std::to_string(bytes) +
+                                       " bytes exceeds the device memory (memory cap)");
+    }
+    h->bytes_held += bytes;
+    if (wide) {
+#define NBB_CALL(K, S, ...) build_nbr_table_kernel<K, S, uint64_t><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->frac, h->cells, deg, (uint64_t*)h->d_tab)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+    } else {
+#define NBB_CALL(K, S, ...) build_nbr_table_kernel<K, S, uint32_t><<<grid_for(h->cells, 256), 256, 0, h->stream>>>(h->frac, h->cells, deg, (uint32_t*)h->d_tab)
+        NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+    }
+    CK(cudaGetLastError());
+    h->tab_deg = deg;
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
@@ -610,6 +664,18 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     ++h->launches;  // one kernel per step on the byte layouts
     prof_mark(h);
     struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
+    if (kern == NBBGPU_KERNEL_TABLE) {
+        uint64_t lo, hi;
+        owned_range(h, lo, hi);
+        ensure_nbr_table(h, deg);
+        const bool wide = h->cells > 0xFFFFFFFFull;
+        const int blocks = grid_for(hi - lo, 256);
+        if (wide && deg == 8) step_table_kernel<uint64_t, 8><<<blocks, 256, 0, h->stream>>>((const uint64_t*)h->d_tab, h->cells, src, dst, lo, hi, birth, survive);
+        else if (wide) step_table_kernel<uint64_t, 4><<<blocks, 256, 0, h->stream>>>((const uint64_t*)h->d_tab, h->cells, src, dst, lo, hi, birth, survive);
+        else if (deg == 8) step_table_kernel<uint32_t, 8><<<blocks, 256, 0, h->stream>>>((const uint32_t*)h->d_tab, h->cells, src, dst, lo, hi, birth, survive);
+        else step_table_kernel<uint32_t, 4><<<blocks, 256, 0, h->stream>>>((const uint32_t*)h->d_tab, h->cells, src, dst, lo, hi, birth, survive);
+        return;
+    }
     if (kern == NBBGPU_KERNEL_NAIVE) {
         uint64_t lo, hi;
         owned_range(h, lo, hi);
@@ -692,6 +758,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_phent) cudaFree(h->d_phent);
     if (h->d_gbar) cudaFree(h->d_gbar);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
+    if (h->d_tab) cudaFree(h->d_tab);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
     for (auto* p : h->d_recvs) if (p) cudaFree(p);
@@ -811,6 +878,7 @@ void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, i
     CK(cudaEventRecord(h->ev1, h->stream));
     if (!dout) CK(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDefault, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    check_peer_error(h);
     if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
     if (!din) cudaFree(dI);
     if (!dout) cudaFree(dO);
@@ -1043,6 +1111,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
         return;
     }
     CK(cudaStreamSynchronize(h->stream));
+    check_peer_error(h);
     if (ms) CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
     if (main_ms) {
         float acc = 0.f;
@@ -1084,6 +1153,7 @@ int nbbgpu_synchronize(nbbgpu_t h) {
     return guarded([&] {
         check_handle(h);
         CK(cudaStreamSynchronize(h->stream));
+        check_peer_error(h);
     });
 }
 
@@ -1307,7 +1377,9 @@ int nbbgpu_peak_bytes(nbbgpu_t h, uint64_t* out) {
 int nbbgpu_set_kernel(nbbgpu_t h, int kernel) {
     return guarded([&] {
         if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
-        if (kernel < NBBGPU_KERNEL_AUTO || kernel > NBBGPU_KERNEL_PACKED) raise(NBBGPU_ERR_INVALID, "unknown kernel");
+        if (kernel < NBBGPU_KERNEL_AUTO || kernel > NBBGPU_KERNEL_TABLE) raise(NBBGPU_ERR_INVALID, "unknown kernel");
+        if (kernel == NBBGPU_KERNEL_TABLE && h->mode != NBBGPU_MODE_COMPACT)
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "the neighbor table applies to the linear compact backend only");
         if (kernel == NBBGPU_KERNEL_TILED && (h->mode != NBBGPU_MODE_COMPACT || h->q == 0))
             raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no tile level for this fractal/level");
         if (kernel == NBBGPU_KERNEL_PACKED && (h->mode != NBBGPU_MODE_COMPACT || h->pq < 2))

@@ -58,6 +58,9 @@ struct PackedGeom {
     uint64_t w;              // compact row stride (bytes of the reference layout)
 };
 
+// word of the 256-byte arrival-counter allocation that holds the peer-wait error flag
+constexpr uint32_t kPeerErrWord = 16;
+
 struct PackedStepParams {
     uint32_t C, Cp, SW;      // local cells, words per group record, words per smem stage
     uint32_t nH, nHp, nSrc;  // halo slots (padded to 4), boundary sources
@@ -76,6 +79,10 @@ struct PackedStepParams {
     // pushed this step's boundary words (system-scope arrival counter >= target)
     const uint32_t* wait_cnt;
     uint32_t wait_target;
+    // bounded wait: after wait_ns nanoseconds the waiter sets *wait_err, stops
+    // waiting (this and every later step) and the host raises on synchronize
+    uint32_t* wait_err;
+    uint64_t wait_ns;
     // stream the group records through L2 as evict-first (TMA cache hint), so the
     // small per-step tables (ntab, boundary planes, halo words) stay L2-resident
     int stream_ef;
@@ -97,15 +104,26 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
     return v;
 }
 
-// one thread per CTA spins on the arrival counter (bounded: a lost peer traps the
-// kernel after ~2 s instead of hanging the device), then the CTA proceeds
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// one thread per CTA spins on the arrival counter, then the CTA proceeds.  The
+// wait is bounded by wall time (NBBGPU_PEER_TIMEOUT_S, default 600 s): host-side
+// skew between ranks (seeding, checkpoints, GC) never kills the context; a peer
+// that is really gone sets the handle's error word instead of trapping.
 __device__ __forceinline__ void wait_peers(const PackedStepParams& p) {
     if (!p.wait_cnt) return;
-    if (threadIdx.x == 0) {
-        const long long t0 = clock64();
+    if (threadIdx.x == 0 && *(volatile uint32_t*)p.wait_err == 0) {
+        const uint64_t t0 = globaltimer_ns();
         while ((int32_t)(ld_acquire_sys(p.wait_cnt) - p.wait_target) < 0) {
-            __nanosleep(64);
-            if (clock64() - t0 > 4000000000LL) __trap();
+            __nanosleep(256);
+            if (globaltimer_ns() - t0 > p.wait_ns) {  // a peer stopped stepping: flag, do not trap
+                atomicExch(p.wait_err, 1u);
+                break;
+            }
         }
     }
     __syncthreads();

@@ -22,7 +22,7 @@ from .stencil import Backend, Neighborhood, StencilRule
 
 DEFAULT_MEMORY_CAP = 2 << 30  # kDefaultMemoryCap, proj/include/nbb/grid.hpp:13
 
-KERNELS = {"auto": 0, "naive": 1, "tiled": 2, "packed": 3}
+KERNELS = {"auto": 0, "naive": 1, "tiled": 2, "packed": 3, "table": 4}
 MAP_VARIANTS = {"digit": 0, "mma": 1}
 
 
@@ -74,8 +74,8 @@ class Simulation:
         if backend not in (Backend.GpuCompact, Backend.GpuBoundingBox, Backend.GpuLambda):
             raise OutOfDomain(f"backend '{backend.value}' is a CPU backend of the reference; "
                               "this engine provides gpu-compact, gpu-bb and gpu-lambda")
-        # option validation, stencil.cpp:128-135 (the neighbour table is accepted for the
-        # linear compact backend: the GPU kernels' tile tables play its role)
+        # option validation, stencil.cpp:128-135; neighbor_table selects the GPU
+        # neighbour-table kernel (stencil.cpp:340-352, 401-414)
         if options.block_size > 0 and backend != Backend.GpuCompact:
             raise OutOfDomain("block size applies to the compact backend only")
         if options.neighbor_table and (backend != Backend.GpuCompact or options.block_size > 0):
@@ -99,8 +99,11 @@ class Simulation:
         w, hh, side = C.c_int64(), C.c_int64(), C.c_int64()
         _abi.check(L.nbbgpu_dims(h, C.byref(w), C.byref(hh), C.byref(side)))
         self._w, self._hgt, self._side = w.value, hh.value, side.value
-        if options.kernel != "auto":
-            _abi.check(L.nbbgpu_set_kernel(h, KERNELS[options.kernel]))
+        kernel = options.kernel
+        if options.neighbor_table and kernel == "auto":
+            kernel = "table"
+        if kernel != "auto":
+            _abi.check(L.nbbgpu_set_kernel(h, KERNELS[kernel]))
         if options.map_variant != "digit":
             _abi.check(L.nbbgpu_set_map_variant(h, MAP_VARIANTS[options.map_variant]))
         self._front_cache: Optional[HostGrid] = None
@@ -154,7 +157,7 @@ class Simulation:
     def active_kernel(self) -> Tuple[str, int]:
         k, q = C.c_int(), C.c_int()
         _abi.check(_abi.lib().nbbgpu_active_kernel(self._h, C.byref(k), C.byref(q)))
-        return {1: "naive", 2: "tiled", 3: "packed"}[k.value], q.value
+        return {1: "naive", 2: "tiled", 3: "packed", 4: "table"}[k.value], q.value
 
     def handle(self):
         return self._h

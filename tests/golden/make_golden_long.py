@@ -44,7 +44,7 @@ def run(desc, level, checkpoints, table=False, parallel_seed=False):
 
 
 def main():
-    which = sys.argv[1:] or ["t16", "c9", "t18", "h10", "y8", "t20"]
+    which = sys.argv[1:] or ["t16", "c9", "t18", "h10", "y8", "h11", "y9", "t20"]
     path = os.path.join(HERE, "golden_long.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     T = builtin_descriptor("sierpinski-triangle")
@@ -53,11 +53,13 @@ def main():
     Y = load_descriptor("@" + os.path.join(ROOT, "descriptors/candy.desc"))
     jobs = {
         "t16": lambda: run(T, 16, [0, 1, 3, 10, 100, 500, 1000], table=True),
-        "c9": lambda: run(Cd, 9, [0, 1, 2, 10], table=True),
-        "t18": lambda: run(T, 18, [0, 1], parallel_seed=True),
+        "c9": lambda: run(Cd, 9, [0, 1, 2, 10, 100, 500], table=True),
+        "t18": lambda: run(T, 18, [0, 1, 2, 3, 5, 10], parallel_seed=True),
         "h10": lambda: run(H, 10, [0, 1], parallel_seed=True),
         "y8": lambda: run(Y, 8, [0, 1], parallel_seed=True),
-        "t20": lambda: run(T, 20, [0, 1], parallel_seed=True),
+        "h11": lambda: run(H, 11, [0, 1, 2], parallel_seed=True),
+        "y9": lambda: run(Y, 9, [0, 1, 2], parallel_seed=True),
+        "t20": lambda: run(T, 20, [0, 1, 2, 3, 5, 10], parallel_seed=True),
     }
     for key in which:
         t0 = time.time()

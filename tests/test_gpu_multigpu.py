@@ -62,3 +62,39 @@ def test_multigpu_cells_and_upload():
     assert multi.state_hash() == one.state_hash()
     one.close()
     multi.close()
+
+
+def _ngpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs two distinct GPUs")
+def test_multigpu_distinct_devices():
+    # kernel attributes (opt-in shared memory, 16-CTA clusters) are per device: the
+    # second device's ws3 / pack kernels must launch too
+    n = min(_ngpus(), 4)
+    one = Simulation(T, 16, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+    multi = Simulation(T, 16, Backend.GpuCompact, SimOptions(gpus=n, memory_cap=1 << 40))
+    one.seed_random(42, 0.5)
+    multi.seed_random(42, 0.5)
+    one.step(conway_rule(), 5)
+    multi.step(conway_rule(), 5)
+    assert multi.state_hash() == one.state_hash()
+    one.close()
+    multi.close()
+
+
+def test_second_handle_on_same_device_after_first():
+    # a fresh handle (new tables, same kernels) still launches: attributes are keyed
+    # per (kernel, device), not per process
+    for level in (12, 16):
+        a = Simulation(T, level, Backend.GpuCompact, SimOptions(kernel="packed"))
+        a.seed_random(1, 0.5)
+        a.step(conway_rule(), 3)
+        b = Simulation(T, level, Backend.GpuCompact, SimOptions(kernel="packed"))
+        b.seed_random(1, 0.5)
+        b.step(conway_rule(), 3)
+        assert a.state_hash() == b.state_hash()
+        a.close()
+        b.close()

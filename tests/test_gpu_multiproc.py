@@ -34,7 +34,9 @@ def test_multirank_bench_matches_single(nproc):  # torch.distributed point-to-po
     single = _bench(1, 14, 0)
     multi = _bench(nproc, 14, 29517 + nproc)
     assert multi["final_state_hash"] == single["final_state_hash"]
-    assert multi["n_gpus"] == nproc and "packed" in multi["config"]["kernel"]
+    # ranks sharing cuda:0: one GPU stepped, nproc partitions
+    assert multi["n_gpus"] == 1 and multi["config"]["partitions"] == nproc
+    assert "packed" in multi["config"]["kernel"]
 
 
 @pytest.mark.parametrize("nproc", [2, 3])
@@ -53,6 +55,28 @@ def test_multirank_auto_transport_picks_p2p():
     out = _bench(2, 12, 29817, transport="auto")
     assert "halo transport p2p" in out["config"]["parallelism"]
     assert out["final_state_hash"] == _bench(1, 12, 0)["final_state_hash"]
+
+
+def test_bench_gpus_without_torchrun_relaunches():
+    # `bench.py --gpus 2` (no torchrun): re-launched as 2 ranks; pinned to one device
+    # here, so the line reports 2 partitions on 1 GPU -- never n_gpus 2
+    cmd = [sys.executable, "bench.py", "--level", "14", "--steps", "4", "--warmup", "3", "--no-e2e",
+           "--no-cpu-baseline", "--gpus", "2", "--dist-backend", "gloo", "--transport", "p2p", "--device", "0"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["config"]["partitions"] == 2
+    assert line["final_state_hash"] == _bench(1, 14, 0)["final_state_hash"]
+
+
+def test_bench_gpus_refuses_without_devices():
+    import torch
+    n = torch.cuda.device_count() + 1
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--steps", "3"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert "error" in line and line["n_gpus"] == n - 1
 
 
 def test_multirank_p2p_in_kernel_halo_r18():
