@@ -151,6 +151,16 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
+def _device_uuid(device):
+    """Physical identity of a CUDA device (ranks sharing one GPU count once)."""
+    import torch
+    props = torch.cuda.get_device_properties(device)
+    uuid = getattr(props, "uuid", None)
+    if uuid is None:
+        return str(device)
+    return bytes(uuid.bytes).hex() if hasattr(uuid, "bytes") else str(uuid)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -261,8 +271,7 @@ def run_ours(args):
             dsim = DistributedSimulation(sim, dist, rank, ws, transport="torch", host_staging=True)
         owned = dsim.owned_cells()
         devs = [None] * ws
-        dist.all_gather_object(devs, torch.cuda.get_device_properties(device).uuid.hex
-                               if hasattr(torch.cuda.get_device_properties(device), "uuid") else str(device))
+        dist.all_gather_object(devs, _device_uuid(device))
         n = len(set(devs))  # GPUs that actually stepped (ranks sharing a device count once)
     else:
         owned = cells
