@@ -1,43 +1,50 @@
-// bb.cuh -- vectorised bounding-box baseline (north-star item 3).
+// bb.cuh -- the bounding-box GPU baseline (north-star item 3), any growth factor s.
 //
-// Simulation::step_bounding_box (stencil.cpp:291-311) as a competent dense GPU
-// stencil: each thread owns 16 consecutive bytes of a row of the embedded n x n
-// box (n % 16 == 0, i.e. s = 2 or 4), loads the three rows with 16-B vector
-// loads, gets the edge bytes from the neighbouring lanes by shuffles, sums the 8
-// (or 4) neighbour bytes with SWAR adds (counts <= 8 fit a byte), applies the rule
-// with SWAR byte compares / PRMT table lookups, masks holes to 0 (holes are 0 in
-// both buffers, so writing 0 equals "never updated") and stores 16 B.
-// Membership: low 4 bits of x, y through a 16x16-bit table (per y mod 16), the
-// high digits by a scalar digit check per 16-cell vector (x & y == 0 fast path
-// for the triangle).
+// Simulation::step_bounding_box (stencil.cpp:291-311) over the reference's embedded
+// layout (n x n bytes, row-major, holes 0) as a dense row-streaming stencil:
+//
+// * Chunks.  The buffer is cut into 16-byte aligned chunks.  "Aligned row" y is the
+//   chunk range [floor16(y n), floor16((y+1) n)) (the last row runs to ceil16(n^2),
+//   into the 64 B allocation pad), so rows of any width n tile the buffer and
+//   every chunk holds at most one row boundary.  A linear byte i has the
+//   neighbours i +- 1, i +- n, i +- n +- 1 whatever the row alignment; only the
+//   column edges (x = 0 / x = n - 1) need masks, and out-of-buffer bytes read 0.
+// * CTA = one strip of cps chunks of every aligned row of a band of R rows.  It
+//   streams the band top to bottom through an NS-slot shared-memory ring of row
+//   segments (cps + 4 chunks: 32 B margins either side) with cp.async (zero-fill
+//   outside the buffer), so every byte crosses HBM -> SM once per step; one
+//   __syncthreads per row.  Thread t computes chunk t of the row: the middle
+//   16 bytes of each of the 3 rows by LDS.128 (the rows above / below are
+//   shifted by the warp-uniform delta = floor16(y n) -+ n - floor16((y -+ 1) n)),
+//   the edge bytes from the neighbouring lanes by shuffles, SWAR neighbour
+//   counts (bytes <= 8), the rule by SWAR compares / PRMT tables, a 16-bit hole
+//   mask, one 16-byte store.
+// * Membership (cell_in_fractal, maps.cpp:80-107) = the low m levels (S = s^m >= 32
+//   columns) from a doubled bit table in shared memory AND the top r - m levels
+//   from a coarse bitmap ((n / S)^2 bits, L2-resident).
+// * Holes are 0 in both buffers and never change, so a warp whose 512 bytes of a
+//   row are all holes (one coarse-bitmap test) neither loads (its ring slots are
+//   zeroed in shared memory) nor computes nor stores them: the baseline touches
+//   the box only where the fractal is (the reference skips holes the same way,
+//   stencil.cpp:300-301).
 #pragma once
 
 #include "common.cuh"
 
 namespace nbbgpu {
 
-struct BBParams {
-    Frac f;
-    uint32_t n;          // side
-    int mlow;            // levels covered by the low 4 bits (s=2: 4, s=4: 2)
-    int triangle;        // fast path: member <=> (x & y) == 0
-    uint16_t low[16];    // low[y & 15] bit i: low-level membership of (x0 + i, y)
+struct BBRowParams {
+    uint64_t n;         // side s^r (>= 32)
+    uint64_t alloc;     // bytes readable at the buffer (n^2 + pad)
+    uint64_t magicS;    // floor(2^64 / S) + 1: x / S = umulhi(x, magicS) for x < 2^32
+    uint32_t S;         // low-table side s^m
+    uint32_t CW;        // coarse side n / S
+    uint32_t lt_words;  // words per doubled low-table row
+    uint32_t cps;       // chunks per strip (= threads per CTA, multiple of 32)
+    uint32_t rows;      // rows per CTA (band height)
     uint32_t birth, survive;
     int moore;
 };
-
-// high-level membership of the 16-aligned vector starting at (x0, y)
-__device__ __forceinline__ bool bb_high_member(const BBParams& p, uint32_t x0, uint32_t y) {
-    if (p.triangle) return ((x0 & y) & ~15u) == 0;
-    const uint32_t s = p.f.s;
-    uint32_t x = x0 >> 4, yy = y >> 4;  // 16 = s^mlow
-    for (int mu = p.mlow; mu < p.f.r; ++mu) {
-        if (p.f.id_of_subbox[(yy % s) * s + (x % s)] < 0) return false;
-        x /= s;
-        yy /= s;
-    }
-    return true;
-}
 
 // 4 bits -> 4 bytes of 0/1
 __device__ __forceinline__ uint32_t bb_spread4(uint32_t nib) { return ((nib & 0xFu) * 0x00204081u) & 0x01010101u; }
@@ -66,12 +73,131 @@ __device__ __forceinline__ uint32_t bb_rule(uint32_t cnt, uint32_t alive, uint32
     }
 }
 
-template <bool CONWAY>
-__global__ void __launch_bounds__(256) step_bb_vec_kernel(const BBParams p, const uint8_t* __restrict__ src,
-                                                          uint8_t* __restrict__ dst) {
-    const uint32_t n = p.n, vpr = n >> 4;  // vectors per row
-    const uint64_t total = (uint64_t)n * vpr;
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ bool bb_coarse_bit(const uint32_t* __restrict__ coarse, uint64_t b) {
+    return (__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+// membership bits of cells (x .. x+15, y), 0 <= x, y < n; bits at x' >= n are 0
+__device__ __forceinline__ uint32_t bb_member16(const BBRowParams& p, const uint32_t* lt,
+                                                const uint32_t* __restrict__ coarse, uint32_t x, uint32_t y) {
+    const uint32_t cx = (uint32_t)__umul64hi((uint64_t)x, p.magicS);
+    const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
+    const uint32_t xl = x - cx * p.S, yl = y - cy * p.S;
+    const uint32_t* row = lt + yl * p.lt_words;
+    const uint32_t w = xl >> 5;
+    uint32_t bits = __funnelshift_r(row[w], row[w + 1], xl & 31) & 0xFFFFu;  // doubled row: no wrap
+    const uint64_t cb = (uint64_t)cy * p.CW + cx;
+    const uint32_t split = p.S - xl;  // bits >= split lie in coarse cell cx + 1
+    uint32_t keep = bb_coarse_bit(coarse, cb) ? 0xFFFFu : 0u;
+    if (split < 16) {
+        const uint32_t lo = (1u << split) - 1u;
+        const bool c1 = cx + 1 < p.CW && bb_coarse_bit(coarse, cb + 1);
+        keep = (keep & lo) | (c1 ? (~lo & 0xFFFFu) : 0u);
+    }
+    bits &= keep;
+    const uint64_t left = p.n - x;
+    if (left < 16) bits &= (1u << left) - 1u;
+    return bits;
+}
+
+// membership of the 16 bytes of the chunk at linear c (first byte in row y or y-1)
+__device__ __forceinline__ uint32_t bb_chunk_member(const BBRowParams& p, const uint32_t* lt,
+                                                    const uint32_t* __restrict__ coarse, int64_t c, int64_t y) {
+    const int64_t b1 = y * (int64_t)p.n - c;  // row y starts at byte b1 of the chunk
+    if (b1 > 0)
+        return (bb_member16(p, lt, coarse, (uint32_t)(p.n - b1), (uint32_t)(y - 1)) & ((1u << b1) - 1u)) |
+               ((bb_member16(p, lt, coarse, 0u, (uint32_t)y) << b1) & 0xFFFFu);
+    return bb_member16(p, lt, coarse, (uint32_t)(-b1), (uint32_t)y);
+}
+
+// does row y hold a fractal cell in [x0, x0 + 512)?  (coarse test, x0 >= 0; a
+// conservative "yes" when the range reaches past the row)
+__device__ __forceinline__ bool bb_run_live(const BBRowParams& p, const uint32_t* __restrict__ coarse, int64_t x0,
+                                            int64_t y) {
+    if (x0 + 512 > (int64_t)p.n) return true;
+    const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
+    const uint32_t cx0 = (uint32_t)__umul64hi((uint64_t)x0, p.magicS);
+    const uint32_t cx1 = (uint32_t)__umul64hi((uint64_t)(x0 + 511), p.magicS);  // <= cx0 + 16
+    const uint64_t b0 = (uint64_t)cy * p.CW + cx0;
+    const uint32_t nb = cx1 - cx0 + 1;
+    const uint64_t w = b0 >> 5;
+    const uint32_t lo = __ldg(coarse + w), hi = (b0 & 31) + nb > 32 ? __ldg(coarse + w + 1) : 0u;
+    const uint32_t bits = __funnelshift_r(lo, hi, (uint32_t)(b0 & 31));
+    return (bits & (nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u))) != 0u;
+}
+
+__device__ __forceinline__ void bb_cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void bb_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bb_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ int64_t bb_floor16(int64_t v) { return v & ~(int64_t)15; }
+
+// 16 bytes at byte offset o (0..15, warp-uniform) of the 32 bytes a|b
+__device__ __forceinline__ void bb_extract(const uint4 a, const uint4 b, uint32_t o, uint32_t out[4]) {
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t sh = 8u * (o & 3u);
+    switch (o >> 2) {  // uniform across the warp: no divergence, static register indices
+    case 0:
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j], v[j + 1], sh);
+        break;
+    case 1:
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 1], v[j + 2], sh);
+        break;
+    case 2:
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 2], v[j + 3], sh);
+        break;
+    default:
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 3], v[j + 4], sh);
+        break;
+    }
+}
+
+// one row window: R[1..4] = bytes [off, off + 16) of the slot, R[0] top byte = byte
+// off - 1, R[5] low byte = byte off + 16 (from the neighbouring lanes)
+__device__ __forceinline__ void bb_window(const uint8_t* slot, uint32_t off, int lane, uint32_t R[6]) {
+    uint32_t m[4];
+    const uint32_t a = off & ~15u;
+    const uint4 va = *reinterpret_cast<const uint4*>(slot + a);
+    if ((off & 15u) == 0u) {
+        m[0] = va.x; m[1] = va.y; m[2] = va.z; m[3] = va.w;
+    } else {
+        const uint4 vb = *reinterpret_cast<const uint4*>(slot + a + 16);
+        bb_extract(va, vb, off & 15u, m);
+    }
+    R[1] = m[0]; R[2] = m[1]; R[3] = m[2]; R[4] = m[3];
+    R[0] = __shfl_up_sync(0xFFFFFFFFu, m[3], 1);
+    R[5] = __shfl_down_sync(0xFFFFFFFFu, m[0], 1);
+    if (lane == 0) R[0] = (uint32_t)slot[off - 1] << 24;
+    if (lane == 31) R[5] = slot[off + 16];
+}
+
+__device__ __forceinline__ uint32_t bb_byte_mask(int64_t b, int j) {  // byte b (0..15) within word j
+    return (b >= 0 && b < 16 && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
+}
+
+template <bool CONWAY, int NS>
+__global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, const uint32_t* __restrict__ lowtab,
+                                                           const uint32_t* __restrict__ coarse,
+                                                           const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+    static_assert(NS >= 4, "rows y-1, y, y+1 plus one in flight");
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t W = (p.cps + 4) * 16;  // slot bytes
+    uint32_t* lt = reinterpret_cast<uint32_t*>(sm + NS * W);
+    const int t = threadIdx.x, lane = t & 31;
+    const int64_t n = (int64_t)p.n;
+    const int64_t y0 = (int64_t)blockIdx.y * p.rows;
+    const int64_t y1 = min(y0 + (int64_t)p.rows, n);
+    const int64_t xs = (int64_t)blockIdx.x * p.cps * 16;  // strip offset within an aligned row
+    for (uint32_t i = t; i < p.S * p.lt_words; i += blockDim.x) lt[i] = __ldg(lowtab + i);
+    __syncthreads();
+
     // rule tables (bytes 0/1) for counts 0..7 and the count-8 entries
     uint32_t tb_lo = 0, tb_hi = 0, ts_lo = 0, ts_hi = 0;
 #pragma unroll
@@ -82,64 +208,97 @@ __global__ void __launch_bounds__(256) step_bb_vec_kernel(const BBParams p, cons
         ts_hi |= ((p.survive >> (c + 4)) & 1u) << (8 * c);
     }
     const uint32_t b8 = ((p.birth >> 8) & 1u) * 0x01010101u, s8 = ((p.survive >> 8) & 1u) * 0x01010101u;
-    // grid-stride over whole warps so the shuffles always see 32 active lanes
-    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < total;
-         base += nthreads) {
-        const uint64_t v = base + lane;
-        const bool valid = v < total;
-        const uint32_t y = valid ? (uint32_t)(v / vpr) : 0u;
-        const uint32_t xv = valid ? (uint32_t)(v - (uint64_t)y * vpr) : 0u;
-        const uint32_t x0 = xv * 16;
-        const uint8_t* row = src + (uint64_t)y * n;
-        uint4 up = make_uint4(0, 0, 0, 0), mid = up, dn = up;
-        if (valid) {
-            mid = __ldg(reinterpret_cast<const uint4*>(row + x0));
-            if (y > 0) up = __ldg(reinterpret_cast<const uint4*>(row - n + x0));
-            if (y + 1 < n) dn = __ldg(reinterpret_cast<const uint4*>(row + n + x0));
-        }
-        // edge bytes: left = byte x0-1 (lane-1's .w top byte), right = byte x0+16
-        uint32_t lu = __shfl_up_sync(0xffffffffu, up.w, 1), lm = __shfl_up_sync(0xffffffffu, mid.w, 1),
-                 ld = __shfl_up_sync(0xffffffffu, dn.w, 1);
-        uint32_t ru = __shfl_down_sync(0xffffffffu, up.x, 1), rm = __shfl_down_sync(0xffffffffu, mid.x, 1),
-                 rd = __shfl_down_sync(0xffffffffu, dn.x, 1);
-        const bool same_row_left = lane > 0 && xv > 0;        // lane-1 holds the previous vector
-        const bool same_row_right = lane < 31 && xv + 1 < vpr;  // lane+1 holds the next vector
-        if (valid && !same_row_left) {
-            lu = lm = ld = 0;
-            if (x0 > 0) {
-                lm = (uint32_t)row[x0 - 1] << 24;
-                if (y > 0) lu = (uint32_t)row[(int64_t)x0 - 1 - (int64_t)n] << 24;
-                if (y + 1 < n) ld = (uint32_t)row[(int64_t)x0 - 1 + (int64_t)n] << 24;
-            }
-        }
-        if (valid && !same_row_right) {
-            ru = rm = rd = 0;
-            if (x0 + 16 < n) {
-                rm = row[x0 + 16];
-                if (y > 0) ru = row[(int64_t)x0 + 16 - (int64_t)n];
-                if (y + 1 < n) rd = row[(int64_t)x0 + 16 + (int64_t)n];
-            }
-        }
-        if (!valid) continue;
-        const uint32_t U[6] = {lu, up.x, up.y, up.z, up.w, ru};
-        const uint32_t M[6] = {lm, mid.x, mid.y, mid.z, mid.w, rm};
-        const uint32_t D[6] = {ld, dn.x, dn.y, dn.z, dn.w, rd};
-        // membership of the 16 cells
-        const uint32_t lowmask = bb_high_member(p, x0, y) ? p.low[y & 15] : 0u;
+
+    // row rho of the band (-1 .. n) -> slot (rho + NS) % NS; thread t loads chunk
+    // t + 2 of the segment, threads 0..3 also the margin chunks 0, 1, cps+2, cps+3
+    auto load_row = [&](int64_t rho) {
+        uint8_t* slot = sm + ((rho + NS) % NS) * W;
+        const int64_t base = bb_floor16(rho * n) + xs - 32;
+        // whole-warp hole skip of the warp's own 32 chunks (x range of row rho)
+        const int64_t wfirst = base + 32 + (int64_t)(t & ~31) * 16;
+        const int64_t x0 = wfirst - rho * n;
+        const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, coarse, x0, rho);
+        auto one = [&](uint32_t ch, bool want) {
+            const int64_t a = base + 16 * (int64_t)ch;
+            const bool in = want && a >= 0 && a + 16 <= (int64_t)p.alloc;
+            if (in) bb_cp_async16((uint32_t)__cvta_generic_to_shared(slot + 16 * ch), src + a, 16);
+            else *reinterpret_cast<uint4*>(slot + 16 * ch) = make_uint4(0, 0, 0, 0);
+        };
+        one((uint32_t)t + 2, live);
+        if (t < 4) one(t < 2 ? (uint32_t)t : p.cps + (uint32_t)t, true);
+    };
+
+    for (int i = 0; i < NS - 1; ++i) {
+        load_row(y0 - 1 + i);
+        bb_cp_commit();
+    }
+    for (int64_t y = y0; y < y1; ++y) {
+        bb_cp_wait<NS - 4>();  // rows <= y + 1 landed (this thread's copies)
+        __syncthreads();       // ... everyone's; slot of row y - 2 is free
+        load_row(y + NS - 2);
+        bb_cp_commit();
+
+        const int64_t sty = bb_floor16(y * n);
+        const int64_t c = sty + xs + 16 * (int64_t)t;
+        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16((y + 1) * n);
+        const int64_t wfirst = sty + xs + (int64_t)(t & ~31) * 16;
+        const bool live = wfirst - y * n < 0 || bb_run_live(p, coarse, wfirst - y * n, y);
+        if (!live) continue;  // warp-uniform: 512 bytes of holes stay 0
+        const uint8_t* sU = sm + ((y - 1 + NS) % NS) * W;
+        const uint8_t* sM = sm + ((y + NS) % NS) * W;
+        const uint8_t* sD = sm + ((y + 1) % NS) * W;
+        const uint32_t offM = 32 + 16 * t;
+        const uint32_t offU = (uint32_t)(sty - n - bb_floor16((y - 1) * n)) + offM;
+        const uint32_t offD = (uint32_t)(sty + n - bb_floor16((y + 1) * n)) + offM;
+        uint32_t U[6], M[6], D[6];
+        bb_window(sU, offU, lane, U);
+        bb_window(sM, offM, lane, M);
+        bb_window(sD, offD, lane, D);
+        if (c >= end) continue;
+        const uint32_t mem = bb_chunk_member(p, lt, coarse, c, y);
+        if (mem == 0u) continue;
+        // column edges: byte b1 has x = 0 (no west neighbours), byte b1 - 1 / b2 - 1
+        // has x = n - 1 (no east neighbours)
+        const int64_t b1 = y * n - c, b2 = b1 + n;
         uint32_t out[4];
 #pragma unroll
         for (int j = 1; j <= 4; ++j) {
-            // byte-shifted neighbours: west = byte x-1, east = byte x+1
-            const uint32_t uw = __funnelshift_l(U[j - 1], U[j], 8), ue = __funnelshift_r(U[j], U[j + 1], 8);
+            const uint32_t wm = bb_byte_mask(b1, j - 1) | bb_byte_mask(b2, j - 1);
+            const uint32_t em = bb_byte_mask(b1 - 1, j - 1) | bb_byte_mask(b2 - 1, j - 1);
             const uint32_t mw = __funnelshift_l(M[j - 1], M[j], 8), me = __funnelshift_r(M[j], M[j + 1], 8);
-            const uint32_t dw = __funnelshift_l(D[j - 1], D[j], 8), de = __funnelshift_r(D[j], D[j + 1], 8);
-            uint32_t cnt = U[j] + D[j] + mw + me;  // von Neumann: N, S, W, E
-            if (p.moore) cnt += uw + ue + dw + de;
+            uint32_t west = mw, east = me;
+            if (p.moore) {
+                west += __funnelshift_l(U[j - 1], U[j], 8) + __funnelshift_l(D[j - 1], D[j], 8);
+                east += __funnelshift_r(U[j], U[j + 1], 8) + __funnelshift_r(D[j], D[j + 1], 8);
+            }
+            const uint32_t cnt = U[j] + D[j] + (west & ~wm) + (east & ~em);
             const uint32_t r = bb_rule<CONWAY>(cnt, M[j], tb_lo, tb_hi, ts_lo, ts_hi, b8, s8);
-            out[j - 1] = r & bb_spread4(lowmask >> (4 * (j - 1)));
+            out[j - 1] = r & bb_spread4(mem >> (4 * (j - 1)));
         }
-        *reinterpret_cast<uint4*>(dst + (uint64_t)y * n + x0) = make_uint4(out[0], out[1], out[2], out[3]);
+        *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+    bb_cp_wait<0>();
+}
+
+// coarse membership bitmap: bit cy * CW + cx = cells (cx, cy) of the level-L
+// coarse box are in the fractal (the top L levels of maps.cpp:80-107)
+__global__ void bb_coarse_kernel(Frac f, int L, uint32_t CW, uint32_t* __restrict__ out, uint64_t nwords) {
+    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < nwords;
+         wi += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint64_t i = wi * 32 + b;
+            if (i >= (uint64_t)CW * CW) break;
+            uint32_t x = (uint32_t)(i % CW), y = (uint32_t)(i / CW);
+            bool in = true;
+            for (int mu = 0; mu < L && in; ++mu) {
+                in = f.id_of_subbox[(y % f.s) * f.s + (x % f.s)] >= 0;
+                x /= f.s;
+                y /= f.s;
+            }
+            if (in) v |= 1u << b;
+        }
+        out[wi] = v;
     }
 }
 

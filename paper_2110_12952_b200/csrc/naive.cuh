@@ -166,4 +166,16 @@ __global__ void check_binary_kernel(const uint8_t* __restrict__ p, uint64_t n, i
         if (p[i] > 1) *flag = 1;
 }
 
+// Bounding-box uploads: a live byte on a hole sets *flag (the reference's holes
+// are never written -- set_cell requires a fractal cell, stencil.cpp:190-194).
+template <int K, int S>
+__global__ void check_bb_holes_kernel(Frac f, const uint8_t* __restrict__ p, int* flag) {
+    const uint64_t n = f.side, total = n * n;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t cx, cy;
+        if (p[i] && !nu_map<K, S>(f, (uint32_t)(i % n), (uint32_t)(i / n), cx, cy)) *flag = 1;
+    }
+}
+
 }  // namespace nbbgpu

@@ -316,6 +316,11 @@ struct nbbgpu_sim {
     BlockedGeom bg{};          // NBBGPU_MODE_BLOCKED: block size rho = s^m, coarse tables
     uint32_t* d_lowmask = nullptr;  // filler mask of one block (rho^2 bits)
     uint32_t* d_blocktab = nullptr; // per block: neighbour blocks + coarse corner
+    // NBBGPU_MODE_BB row-streaming kernel (bb.cuh): doubled low table + coarse bitmap
+    uint32_t* d_bblow = nullptr;
+    uint32_t* d_bbcoarse = nullptr;
+    BBRowParams bbp{};
+    bool bb_ready = false;
     uint64_t cells = 0;      // stored cells per buffer
     uint8_t* buf[2] = {nullptr, nullptr};
     int cur = 0;             // front = buf[cur]
@@ -594,6 +599,72 @@ void ensure_nbr_table(nbbgpu_t h, int deg) {
     h->tab_deg = deg;
 }
 
+// tables of the row-streaming BB kernel (bb.cuh), once per handle
+void ensure_bb_tables(nbbgpu_t h) {
+    if (h->bb_ready) return;
+    const HostFrac& F = h->hf;
+    const int64_t n = F.side, s = F.s;
+    int m = 0;
+    int64_t S = 1;
+    while (S < 32) { S *= s; ++m; }
+    if (m > F.r) raise(NBBGPU_ERR_CUDA, "internal: bounding box below 32 columns");
+    BBRowParams& p = h->bbp;
+    p = BBRowParams{};
+    p.n = (uint64_t)n;
+    p.alloc = h->cells + 64;
+    p.S = (uint32_t)S;
+    p.CW = (uint32_t)(n / S);
+    p.magicS = ~0ull / (uint64_t)S + 1;
+    p.lt_words = (uint32_t)((2 * S + 31) / 32 + 1);
+    // low table: row yl, bit xl (0 <= xl < 2S) = the low m digit pairs of
+    // (xl mod S, yl) are replica positions
+    std::vector<uint32_t> lt((size_t)S * p.lt_words, 0u);
+    for (int64_t yl = 0; yl < S; ++yl)
+        for (int64_t xl = 0; xl < 2 * S; ++xl) {
+            int64_t x = xl % S, y = yl;
+            bool in = true;
+            for (int mu = 0; mu < m && in; ++mu) {
+                in = F.id[(y % s) * s + (x % s)] >= 0;
+                x /= s;
+                y /= s;
+            }
+            if (in) lt[(size_t)yl * p.lt_words + (xl >> 5)] |= 1u << (xl & 31);
+        }
+    dmalloc_cap(h->d_bblow, lt.size() * 4, "bounding-box low table");
+    CK(cudaMemcpy(h->d_bblow, lt.data(), lt.size() * 4, cudaMemcpyHostToDevice));
+    const uint64_t nwords = ((uint64_t)p.CW * p.CW + 31) / 32 + 1;
+    dmalloc_cap(h->d_bbcoarse, nwords * 4, "bounding-box coarse bitmap");
+    CK(cudaMemsetAsync(h->d_bbcoarse, 0, nwords * 4, h->stream));
+    bb_coarse_kernel<<<grid_for(nwords, 256), 256, 0, h->stream>>>(h->frac, F.r - m, p.CW, h->d_bbcoarse, nwords - 1);
+    CK(cudaGetLastError());
+    // strips: chunks per aligned row <= (n + 30) / 16 + 1, at most 256 per CTA
+    const uint64_t maxch = ((uint64_t)n + 30) / 16 + 2;
+    const uint64_t nsx = (maxch + 255) / 256;
+    p.cps = (uint32_t)(((maxch + nsx - 1) / nsx + 31) / 32 * 32);
+    uint64_t rows = 64;
+    while (rows > 8 && nsx * (((uint64_t)n + rows - 1) / rows) < 4ull * 148) rows /= 2;
+    p.rows = (uint32_t)rows;
+    h->bb_ready = true;
+}
+
+void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
+    ensure_bb_tables(h);
+    BBRowParams p = h->bbp;
+    p.birth = birth;
+    p.survive = survive;
+    p.moore = moore;
+    constexpr int NS = 6;
+    const uint64_t nsx = (((uint64_t)p.n + 30) / 16 + 2 + p.cps - 1) / p.cps;
+    const dim3 grid((unsigned)nsx, (unsigned)((p.n + p.rows - 1) / p.rows));
+    const size_t smem = (size_t)NS * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4;
+    const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
+    if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
+    if (conway)
+        step_bb_rows_kernel<true, NS><<<grid, p.cps, smem, h->stream>>>(p, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+    else
+        step_bb_rows_kernel<false, NS><<<grid, p.cps, smem, h->stream>>>(p, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+}
+
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const int deg = moore ? 8 : 4;
     const uint8_t* src = h->front();
@@ -618,39 +689,11 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
         struct ProfEnd { nbbgpu_t h; ~ProfEnd() { prof_mark(h); } } prof_end{h};
         const uint64_t n = (uint64_t)h->hf.side * h->hf.side;
         const int s = h->hf.s;
-        if ((s == 2 || s == 4) && h->hf.side % 16 == 0 && h->kernel != NBBGPU_KERNEL_NAIVE) {
-            // vectorised BB baseline (bb.cuh)
-            BBParams p{};
-            p.f = h->frac;
-            p.n = (uint32_t)h->hf.side;
-            p.mlow = s == 2 ? 4 : 2;
-            p.triangle = (h->hf.k == 3 && s == 2 && h->hf.gx[0] == 0 && h->hf.gy[0] == 0 &&
-                          h->hf.gx[1] == 1 && h->hf.gy[1] == 0 && h->hf.gx[2] == 0 && h->hf.gy[2] == 1);
-            for (int yl = 0; yl < 16; ++yl) {
-                uint32_t m = 0;
-                for (int i = 0; i < 16; ++i) {
-                    bool ok = true;
-                    int xx = i, yy = yl;
-                    for (int mu = 0; mu < p.mlow && mu < h->hf.r; ++mu) {
-                        if (h->hf.id[(yy % s) * s + (xx % s)] < 0) ok = false;
-                        xx /= s;
-                        yy /= s;
-                    }
-                    if (ok) m |= 1u << i;
-                }
-                p.low[yl] = (uint16_t)m;
-            }
-            p.birth = birth;
-            p.survive = survive;
-            p.moore = moore;
-            const uint64_t vecs = n / 16;
-            const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((vecs + 255) / 256, 148ull * 16));
-            if ((birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore)
-                step_bb_vec_kernel<true><<<blocks, 256, 0, h->stream>>>(p, src, dst);
-            else
-                step_bb_vec_kernel<false><<<blocks, 256, 0, h->stream>>>(p, src, dst);
+        if (h->hf.side >= 32 && h->kernel != NBBGPU_KERNEL_NAIVE) {
+            launch_bb_rows(h, birth, survive, moore);  // bb.cuh
             return;
         }
+        (void)s;
 #define NBB_CALL(K, S, ...) step_bb_naive_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, src, dst, birth, survive, deg)
         NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL
@@ -758,6 +801,8 @@ void free_all(nbbgpu_t h) {
     if (h->d_phent) cudaFree(h->d_phent);
     if (h->d_gbar) cudaFree(h->d_gbar);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
+    if (h->d_bblow) cudaFree(h->d_bblow);
+    if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);
     if (h->d_tab) cudaFree(h->d_tab);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
@@ -1237,13 +1282,20 @@ int nbbgpu_upload(nbbgpu_t h, const uint8_t* src, uint64_t bytes) {
         CK(cudaMemcpyAsync(h->back(), src, bytes, cudaMemcpyDefault, h->stream));
         CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
         check_binary_kernel<<<grid_for(bytes, 256), 256, 0, h->stream>>>(h->back(), bytes, h->d_flag);
+        if (h->mode == NBBGPU_MODE_BB) {  // holes are dead in the box (set_cell rejects them)
+#define NBB_CALL(K, S, ...) check_bb_holes_kernel<K, S><<<grid_for(bytes, 256), 256, 0, h->stream>>>(h->frac, h->back(), h->d_flag)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
         int flag = 0;
         CK(cudaMemcpyAsync(&flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
         if (flag) {
             CK(cudaMemsetAsync(h->back(), 0, bytes, h->stream));
             CK(cudaStreamSynchronize(h->stream));
-            raise(NBBGPU_ERR_OUT_OF_DOMAIN, "GPU backends store binary cell states (bytes 0/1)");
+            raise(NBBGPU_ERR_OUT_OF_DOMAIN, h->mode == NBBGPU_MODE_BB
+                                                ? "GPU backends store binary cell states (bytes 0/1) and dead holes"
+                                                : "GPU backends store binary cell states (bytes 0/1)");
         }
         CK(cudaMemcpyAsync(h->front(), h->back(), bytes, cudaMemcpyDeviceToDevice, h->stream));
         CK(cudaMemsetAsync(h->back(), 0, bytes, h->stream));

@@ -900,15 +900,17 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                     for (int u = 0; u < 8; ++u)
                         v[u] = t2[u] != kNoTile ? __ldcg(bsrc + (size_t)(t2[u] >> 5) * p.nSrc + (sl[u] & 0xFFFFu)) >> (t2[u] & 31)
                                                 : 0u;
-                    uint32_t mine = 0;
+                    // every lane holds every ballot; lane 0 -- the thread that arrives on
+                    // the full barrier -- stores them, so its release covers the writes
+                    uint32_t words[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
-                        if (lane == (uint32_t)u) mine = word;
+                    for (int u = 0; u < 8; ++u) words[u] = __ballot_sync(0xFFFFFFFFu, (v[u] & 1u) != 0);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (j0 + u < p.nH) Hs[j0 + u] = words[u];
                     }
-                    if (lane < 8 && j0 + lane < p.nH) Hs[j0 + lane] = mine;
                 }
-                __syncwarp();
                 if (lane == 0) mbar_arrive(full0 + 8 * s);  // release: the halo words are visible
             }
             return;

@@ -342,25 +342,60 @@ def test_run_simulation_determinism():
         run_simulation(T, 3, Backend.GpuCompact, conway_rule(), -1, 0, 0.5)
 
 
-def test_bb_vectorised_kernel_vs_oracle():
-    # the vectorised BB baseline (s = 2, 4) against the oracle's step_bounding_box,
-    # including B0 rules (holes must stay 0) and von Neumann neighbourhoods
-    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
-                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
-    rng = np.random.default_rng(99)
-    for desc, r in [(T, 5), (T, 7), (SOLID, 6), (Y, 3)]:
-        for trial in range(4):
-            rule = conway_rule() if trial == 0 else StencilRule(
-                int(rng.integers(0, 512)) | (1 if trial == 3 else 0), int(rng.integers(0, 512)),
-                Neighborhood.Moore if trial != 2 else Neighborhood.VonNeumann)
-            o = oracle.Oracle(desc.replicas, desc.k, desc.s, r, mode="bb")
-            o.seed(trial + 3, 0.5)
-            sim = Simulation(desc, r, Backend.GpuBoundingBox)
-            sim.seed_random(trial + 3, 0.5)
-            for i in range(5):
-                o.step(rule.birth, rule.survive, rule.moore)
-                sim.step(rule)
-                assert np.array_equal(sim.front().data, o.front), (desc.name, r, rule.to_string(), i)
+BB_CASES = [  # (descriptor, level): every growth factor class and n mod 16 (row alignment)
+    (T, 5), (T, 7), (T, 10), (SOLID, 6),
+    (FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                    (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)]), 3),  # n = 64
+    (CARPET, 4), (CARPET, 5), (CARPET, 6),                       # n = 81, 243, 729
+    (VICSEK, 4), (VICSEK, 5),                                    # n % 16 = 1, 3
+    (FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)]), 5),
+    (FractalDescriptor("p5", 13, 5, [(0, 0), (2, 0), (4, 0), (1, 1), (3, 1), (0, 2), (2, 2), (4, 2),
+                                     (1, 3), (3, 3), (0, 4), (2, 4), (4, 4)]), 3),  # n = 125
+    (FractalDescriptor("s6", 20, 6, [(x, y) for y in range(6) for x in range(6)
+                                     if (x + 2 * y) % 9 not in (0, 4)][:20]), 2),   # n = 36
+    (FractalDescriptor("s7", 25, 7, [(x, y) for y in range(7) for x in range(7) if (x * y) % 3 != 1][:25]), 2),
+    (FractalDescriptor("s16", 100, 16, [(x, y) for y in range(16) for x in range(16)
+                                        if (x ^ y) % 5 != 2 and (x + y) % 7 != 3][:100]), 2),  # n = 256
+    (FractalDescriptor("s11", 60, 11, [(x, y) for y in range(11) for x in range(11)
+                                       if (3 * x + y) % 4 != 0][:60]), 2),  # n = 121 (n % 16 = 9)
+]
+
+
+@pytest.mark.parametrize("case", range(len(BB_CASES)))
+def test_bb_rows_kernel_vs_oracle(case):
+    # the row-streaming BB baseline (bb.cuh, any s, any row alignment) against the
+    # oracle's step_bounding_box byte for byte, with B0 rules (holes must stay 0),
+    # von Neumann neighbourhoods, sparse and dense seeds
+    desc, r = BB_CASES[case]
+    desc.validate()
+    rng = np.random.default_rng(99 + case)
+    for trial in range(4):
+        rule = conway_rule() if trial == 0 else StencilRule(
+            int(rng.integers(0, 512)) | (1 if trial == 3 else 0), int(rng.integers(0, 512)),
+            Neighborhood.Moore if trial != 2 else Neighborhood.VonNeumann)
+        density = (0.5, 0.2, 0.8, 0.5)[trial]
+        o = oracle.Oracle(desc.replicas, desc.k, desc.s, r, mode="bb")
+        o.seed(trial + 3, density)
+        sim = Simulation(desc, r, Backend.GpuBoundingBox)
+        sim.seed_random(trial + 3, density)
+        for i in range(5):
+            o.step(rule.birth, rule.survive, rule.moore)
+            sim.step(rule)
+            assert np.array_equal(sim.front().data, o.front), (desc.name, r, rule.to_string(), i)
+        assert sim.state_hash() == o.state_hash()
+        sim.close()
+
+
+def test_bb_upload_rejects_live_holes():
+    sim = Simulation(CARPET, 4, Backend.GpuBoundingBox)
+    sim.seed_random(1, 0.5)
+    data = sim.front().data.copy()
+    bad = data.copy()
+    bad[1 * 81 + 1] = 1  # (1, 1) is a hole of the carpet
+    with pytest.raises(OutOfDomain, match="dead holes"):
+        sim.upload(bad)
+    assert np.array_equal(sim.front().data, data)
+    sim.close()
 
 
 def test_naive_kernel_with_tensor_core_maps():

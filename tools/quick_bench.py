@@ -28,17 +28,22 @@ def main(cases):
         f, level, kernel = case.split(":")
         level = int(level)
         d = DESCS[f]
-        sim = Simulation(d, level, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 42))
+        if kernel == "bb":  # the bounding-box baseline
+            sim = Simulation(d, level, Backend.GpuBoundingBox, SimOptions(memory_cap=1 << 42))
+        else:
+            sim = Simulation(d, level, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 42))
         sim.seed_random(42, 0.5)
         sim.step(rule, 3)
         steps = int(os.environ.get("QB_STEPS", "20"))
         ms = sim.step_timed(rule, steps) / steps
         cells = d.k ** level
         extra = ""
+        if kernel == "bb":
+            extra = f" | BB dense model {2 * d.s ** (2 * level) / (ms / 1e3) / 1e9:.0f} GB/s"
         if os.environ.get("QB_PROF"):
             tot, main, n = sim.step_profiled(rule, steps)
             extra = f" | step kernel {main / steps * 1e3:.1f} us of {tot / steps * 1e3:.1f} us, {n / steps:.0f} launches/step"
-        print(f"{case:14s} {sim.active_kernel()} {ms:9.4f} ms/step {cells * 1e3 / ms:10.3e} cell-updates/s "
+        print(f"{case:14s} {sim.active_kernel() if kernel != 'bb' else 'bb'} {ms:9.4f} ms/step {cells * 1e3 / ms:10.3e} cell-updates/s "
               f"hash={sim.state_hash():016x} held={sim.peak_bytes() / 1e9:.3f} GB{extra}", flush=True)
         sim.close()
 
