@@ -73,25 +73,37 @@ __device__ __forceinline__ uint32_t bb_rule(uint32_t cnt, uint32_t alive, uint32
     }
 }
 
-__device__ __forceinline__ bool bb_coarse_bit(const uint32_t* __restrict__ coarse, uint64_t b) {
-    return (__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u;
+// The coarse bitmap rows / columns a CTA touches, cached in shared memory: rows
+// [cy0, cy0 + nrows), columns [cx0, cx1] (wpr words per row), and column CW - 1
+// per row in `last` (strip 0's row-straddling chunks end the previous row).
+struct BBCoarse {
+    const uint32_t* bits;
+    uint32_t cy0, cx0, cx1, wpr, last;
+};
+
+__device__ __forceinline__ bool bb_coarse_bit(const BBCoarse& c, uint32_t cx, uint32_t cy) {
+    const uint32_t ry = cy - c.cy0;
+    if (cx >= c.cx0 && cx <= c.cx1) {
+        const uint32_t b = cx - c.cx0;
+        return (c.bits[ry * c.wpr + (b >> 5)] >> (b & 31)) & 1u;
+    }
+    return (c.last >> ry) & 1u;
 }
 
 // membership bits of cells (x .. x+15, y), 0 <= x, y < n; bits at x' >= n are 0
-__device__ __forceinline__ uint32_t bb_member16(const BBRowParams& p, const uint32_t* lt,
-                                                const uint32_t* __restrict__ coarse, uint32_t x, uint32_t y) {
+__device__ __forceinline__ uint32_t bb_member16(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
+                                                uint32_t x, uint32_t y) {
     const uint32_t cx = (uint32_t)__umul64hi((uint64_t)x, p.magicS);
     const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
     const uint32_t xl = x - cx * p.S, yl = y - cy * p.S;
     const uint32_t* row = lt + yl * p.lt_words;
     const uint32_t w = xl >> 5;
     uint32_t bits = __funnelshift_r(row[w], row[w + 1], xl & 31) & 0xFFFFu;  // doubled row: no wrap
-    const uint64_t cb = (uint64_t)cy * p.CW + cx;
     const uint32_t split = p.S - xl;  // bits >= split lie in coarse cell cx + 1
-    uint32_t keep = bb_coarse_bit(coarse, cb) ? 0xFFFFu : 0u;
+    uint32_t keep = bb_coarse_bit(cc, cx, cy) ? 0xFFFFu : 0u;
     if (split < 16) {
         const uint32_t lo = (1u << split) - 1u;
-        const bool c1 = cx + 1 < p.CW && bb_coarse_bit(coarse, cb + 1);
+        const bool c1 = cx + 1 < p.CW && bb_coarse_bit(cc, cx + 1, cy);
         keep = (keep & lo) | (c1 ? (~lo & 0xFFFFu) : 0u);
     }
     bits &= keep;
@@ -101,29 +113,27 @@ __device__ __forceinline__ uint32_t bb_member16(const BBRowParams& p, const uint
 }
 
 // membership of the 16 bytes of the chunk at linear c (first byte in row y or y-1)
-__device__ __forceinline__ uint32_t bb_chunk_member(const BBRowParams& p, const uint32_t* lt,
-                                                    const uint32_t* __restrict__ coarse, int64_t c, int64_t y) {
+__device__ __forceinline__ uint32_t bb_chunk_member(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
+                                                    int64_t c, int64_t y) {
     const int64_t b1 = y * (int64_t)p.n - c;  // row y starts at byte b1 of the chunk
     if (b1 > 0)
-        return (bb_member16(p, lt, coarse, (uint32_t)(p.n - b1), (uint32_t)(y - 1)) & ((1u << b1) - 1u)) |
-               ((bb_member16(p, lt, coarse, 0u, (uint32_t)y) << b1) & 0xFFFFu);
-    return bb_member16(p, lt, coarse, (uint32_t)(-b1), (uint32_t)y);
+        return (bb_member16(p, lt, cc, (uint32_t)(p.n - b1), (uint32_t)(y - 1)) & ((1u << b1) - 1u)) |
+               ((bb_member16(p, lt, cc, 0u, (uint32_t)y) << b1) & 0xFFFFu);
+    return bb_member16(p, lt, cc, (uint32_t)(-b1), (uint32_t)y);
 }
 
 // does row y hold a fractal cell in [x0, x0 + 512)?  (coarse test, x0 >= 0; a
 // conservative "yes" when the range reaches past the row)
-__device__ __forceinline__ bool bb_run_live(const BBRowParams& p, const uint32_t* __restrict__ coarse, int64_t x0,
-                                            int64_t y) {
+__device__ __forceinline__ bool bb_run_live(const BBRowParams& p, const BBCoarse& cc, int64_t x0, int64_t y) {
     if (x0 + 512 > (int64_t)p.n) return true;
     const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
     const uint32_t cx0 = (uint32_t)__umul64hi((uint64_t)x0, p.magicS);
     const uint32_t cx1 = (uint32_t)__umul64hi((uint64_t)(x0 + 511), p.magicS);  // <= cx0 + 16
-    const uint64_t b0 = (uint64_t)cy * p.CW + cx0;
-    const uint32_t nb = cx1 - cx0 + 1;
-    const uint64_t w = b0 >> 5;
-    const uint32_t lo = __ldg(coarse + w), hi = (b0 & 31) + nb > 32 ? __ldg(coarse + w + 1) : 0u;
-    const uint32_t bits = __funnelshift_r(lo, hi, (uint32_t)(b0 & 31));
-    return (bits & (nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u))) != 0u;
+    const uint32_t b0 = cx0 - cc.cx0, nb = cx1 - cx0 + 1;
+    const uint32_t* row = cc.bits + (cy - cc.cy0) * cc.wpr;
+    const uint32_t w = b0 >> 5;
+    const uint32_t bits = __funnelshift_r(row[w], row[w + 1], b0 & 31);
+    return (bits & ((1u << nb) - 1u)) != 0u;  // nb <= 18
 }
 
 __device__ __forceinline__ void bb_cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
@@ -182,19 +192,66 @@ __device__ __forceinline__ uint32_t bb_byte_mask(int64_t b, int j) {  // byte b 
     return (b >= 0 && b < 16 && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
 }
 
+// shared-memory layout of step_bb_rows_kernel: NS ring slots, the low table, the
+// coarse cache (at most kBBCacheWords words)
+constexpr uint32_t kBBCacheWords = 64;
+constexpr int kBBStages = 6;
+
+// coarse rows / columns of tile (sx, band): rows y0 - 1 .. y1 + NS, x within
+// [xs - 16, xs + 16 cps + 16], plus column CW - 1
+__device__ __host__ __forceinline__ void bb_tile_cover(const BBRowParams& p, uint32_t sx, uint32_t band, int ns,
+                                                       uint32_t& cy0, uint32_t& cy1, uint32_t& cx0, uint32_t& cx1) {
+    const int64_t n = (int64_t)p.n;
+    const int64_t y0 = (int64_t)band * p.rows, y1 = y0 + p.rows < n ? y0 + p.rows : n;
+    const int64_t xs = (int64_t)sx * p.cps * 16;
+    const int64_t ya = y0 - 1 > 0 ? y0 - 1 : 0, yb = y1 + ns < n - 1 ? y1 + ns : n - 1;
+    const int64_t xa = xs - 16 > 0 ? xs - 16 : 0;
+    const int64_t xb = xs + 16 * (int64_t)p.cps + 16 < n - 1 ? xs + 16 * (int64_t)p.cps + 16 : n - 1;
+    cy0 = (uint32_t)(ya / p.S);
+    cy1 = (uint32_t)(yb / p.S);
+    cx0 = (uint32_t)(xa / p.S);
+    cx1 = (uint32_t)(xb / p.S);
+}
+
+// One CTA per live tile (strip sx of the aligned rows of band b: tiles whose output
+// bytes are all holes are left out of the list on the host).
 template <bool CONWAY, int NS>
-__global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, const uint32_t* __restrict__ lowtab,
+__global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles,
+                                                           const uint32_t* __restrict__ lowtab,
                                                            const uint32_t* __restrict__ coarse,
                                                            const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
     static_assert(NS >= 4, "rows y-1, y, y+1 plus one in flight");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t W = (p.cps + 4) * 16;  // slot bytes
     uint32_t* lt = reinterpret_cast<uint32_t*>(sm + NS * W);
+    uint32_t* ccw = lt + p.S * p.lt_words;
     const int t = threadIdx.x, lane = t & 31;
     const int64_t n = (int64_t)p.n;
-    const int64_t y0 = (int64_t)blockIdx.y * p.rows;
+    const uint2 tile = tiles[blockIdx.x];
+    const int64_t y0 = (int64_t)tile.y * p.rows;
     const int64_t y1 = min(y0 + (int64_t)p.rows, n);
-    const int64_t xs = (int64_t)blockIdx.x * p.cps * 16;  // strip offset within an aligned row
+    const int64_t xs = (int64_t)tile.x * p.cps * 16;  // strip offset within an aligned row
+    BBCoarse cc;
+    uint32_t cy1;
+    bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
+    cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 1;
+    cc.bits = ccw;
+    cc.last = 0;
+    for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry)
+        cc.last |= (uint32_t)((__ldg(coarse + (((uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1) >> 5)) >>
+                               ((((uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1)) & 31)) & 1u) << ry;
+    for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += blockDim.x) {
+        const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
+        const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
+        const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
+        uint32_t v = 0;
+        if (32 * k < ncols) {
+            v = __funnelshift_r(__ldg(coarse + (b0 >> 5)), __ldg(coarse + (b0 >> 5) + 1), (uint32_t)(b0 & 31));
+            const uint32_t left = ncols - 32 * k;
+            if (left < 32) v &= (1u << left) - 1u;
+        }
+        ccw[i] = v;
+    }
     for (uint32_t i = t; i < p.S * p.lt_words; i += blockDim.x) lt[i] = __ldg(lowtab + i);
     __syncthreads();
 
@@ -215,9 +272,8 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         uint8_t* slot = sm + ((rho + NS) % NS) * W;
         const int64_t base = bb_floor16(rho * n) + xs - 32;
         // whole-warp hole skip of the warp's own 32 chunks (x range of row rho)
-        const int64_t wfirst = base + 32 + (int64_t)(t & ~31) * 16;
-        const int64_t x0 = wfirst - rho * n;
-        const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, coarse, x0, rho);
+        const int64_t x0 = base + 32 + (int64_t)(t & ~31) * 16 - rho * n;
+        const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
         auto one = [&](uint32_t ch, bool want) {
             const int64_t a = base + 16 * (int64_t)ch;
             const bool in = want && a >= 0 && a + 16 <= (int64_t)p.alloc;
@@ -241,8 +297,8 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         const int64_t sty = bb_floor16(y * n);
         const int64_t c = sty + xs + 16 * (int64_t)t;
         const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16((y + 1) * n);
-        const int64_t wfirst = sty + xs + (int64_t)(t & ~31) * 16;
-        const bool live = wfirst - y * n < 0 || bb_run_live(p, coarse, wfirst - y * n, y);
+        const int64_t x0 = sty + xs + (int64_t)(t & ~31) * 16 - y * n;
+        const bool live = x0 < 0 || bb_run_live(p, cc, x0, y);
         if (!live) continue;  // warp-uniform: 512 bytes of holes stay 0
         const uint8_t* sU = sm + ((y - 1 + NS) % NS) * W;
         const uint8_t* sM = sm + ((y + NS) % NS) * W;
@@ -255,7 +311,7 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         bb_window(sM, offM, lane, M);
         bb_window(sD, offD, lane, D);
         if (c >= end) continue;
-        const uint32_t mem = bb_chunk_member(p, lt, coarse, c, y);
+        const uint32_t mem = bb_chunk_member(p, lt, cc, c, y);
         if (mem == 0u) continue;
         // column edges: byte b1 has x = 0 (no west neighbours), byte b1 - 1 / b2 - 1
         // has x = n - 1 (no east neighbours)
@@ -278,6 +334,31 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
     }
     bb_cp_wait<0>();
+}
+
+// tile liveness: any fractal cell among the coarse cells covering a tile's output
+// bytes (rows y0 - 1 .. y1 - 1, x in [xs - 16, xs + 16 cps + 16], column CW - 1 for
+// strip 0's row-straddling chunks)
+__global__ void bb_tile_live_kernel(const BBRowParams p, const uint32_t* __restrict__ coarse, uint32_t nsx,
+                                    uint32_t nbands, uint8_t* __restrict__ live) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)nsx * nbands;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sx = (uint32_t)(i % nsx), band = (uint32_t)(i / nsx);
+        uint32_t cy0, cy1, cx0, cx1;
+        bb_tile_cover(p, sx, band, 0, cy0, cy1, cx0, cx1);
+        bool any = false;
+        for (uint32_t cy = cy0; cy <= cy1 && !any; ++cy) {
+            for (uint32_t cx = cx0; cx <= cx1 && !any; ++cx) {
+                const uint64_t b = (uint64_t)cy * p.CW + cx;
+                any = (coarse[b >> 5] >> (b & 31)) & 1u;
+            }
+            if (sx == 0) {
+                const uint64_t b = (uint64_t)cy * p.CW + p.CW - 1;
+                any = any || ((coarse[b >> 5] >> (b & 31)) & 1u);
+            }
+        }
+        live[i] = any ? 1 : 0;
+    }
 }
 
 // coarse membership bitmap: bit cy * CW + cx = cells (cx, cy) of the level-L

@@ -319,6 +319,8 @@ struct nbbgpu_sim {
     // NBBGPU_MODE_BB row-streaming kernel (bb.cuh): doubled low table + coarse bitmap
     uint32_t* d_bblow = nullptr;
     uint32_t* d_bbcoarse = nullptr;
+    uint2* d_bbtiles = nullptr;     // live (strip, band) tiles
+    uint32_t bb_ntiles = 0;
     BBRowParams bbp{};
     bool bb_ready = false;
     uint64_t cells = 0;      // stored cells per buffer
@@ -644,6 +646,24 @@ void ensure_bb_tables(nbbgpu_t h) {
     uint64_t rows = 64;
     while (rows > 8 && nsx * (((uint64_t)n + rows - 1) / rows) < 4ull * 148) rows /= 2;
     p.rows = (uint32_t)rows;
+    // live tiles: (strip, band) pairs whose output bytes hold a fractal cell
+    const uint64_t nbands = ((uint64_t)n + rows - 1) / rows, ntiles = nsx * nbands;
+    if (nsx > 0xFFFFFFFFull || nbands > 0xFFFFFFFFull) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "bounding box too large");
+    uint8_t* d_live = nullptr;
+    dmalloc_cap(d_live, ntiles, "bounding-box tile flags");
+    bb_tile_live_kernel<<<grid_for(ntiles, 256), 256, 0, h->stream>>>(p, h->d_bbcoarse, (uint32_t)nsx, (uint32_t)nbands, d_live);
+    std::vector<uint8_t> live(ntiles);
+    const cudaError_t e1 = cudaMemcpyAsync(live.data(), d_live, ntiles, cudaMemcpyDeviceToHost, h->stream);
+    const cudaError_t e2 = cudaStreamSynchronize(h->stream);
+    cudaFree(d_live);
+    CK(e1);
+    CK(e2);
+    std::vector<uint2> tiles;
+    for (uint64_t i = 0; i < ntiles; ++i)
+        if (live[i]) tiles.push_back(make_uint2((uint32_t)(i % nsx), (uint32_t)(i / nsx)));
+    h->bb_ntiles = (uint32_t)tiles.size();
+    dmalloc_cap(h->d_bbtiles, std::max<size_t>(1, tiles.size()) * sizeof(uint2), "bounding-box tile list");
+    if (!tiles.empty()) CK(cudaMemcpy(h->d_bbtiles, tiles.data(), tiles.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     h->bb_ready = true;
 }
 
@@ -653,16 +673,15 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.birth = birth;
     p.survive = survive;
     p.moore = moore;
-    constexpr int NS = 6;
-    const uint64_t nsx = (((uint64_t)p.n + 30) / 16 + 2 + p.cps - 1) / p.cps;
-    const dim3 grid((unsigned)nsx, (unsigned)((p.n + p.rows - 1) / p.rows));
-    const size_t smem = (size_t)NS * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4;
+    if (h->bb_ntiles == 0) return;
+    const dim3 grid(h->bb_ntiles);
+    const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4;
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
     if (conway)
-        step_bb_rows_kernel<true, NS><<<grid, p.cps, smem, h->stream>>>(p, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+        step_bb_rows_kernel<true, kBBStages><<<grid, p.cps, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
     else
-        step_bb_rows_kernel<false, NS><<<grid, p.cps, smem, h->stream>>>(p, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+        step_bb_rows_kernel<false, kBBStages><<<grid, p.cps, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
@@ -803,6 +822,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_lowmask) cudaFree(h->d_lowmask);
     if (h->d_bblow) cudaFree(h->d_bblow);
     if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);
+    if (h->d_bbtiles) cudaFree(h->d_bbtiles);
     if (h->d_tab) cudaFree(h->d_tab);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
