@@ -169,10 +169,8 @@ __device__ __forceinline__ void bb_extract(const uint4 a, const uint4 b, uint32_
     }
 }
 
-// one row window: R[1..4] = bytes [off, off + 16) of the slot, R[0] top byte = byte
-// off - 1, R[5] low byte = byte off + 16 (from the neighbouring lanes)
-__device__ __forceinline__ void bb_window(const uint8_t* slot, uint32_t off, int lane, uint32_t R[6]) {
-    uint32_t m[4];
+// the 16 bytes [off, off + 16) of a ring slot (off & 15 is warp-uniform)
+__device__ __forceinline__ void bb_mid(const uint8_t* slot, uint32_t off, uint32_t m[4]) {
     const uint32_t a = off & ~15u;
     const uint4 va = *reinterpret_cast<const uint4*>(slot + a);
     if ((off & 15u) == 0u) {
@@ -181,15 +179,11 @@ __device__ __forceinline__ void bb_window(const uint8_t* slot, uint32_t off, int
         const uint4 vb = *reinterpret_cast<const uint4*>(slot + a + 16);
         bb_extract(va, vb, off & 15u, m);
     }
-    R[1] = m[0]; R[2] = m[1]; R[3] = m[2]; R[4] = m[3];
-    R[0] = __shfl_up_sync(0xFFFFFFFFu, m[3], 1);
-    R[5] = __shfl_down_sync(0xFFFFFFFFu, m[0], 1);
-    if (lane == 0) R[0] = (uint32_t)slot[off - 1] << 24;
-    if (lane == 31) R[5] = slot[off + 16];
 }
 
-__device__ __forceinline__ uint32_t bb_byte_mask(int64_t b, int j) {  // byte b (0..15) within word j
-    return (b >= 0 && b < 16 && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
+// 0xFF in byte b (0..15) of a 16-byte chunk, as word j
+__device__ __forceinline__ uint32_t bb_byte_mask(int b, int j) {
+    return ((unsigned)b < 16u && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
 }
 
 // shared-memory layout of step_bb_rows_kernel: NS ring slots, the low table, the
@@ -266,13 +260,14 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
     }
     const uint32_t b8 = ((p.birth >> 8) & 1u) * 0x01010101u, s8 = ((p.survive >> 8) & 1u) * 0x01010101u;
 
-    // row rho of the band (-1 .. n) -> slot (rho + NS) % NS; thread t loads chunk
-    // t + 2 of the segment, threads 0..3 also the margin chunks 0, 1, cps+2, cps+3
-    auto load_row = [&](int64_t rho) {
-        uint8_t* slot = sm + ((rho + NS) % NS) * W;
-        const int64_t base = bb_floor16(rho * n) + xs - 32;
-        // whole-warp hole skip of the warp's own 32 chunks (x range of row rho)
-        const int64_t x0 = base + 32 + (int64_t)(t & ~31) * 16 - rho * n;
+    // row rho of the band (-1 .. n) -> slot (rho + 1) % NS (rho >= -1); thread t
+    // loads chunk t + 2 of the segment, threads 0..3 also the margin chunks 0, 1,
+    // cps+2, cps+3.  A warp whose own 32 chunks are holes zero-fills them instead.
+    const int64_t wx = xs + (int64_t)(t & ~31) * 16;  // the warp's first chunk, relative to floor16(rho n)
+    auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
+        uint8_t* slot = sm + sl * W;
+        const int64_t base = bb_floor16(rn) + xs - 32;
+        const int64_t x0 = bb_floor16(rn) + wx - rn;
         const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
         auto one = [&](uint32_t ch, bool want) {
             const int64_t a = base + 16 * (int64_t)ch;
@@ -284,51 +279,86 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         if (t < 4) one(t < 2 ? (uint32_t)t : p.cps + (uint32_t)t, true);
     };
 
-    for (int i = 0; i < NS - 1; ++i) {
-        load_row(y0 - 1 + i);
-        bb_cp_commit();
+    int sl_load = 0;  // slot of row y0 - 1 (rows map to slots in order)
+    {
+        int64_t rn = (y0 - 1) * n;
+        for (int i = 0; i < NS - 1; ++i, rn += n) {
+            load_row(y0 - 1 + i, rn, sl_load);
+            sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
+            bb_cp_commit();
+        }
     }
-    for (int64_t y = y0; y < y1; ++y) {
+    int slU = 0;                       // slot of row y - 1
+    int64_t yn = y0 * n;               // y * n
+    int64_t rn_load = (y0 + NS - 2) * n;
+    const uint32_t offM = 32 + 16 * t;
+    for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
         bb_cp_wait<NS - 4>();  // rows <= y + 1 landed (this thread's copies)
         __syncthreads();       // ... everyone's; slot of row y - 2 is free
-        load_row(y + NS - 2);
+        load_row(y + NS - 2, rn_load, sl_load);
+        sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
         bb_cp_commit();
 
-        const int64_t sty = bb_floor16(y * n);
+        const int slM = slU + 1 == NS ? 0 : slU + 1, slD = slM + 1 == NS ? 0 : slM + 1;
+        const uint8_t* sU = sm + slU * W;
+        const uint8_t* sM = sm + slM * W;
+        const uint8_t* sD = sm + slD * W;
+        slU = slM;
+        const int64_t sty = bb_floor16(yn);
+        const int64_t x0 = sty + wx - yn;  // warp's first byte, as x of row y (< 0: straddles)
+        if (x0 >= 0 && !bb_run_live(p, cc, x0, y)) continue;  // warp-uniform: 512 bytes of holes
+        const uint32_t offU = (uint32_t)(sty - n - bb_floor16(yn - n)) + offM;
+        const uint32_t offD = (uint32_t)(sty + n - bb_floor16(yn + n)) + offM;
+        uint32_t U[4], M[4], D[4];
+        bb_mid(sU, offU, U);
+        bb_mid(sM, offM, M);
+        bb_mid(sD, offD, D);
+        // the columns the west / east neighbours come from: Moore -> the vertical
+        // sums U + M + D, von Neumann -> M; edge bytes from the neighbouring lanes
+        uint32_t E[6];
+        if (p.moore) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) E[j + 1] = U[j] + M[j] + D[j];  // bytes <= 3
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) E[j + 1] = M[j];
+        }
+        E[0] = __shfl_up_sync(0xFFFFFFFFu, E[4], 1);
+        E[5] = __shfl_down_sync(0xFFFFFFFFu, E[1], 1);
+        if (lane == 0) {
+            uint32_t v = sM[offM - 1];
+            if (p.moore) v += sU[offU - 1] + sD[offD - 1];
+            E[0] = v << 24;
+        }
+        if (lane == 31) {
+            uint32_t v = sM[offM + 16];
+            if (p.moore) v += sU[offU + 16] + sD[offD + 16];
+            E[5] = v;
+        }
         const int64_t c = sty + xs + 16 * (int64_t)t;
-        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16((y + 1) * n);
-        const int64_t x0 = sty + xs + (int64_t)(t & ~31) * 16 - y * n;
-        const bool live = x0 < 0 || bb_run_live(p, cc, x0, y);
-        if (!live) continue;  // warp-uniform: 512 bytes of holes stay 0
-        const uint8_t* sU = sm + ((y - 1 + NS) % NS) * W;
-        const uint8_t* sM = sm + ((y + NS) % NS) * W;
-        const uint8_t* sD = sm + ((y + 1) % NS) * W;
-        const uint32_t offM = 32 + 16 * t;
-        const uint32_t offU = (uint32_t)(sty - n - bb_floor16((y - 1) * n)) + offM;
-        const uint32_t offD = (uint32_t)(sty + n - bb_floor16((y + 1) * n)) + offM;
-        uint32_t U[6], M[6], D[6];
-        bb_window(sU, offU, lane, U);
-        bb_window(sM, offM, lane, M);
-        bb_window(sD, offD, lane, D);
+        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
         if (c >= end) continue;
-        const uint32_t mem = bb_chunk_member(p, lt, cc, c, y);
+        // membership (fast path: the whole chunk in row y)
+        const int64_t xc = c - yn;
+        uint32_t mem;
+        if (xc >= 0) mem = bb_member16(p, lt, cc, (uint32_t)xc, (uint32_t)y);
+        else mem = bb_chunk_member(p, lt, cc, c, y);
         if (mem == 0u) continue;
-        // column edges: byte b1 has x = 0 (no west neighbours), byte b1 - 1 / b2 - 1
-        // has x = n - 1 (no east neighbours)
-        const int64_t b1 = y * n - c, b2 = b1 + n;
+        // column edges inside the chunk: x = 0 at byte -xc (row y) and n - xc (row
+        // y + 1); x = n - 1 one byte before each
+        const int64_t b2 = n - xc;
+        const bool edge = (uint64_t)(-xc) <= 16u || (uint64_t)b2 <= 16u;
         uint32_t out[4];
 #pragma unroll
         for (int j = 1; j <= 4; ++j) {
-            const uint32_t wm = bb_byte_mask(b1, j - 1) | bb_byte_mask(b2, j - 1);
-            const uint32_t em = bb_byte_mask(b1 - 1, j - 1) | bb_byte_mask(b2 - 1, j - 1);
-            const uint32_t mw = __funnelshift_l(M[j - 1], M[j], 8), me = __funnelshift_r(M[j], M[j + 1], 8);
-            uint32_t west = mw, east = me;
-            if (p.moore) {
-                west += __funnelshift_l(U[j - 1], U[j], 8) + __funnelshift_l(D[j - 1], D[j], 8);
-                east += __funnelshift_r(U[j], U[j + 1], 8) + __funnelshift_r(D[j], D[j + 1], 8);
+            uint32_t w = __funnelshift_l(E[j - 1], E[j], 8), e = __funnelshift_r(E[j], E[j + 1], 8);
+            if (edge) {
+                const int ib1 = (int)(-xc), ib2 = (int)b2;
+                w &= ~(bb_byte_mask(ib1, j - 1) | bb_byte_mask(ib2, j - 1));
+                e &= ~(bb_byte_mask(ib1 - 1, j - 1) | bb_byte_mask(ib2 - 1, j - 1));
             }
-            const uint32_t cnt = U[j] + D[j] + (west & ~wm) + (east & ~em);
-            const uint32_t r = bb_rule<CONWAY>(cnt, M[j], tb_lo, tb_hi, ts_lo, ts_hi, b8, s8);
+            const uint32_t cnt = p.moore ? w + E[j] + e - M[j - 1] : U[j - 1] + D[j - 1] + w + e;
+            const uint32_t r = bb_rule<CONWAY>(cnt, M[j - 1], tb_lo, tb_hi, ts_lo, ts_hi, b8, s8);
             out[j - 1] = r & bb_spread4(mem >> (4 * (j - 1)));
         }
         *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
