@@ -36,11 +36,11 @@ namespace nbbgpu {
 struct BBRowParams {
     uint64_t n;         // side s^r (>= 32)
     uint64_t alloc;     // bytes readable at the buffer (n^2 + pad)
-    uint64_t magicS;    // floor(2^64 / S) + 1: x / S = umulhi(x, magicS) for x < 2^32
+    uint32_t magic;     // floor(2^32 / S) + 1: x / S = umulhi(x, magic) for x < 2^32 / S
     uint32_t S;         // low-table side s^m
     uint32_t CW;        // coarse side n / S
     uint32_t lt_words;  // words per doubled low-table row
-    uint32_t cps;       // chunks per strip (= threads per CTA, multiple of 32)
+    uint32_t cps;       // chunks per strip (2 per thread, multiple of 64, <= 256)
     uint32_t rows;      // rows per CTA (band height)
     uint32_t birth, survive;
     int moore;
@@ -81,6 +81,8 @@ struct BBCoarse {
     uint32_t cy0, cx0, cx1, wpr, last;
 };
 
+__device__ __forceinline__ uint32_t bb_div(const BBRowParams& p, uint32_t x) { return __umulhi(x, p.magic); }
+
 __device__ __forceinline__ bool bb_coarse_bit(const BBCoarse& c, uint32_t cx, uint32_t cy) {
     const uint32_t ry = cy - c.cy0;
     if (cx >= c.cx0 && cx <= c.cx1) {
@@ -90,50 +92,42 @@ __device__ __forceinline__ bool bb_coarse_bit(const BBCoarse& c, uint32_t cx, ui
     return (c.last >> ry) & 1u;
 }
 
-// membership bits of cells (x .. x+15, y), 0 <= x, y < n; bits at x' >= n are 0
-__device__ __forceinline__ uint32_t bb_member16(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
-                                                uint32_t x, uint32_t y) {
-    const uint32_t cx = (uint32_t)__umul64hi((uint64_t)x, p.magicS);
-    const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
+// membership bits of cells (x .. x+NB-1, y), NB = 16 or 32, 0 <= x, y < n; bits at
+// x' >= n are 0.  S >= 32 > NB: the run meets at most two coarse cells.
+template <int NB>
+__device__ __forceinline__ uint32_t bb_member(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
+                                              uint32_t x, uint32_t y) {
+    const uint32_t cx = bb_div(p, x), cy = bb_div(p, y);
     const uint32_t xl = x - cx * p.S, yl = y - cy * p.S;
     const uint32_t* row = lt + yl * p.lt_words;
     const uint32_t w = xl >> 5;
-    uint32_t bits = __funnelshift_r(row[w], row[w + 1], xl & 31) & 0xFFFFu;  // doubled row: no wrap
+    constexpr uint32_t ALL = NB == 32 ? 0xFFFFFFFFu : (1u << NB) - 1u;
+    uint32_t bits = __funnelshift_r(row[w], row[w + 1], xl & 31) & ALL;  // doubled row: no wrap
     const uint32_t split = p.S - xl;  // bits >= split lie in coarse cell cx + 1
-    uint32_t keep = bb_coarse_bit(cc, cx, cy) ? 0xFFFFu : 0u;
-    if (split < 16) {
+    uint32_t keep = bb_coarse_bit(cc, cx, cy) ? ALL : 0u;
+    if (split < (uint32_t)NB) {
         const uint32_t lo = (1u << split) - 1u;
         const bool c1 = cx + 1 < p.CW && bb_coarse_bit(cc, cx + 1, cy);
-        keep = (keep & lo) | (c1 ? (~lo & 0xFFFFu) : 0u);
+        keep = (keep & lo) | (c1 ? (~lo & ALL) : 0u);
     }
     bits &= keep;
     const uint64_t left = p.n - x;
-    if (left < 16) bits &= (1u << left) - 1u;
+    if (left < (uint64_t)NB) bits &= (1u << left) - 1u;
     return bits;
 }
 
-// membership of the 16 bytes of the chunk at linear c (first byte in row y or y-1)
-__device__ __forceinline__ uint32_t bb_chunk_member(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
-                                                    int64_t c, int64_t y) {
-    const int64_t b1 = y * (int64_t)p.n - c;  // row y starts at byte b1 of the chunk
-    if (b1 > 0)
-        return (bb_member16(p, lt, cc, (uint32_t)(p.n - b1), (uint32_t)(y - 1)) & ((1u << b1) - 1u)) |
-               ((bb_member16(p, lt, cc, 0u, (uint32_t)y) << b1) & 0xFFFFu);
-    return bb_member16(p, lt, cc, (uint32_t)(-b1), (uint32_t)y);
-}
-
-// does row y hold a fractal cell in [x0, x0 + 512)?  (coarse test, x0 >= 0; a
+// does row y hold a fractal cell in [x0, x0 + 1024)?  (coarse test, x0 >= 0; a
 // conservative "yes" when the range reaches past the row)
 __device__ __forceinline__ bool bb_run_live(const BBRowParams& p, const BBCoarse& cc, int64_t x0, int64_t y) {
-    if (x0 + 512 > (int64_t)p.n) return true;
-    const uint32_t cy = (uint32_t)__umul64hi((uint64_t)y, p.magicS);
-    const uint32_t cx0 = (uint32_t)__umul64hi((uint64_t)x0, p.magicS);
-    const uint32_t cx1 = (uint32_t)__umul64hi((uint64_t)(x0 + 511), p.magicS);  // <= cx0 + 16
+    if (x0 + 1024 > (int64_t)p.n) return true;
+    const uint32_t cy = bb_div(p, (uint32_t)y);
+    const uint32_t cx0 = bb_div(p, (uint32_t)x0), cx1 = bb_div(p, (uint32_t)x0 + 1023u);  // <= cx0 + 33
     const uint32_t b0 = cx0 - cc.cx0, nb = cx1 - cx0 + 1;
     const uint32_t* row = cc.bits + (cy - cc.cy0) * cc.wpr;
-    const uint32_t w = b0 >> 5;
-    const uint32_t bits = __funnelshift_r(row[w], row[w + 1], b0 & 31);
-    return (bits & ((1u << nb) - 1u)) != 0u;  // nb <= 18
+    const uint32_t w = b0 >> 5, sh = b0 & 31;
+    const uint64_t lo = (uint64_t)row[w] | ((uint64_t)row[w + 1] << 32);
+    const uint64_t v = sh ? (lo >> sh) | ((uint64_t)row[w + 2] << (64 - sh)) : lo;
+    return (v & ((1ull << nb) - 1ull)) != 0ull;
 }
 
 __device__ __forceinline__ void bb_cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
@@ -145,51 +139,49 @@ __device__ __forceinline__ void bb_cp_wait() { asm volatile("cp.async.wait_group
 
 __device__ __forceinline__ int64_t bb_floor16(int64_t v) { return v & ~(int64_t)15; }
 
-// 16 bytes at byte offset o (0..15, warp-uniform) of the 32 bytes a|b
-__device__ __forceinline__ void bb_extract(const uint4 a, const uint4 b, uint32_t o, uint32_t out[4]) {
-    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+// the 32 bytes [off, off + 32) of a ring slot; off & 15 is warp-uniform
+__device__ __forceinline__ void bb_mid32(const uint8_t* slot, uint32_t off, uint32_t m[8]) {
+    const uint32_t a = off & ~15u, o = off & 15u;
+    const uint4 v0 = *reinterpret_cast<const uint4*>(slot + a);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(slot + a + 16);
+    if (o == 0u) {
+        m[0] = v0.x; m[1] = v0.y; m[2] = v0.z; m[3] = v0.w;
+        m[4] = v1.x; m[5] = v1.y; m[6] = v1.z; m[7] = v1.w;
+        return;
+    }
+    const uint4 v2 = *reinterpret_cast<const uint4*>(slot + a + 32);
+    const uint32_t v[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
     const uint32_t sh = 8u * (o & 3u);
     switch (o >> 2) {  // uniform across the warp: no divergence, static register indices
     case 0:
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j], v[j + 1], sh);
+        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j], v[j + 1], sh);
         break;
     case 1:
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 1], v[j + 2], sh);
+        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 1], v[j + 2], sh);
         break;
     case 2:
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 2], v[j + 3], sh);
+        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 2], v[j + 3], sh);
         break;
     default:
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out[j] = __funnelshift_r(v[j + 3], v[j + 4], sh);
+        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 3], v[j + 4], sh);
         break;
     }
 }
 
-// the 16 bytes [off, off + 16) of a ring slot (off & 15 is warp-uniform)
-__device__ __forceinline__ void bb_mid(const uint8_t* slot, uint32_t off, uint32_t m[4]) {
-    const uint32_t a = off & ~15u;
-    const uint4 va = *reinterpret_cast<const uint4*>(slot + a);
-    if ((off & 15u) == 0u) {
-        m[0] = va.x; m[1] = va.y; m[2] = va.z; m[3] = va.w;
-    } else {
-        const uint4 vb = *reinterpret_cast<const uint4*>(slot + a + 16);
-        bb_extract(va, vb, off & 15u, m);
-    }
-}
-
-// 0xFF in byte b (0..15) of a 16-byte chunk, as word j
+// 0xFF in byte b (0..31) of a 32-byte pair, as word j
 __device__ __forceinline__ uint32_t bb_byte_mask(int b, int j) {
-    return ((unsigned)b < 16u && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
+    return ((unsigned)b < 32u && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
 }
 
 // shared-memory layout of step_bb_rows_kernel: NS ring slots, the low table, the
-// coarse cache (at most kBBCacheWords words)
+// coarse cache (kBBCacheWords), the live flags [NS][warps], two mask rows
 constexpr uint32_t kBBCacheWords = 64;
 constexpr int kBBStages = 6;
+constexpr int kBBMaxThreads = 128;
 
 // coarse rows / columns of tile (sx, band): rows y0 - 1 .. y1 + NS, x within
 // [xs - 16, xs + 16 cps + 16], plus column CW - 1
@@ -208,18 +200,20 @@ __device__ __host__ __forceinline__ void bb_tile_cover(const BBRowParams& p, uin
 }
 
 // One CTA per live tile (strip sx of the aligned rows of band b: tiles whose output
-// bytes are all holes are left out of the list on the host).
+// bytes are all holes are left out of the list on the host); 2 chunks per thread.
 template <bool CONWAY, int NS>
-__global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles,
-                                                           const uint32_t* __restrict__ lowtab,
-                                                           const uint32_t* __restrict__ coarse,
-                                                           const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+__global__ void __launch_bounds__(kBBMaxThreads, 8)
+step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const uint32_t* __restrict__ lowtab,
+                    const uint32_t* __restrict__ coarse, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
     static_assert(NS >= 4, "rows y-1, y, y+1 plus one in flight");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t W = (p.cps + 4) * 16;  // slot bytes
+    const int TPB = blockDim.x, NW = TPB >> 5;
     uint32_t* lt = reinterpret_cast<uint32_t*>(sm + NS * W);
     uint32_t* ccw = lt + p.S * p.lt_words;
-    const int t = threadIdx.x, lane = t & 31;
+    uint32_t* mrow = ccw + kBBCacheWords;                         // [2][TPB + 2]
+    uint8_t* flags = reinterpret_cast<uint8_t*>(mrow + 2 * (TPB + 2));  // [NS][NW]
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t n = (int64_t)p.n;
     const uint2 tile = tiles[blockIdx.x];
     const int64_t y0 = (int64_t)tile.y * p.rows;
@@ -228,13 +222,14 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
     BBCoarse cc;
     uint32_t cy1;
     bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
-    cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 1;
+    cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 2;
     cc.bits = ccw;
     cc.last = 0;
-    for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry)
-        cc.last |= (uint32_t)((__ldg(coarse + (((uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1) >> 5)) >>
-                               ((((uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1)) & 31)) & 1u) << ry;
-    for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += blockDim.x) {
+    for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry) {
+        const uint64_t b = (uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1;
+        cc.last |= ((__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u) << ry;
+    }
+    for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += TPB) {
         const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
         const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
         const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
@@ -246,7 +241,7 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
         }
         ccw[i] = v;
     }
-    for (uint32_t i = t; i < p.S * p.lt_words; i += blockDim.x) lt[i] = __ldg(lowtab + i);
+    for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
     __syncthreads();
 
     // rule tables (bytes 0/1) for counts 0..7 and the count-8 entries
@@ -260,23 +255,36 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
     }
     const uint32_t b8 = ((p.birth >> 8) & 1u) * 0x01010101u, s8 = ((p.survive >> 8) & 1u) * 0x01010101u;
 
-    // row rho of the band (-1 .. n) -> slot (rho + 1) % NS (rho >= -1); thread t
-    // loads chunk t + 2 of the segment, threads 0..3 also the margin chunks 0, 1,
-    // cps+2, cps+3.  A warp whose own 32 chunks are holes zero-fills them instead.
-    const int64_t wx = xs + (int64_t)(t & ~31) * 16;  // the warp's first chunk, relative to floor16(rho n)
+    // row rho (-1 .. n) -> the next ring slot; thread t loads chunks 2t+2, 2t+3 of
+    // the segment, threads 0..3 also the margin chunks 0, 1, cps+2, cps+3.  A warp
+    // whose own 64 chunks are holes zero-fills them instead and flags the slot.
+    const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
     auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
         uint8_t* slot = sm + sl * W;
         const int64_t base = bb_floor16(rn) + xs - 32;
         const int64_t x0 = bb_floor16(rn) + wx - rn;
         const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
+        if (lane == 0) flags[sl * NW + warp] = live;
         auto one = [&](uint32_t ch, bool want) {
             const int64_t a = base + 16 * (int64_t)ch;
             const bool in = want && a >= 0 && a + 16 <= (int64_t)p.alloc;
             if (in) bb_cp_async16((uint32_t)__cvta_generic_to_shared(slot + 16 * ch), src + a, 16);
             else *reinterpret_cast<uint4*>(slot + 16 * ch) = make_uint4(0, 0, 0, 0);
         };
-        one((uint32_t)t + 2, live);
+        one(2 * (uint32_t)t + 2, live);
+        one(2 * (uint32_t)t + 3, live);
         if (t < 4) one(t < 2 ? (uint32_t)t : p.cps + (uint32_t)t, true);
+    };
+    // membership bits of row y for x in [xs - 16 + 32k, +32), k = 0 .. TPB
+    auto mask_row = [&](int64_t y, uint32_t* m) {
+        if (y >= y1) return;
+        for (int k = t; k <= TPB; k += TPB) {
+            const int64_t x0 = xs - 16 + 32 * (int64_t)k;
+            uint32_t v = 0;
+            if (x0 < 0) v = bb_member<32>(p, lt, cc, 0u, (uint32_t)y) << 16;  // strip 0: x0 = -16
+            else if (x0 < n) v = bb_member<32>(p, lt, cc, (uint32_t)x0, (uint32_t)y);
+            m[k] = v;
+        }
     };
 
     int sl_load = 0;  // slot of row y0 - 1 (rows map to slots in order)
@@ -288,80 +296,93 @@ __global__ void __launch_bounds__(256) step_bb_rows_kernel(const BBRowParams p, 
             bb_cp_commit();
         }
     }
-    int slU = 0;                       // slot of row y - 1
-    int64_t yn = y0 * n;               // y * n
+    mask_row(y0, mrow);
+    int slU = 0;  // slot of row y - 1
+    int64_t yn = y0 * n;
     int64_t rn_load = (y0 + NS - 2) * n;
-    const uint32_t offM = 32 + 16 * t;
+    const uint32_t offM = 32 + 32 * t;
     for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
         bb_cp_wait<NS - 4>();  // rows <= y + 1 landed (this thread's copies)
-        __syncthreads();       // ... everyone's; slot of row y - 2 is free
+        __syncthreads();       // ... everyone's; slot of row y - 2 and mask row y - 1 are free
         load_row(y + NS - 2, rn_load, sl_load);
         sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
         bb_cp_commit();
+        const int par = (int)((y - y0) & 1);
+        mask_row(y + 1, mrow + (par ^ 1) * (TPB + 2));
 
         const int slM = slU + 1 == NS ? 0 : slU + 1, slD = slM + 1 == NS ? 0 : slM + 1;
         const uint8_t* sU = sm + slU * W;
         const uint8_t* sM = sm + slM * W;
         const uint8_t* sD = sm + slD * W;
         slU = slM;
+        if (!flags[slM * NW + warp]) continue;  // warp-uniform: 1024 bytes of holes stay 0
         const int64_t sty = bb_floor16(yn);
-        const int64_t x0 = sty + wx - yn;  // warp's first byte, as x of row y (< 0: straddles)
-        if (x0 >= 0 && !bb_run_live(p, cc, x0, y)) continue;  // warp-uniform: 512 bytes of holes
+        const int d = (int)(sty - yn);  // -15 .. 0
         const uint32_t offU = (uint32_t)(sty - n - bb_floor16(yn - n)) + offM;
         const uint32_t offD = (uint32_t)(sty + n - bb_floor16(yn + n)) + offM;
-        uint32_t U[4], M[4], D[4];
-        bb_mid(sU, offU, U);
-        bb_mid(sM, offM, M);
-        bb_mid(sD, offD, D);
-        // the columns the west / east neighbours come from: Moore -> the vertical
-        // sums U + M + D, von Neumann -> M; edge bytes from the neighbouring lanes
-        uint32_t E[6];
+        const uint32_t* mr = mrow + par * (TPB + 2);
+        uint32_t mem = __funnelshift_r(mr[t], mr[t + 1], (uint32_t)(16 + d));
+        const int64_t c = sty + xs + 32 * (int64_t)t;
+        const int64_t xc = c - yn;  // x of the pair's first byte in row y (< 0: straddles)
+        if (xc < 0)  // strip 0, thread 0: the first -xc bytes end row y - 1
+            mem |= bb_member<16>(p, lt, cc, (uint32_t)(n + xc), (uint32_t)(y - 1)) & ((1u << (-xc)) - 1u);
+        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
+        if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
+        uint32_t U[8], M[8], D[8];
+        bb_mid32(sM, offM, M);
+        uint32_t E[10];
         if (p.moore) {
+            bb_mid32(sU, offU, U);
+            bb_mid32(sD, offD, D);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[j + 1] = U[j] + M[j] + D[j];  // bytes <= 3
+            for (int j = 0; j < 8; ++j) E[j + 1] = U[j] + M[j] + D[j];  // bytes <= 3
         } else {
+            bb_mid32(sU, offU, U);
+            bb_mid32(sD, offD, D);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[j + 1] = M[j];
+            for (int j = 0; j < 8; ++j) E[j + 1] = M[j];
         }
-        E[0] = __shfl_up_sync(0xFFFFFFFFu, E[4], 1);
-        E[5] = __shfl_down_sync(0xFFFFFFFFu, E[1], 1);
+        // the columns west / east neighbours come from (Moore: vertical sums,
+        // von Neumann: M); the pair's edge bytes from the neighbouring lanes
+        E[0] = __shfl_up_sync(0xFFFFFFFFu, E[8], 1);
+        E[9] = __shfl_down_sync(0xFFFFFFFFu, E[1], 1);
         if (lane == 0) {
             uint32_t v = sM[offM - 1];
             if (p.moore) v += sU[offU - 1] + sD[offD - 1];
             E[0] = v << 24;
         }
         if (lane == 31) {
-            uint32_t v = sM[offM + 16];
-            if (p.moore) v += sU[offU + 16] + sD[offD + 16];
-            E[5] = v;
+            uint32_t v = sM[offM + 32];
+            if (p.moore) v += sU[offU + 32] + sD[offD + 32];
+            E[9] = v;
         }
-        const int64_t c = sty + xs + 16 * (int64_t)t;
-        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
-        if (c >= end) continue;
-        // membership (fast path: the whole chunk in row y)
-        const int64_t xc = c - yn;
-        uint32_t mem;
-        if (xc >= 0) mem = bb_member16(p, lt, cc, (uint32_t)xc, (uint32_t)y);
-        else mem = bb_chunk_member(p, lt, cc, c, y);
         if (mem == 0u) continue;
-        // column edges inside the chunk: x = 0 at byte -xc (row y) and n - xc (row
+        // column edges inside the pair: x = 0 at byte -xc (row y) and n - xc (row
         // y + 1); x = n - 1 one byte before each
         const int64_t b2 = n - xc;
-        const bool edge = (uint64_t)(-xc) <= 16u || (uint64_t)b2 <= 16u;
-        uint32_t out[4];
+        const bool edge = (uint64_t)(-xc) <= 32u || (uint64_t)b2 <= 32u;
+        uint32_t wm[8], em[8];
 #pragma unroll
-        for (int j = 1; j <= 4; ++j) {
-            uint32_t w = __funnelshift_l(E[j - 1], E[j], 8), e = __funnelshift_r(E[j], E[j + 1], 8);
-            if (edge) {
-                const int ib1 = (int)(-xc), ib2 = (int)b2;
-                w &= ~(bb_byte_mask(ib1, j - 1) | bb_byte_mask(ib2, j - 1));
-                e &= ~(bb_byte_mask(ib1 - 1, j - 1) | bb_byte_mask(ib2 - 1, j - 1));
+        for (int j = 0; j < 8; ++j) wm[j] = em[j] = 0u;
+        if (edge) {
+            const int ib1 = (int)(-xc), ib2 = (int)b2;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                wm[j] = bb_byte_mask(ib1, j) | bb_byte_mask(ib2, j);
+                em[j] = bb_byte_mask(ib1 - 1, j) | bb_byte_mask(ib2 - 1, j);
             }
+        }
+        uint32_t out[8];
+#pragma unroll
+        for (int j = 1; j <= 8; ++j) {
+            const uint32_t w = __funnelshift_l(E[j - 1], E[j], 8) & ~wm[j - 1];
+            const uint32_t e = __funnelshift_r(E[j], E[j + 1], 8) & ~em[j - 1];
             const uint32_t cnt = p.moore ? w + E[j] + e - M[j - 1] : U[j - 1] + D[j - 1] + w + e;
             const uint32_t r = bb_rule<CONWAY>(cnt, M[j - 1], tb_lo, tb_hi, ts_lo, ts_hi, b8, s8);
             out[j - 1] = r & bb_spread4(mem >> (4 * (j - 1)));
         }
-        *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+        if (mem & 0xFFFFu) *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
+        if (mem >> 16) *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(out[4], out[5], out[6], out[7]);
     }
     bb_cp_wait<0>();
 }

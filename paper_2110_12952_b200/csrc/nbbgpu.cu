@@ -616,7 +616,8 @@ void ensure_bb_tables(nbbgpu_t h) {
     p.alloc = h->cells + 64;
     p.S = (uint32_t)S;
     p.CW = (uint32_t)(n / S);
-    p.magicS = ~0ull / (uint64_t)S + 1;
+    p.magic = (uint32_t)((1ull << 32) / (uint64_t)S + 1);  // exact x / S for x < 2^32 / S
+    if ((uint64_t)n * (uint64_t)S >= (1ull << 32)) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "bounding box too large");
     p.lt_words = (uint32_t)((2 * S + 31) / 32 + 1);
     // low table: row yl, bit xl (0 <= xl < 2S) = the low m digit pairs of
     // (xl mod S, yl) are replica positions
@@ -641,8 +642,8 @@ void ensure_bb_tables(nbbgpu_t h) {
     CK(cudaGetLastError());
     // strips: chunks per aligned row <= (n + 30) / 16 + 1, at most 256 per CTA
     const uint64_t maxch = ((uint64_t)n + 30) / 16 + 2;
-    const uint64_t nsx = (maxch + 255) / 256;
-    p.cps = (uint32_t)(((maxch + nsx - 1) / nsx + 31) / 32 * 32);
+    const uint64_t nsx = (maxch + 2 * kBBMaxThreads - 1) / (2 * kBBMaxThreads);
+    p.cps = (uint32_t)(((maxch + nsx - 1) / nsx + 63) / 64 * 64);  // 2 chunks per thread, whole warps
     uint64_t rows = 64;
     while (rows > 8 && nsx * (((uint64_t)n + rows - 1) / rows) < 4ull * 148) rows /= 2;
     p.rows = (uint32_t)rows;
@@ -675,13 +676,15 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.moore = moore;
     if (h->bb_ntiles == 0) return;
     const dim3 grid(h->bb_ntiles);
-    const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4;
+    const uint32_t tpb = p.cps / 2;
+    const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4 +
+                        2 * (tpb + 2) * 4 + kBBStages * (tpb / 32);
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
     if (conway)
-        step_bb_rows_kernel<true, kBBStages><<<grid, p.cps, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+        step_bb_rows_kernel<true, kBBStages><<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
     else
-        step_bb_rows_kernel<false, kBBStages><<<grid, p.cps, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+        step_bb_rows_kernel<false, kBBStages><<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
