@@ -211,7 +211,7 @@ def test_packed_chunked_conversions(monkeypatch):
 
 def test_large_levels_hash(golden, golden_long):
     cases = [t for t in golden["traces"] if t["level"] >= 13]
-    for key in ("t16", "c9", "t18", "h10", "y8", "t20"):
+    for key in ("t16", "c9", "t18", "h10", "y8", "h11", "y9", "t20"):
         if key in golden_long:
             cases.append(golden_long[key])
     for t in cases:

@@ -19,6 +19,8 @@ DESCS = {
     "H": FractalDescriptor("h-fractal", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)]),
     "Y": FractalDescriptor("candy", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
                                             (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)]),
+    # a descriptor with no compile-time wiring (generic transition-table program)
+    "K": FractalDescriptor("k6s3", 6, 3, [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 2)]),
 }
 
 
