@@ -158,6 +158,22 @@ int nbbgpu_set_map_variant(nbbgpu_t h, int variant);
 /* The kernel the next step will launch (resolves AUTO) and its tile level q. */
 int nbbgpu_active_kernel(nbbgpu_t h, int* kernel, int* tile_level);
 
+/* The packed kernel's program: NBBGPU_PROGRAM_TABLE (table-driven step_packed_kernel),
+ * _BUILTIN (micro-block wiring compiled in for the triangle, carpet, Vicsek, H and
+ * candy descriptors), _JIT (micro-block wiring of this descriptor, compiled at run
+ * time by NVRTC), _NONE (the next step is not a packed kernel); block_level = the
+ * micro-block level P.  Replaces no reference entity (the reference has one program). */
+#define NBBGPU_PROGRAM_NONE 0
+#define NBBGPU_PROGRAM_TABLE 1
+#define NBBGPU_PROGRAM_BUILTIN 2
+#define NBBGPU_PROGRAM_JIT 3
+int nbbgpu_packed_program(nbbgpu_t h, int* program, int* block_level);
+/* Host only (no GPU): plan the descriptor's packed layout and, when it uses a run-time
+ * specialised micro-block kernel, compile it for sm_100a with NVRTC; name receives the
+ * kernel's lowered name.  OUT_OF_DOMAIN when the plan has no run-time kernel. */
+int nbbgpu_jit_compile_check(const int32_t* replicas_xy, int k, int s, int level, int moore, char* name,
+                             uint64_t name_bytes);
+
 /* The handle's CUDA stream (cudaStream_t) for external event timing. */
 int nbbgpu_stream(nbbgpu_t h, void** stream);
 

@@ -46,6 +46,9 @@ SIGNATURES = {
     "nbbgpu_set_map_variant": (C.c_int, [_H, C.c_int]),
     "nbbgpu_active_kernel": (C.c_int, [_H, _P(C.c_int), _P(C.c_int)]),
     "nbbgpu_stream": (C.c_int, [_H, _P(C.c_void_p)]),
+    "nbbgpu_packed_program": (C.c_int, [_H, _P(C.c_int), _P(C.c_int)]),
+    "nbbgpu_jit_compile_check": (C.c_int, [_P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                           C.c_uint64]),
     "nbbgpu_lambda_batch": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_float)]),
     "nbbgpu_nu_batch": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_float)]),
     "nbbgpu_partition": (C.c_int, [_H, C.c_int, C.c_int]),

@@ -15,8 +15,7 @@
 // embedded (sum_mu gx[d_mu] s^mu, sum_mu gy[d_mu] s^mu).
 #pragma once
 
-#include <cstdint>
-#include <utility>
+#include "rtc_compat.cuh"
 
 namespace nbbgpu {
 
@@ -71,30 +70,37 @@ struct WiringData {
     int epx[kMaxExt] = {}, epy[kMaxExt] = {};  // external positions (box-relative)
 };
 
-template <class FT, int P>
-constexpr WiringData<WiringGeom<FT, P>::NB> make_wiring() {
-    using G = WiringGeom<FT, P>;
-    constexpr int NB = G::NB, BW = G::BW, K = G::K, S = G::S, SP = G::SP;
+// The wiring of a level-P micro-block of the descriptor (K, S, GX, GY): the same
+// function runs at compile time for the built-in tags and for run-time specialised
+// (jit.inc) tags, and on the host for the block tables of the latter.  nb = BW * BH
+// cells are used of the NB-sized arrays.
+template <int NB>
+constexpr WiringData<NB> make_wiring_from(int K, int S, const int* GX, const int* GY, int P) {
+    int BW = 1, BH = 1, SP = 1;
+    for (int i = 0; i < (P + 1) / 2; ++i) BW *= K;
+    for (int i = 0; i < P / 2; ++i) BH *= K;
+    for (int i = 0; i < P; ++i) SP *= S;
+    const int nb = BW * BH;
     WiringData<NB> d{};
-    for (int n = 0; n < NB; ++n) {
+    for (int n = 0; n < nb; ++n) {
         int cx = n % BW, cy = n / BW, x = 0, y = 0, sp = 1;
         for (int mu = 0; mu < P; ++mu) {
             int dg = 0;
             if ((mu & 1) == 0) { dg = cx % K; cx /= K; }
             else { dg = cy % K; cy /= K; }
-            x += FT::GX[dg] * sp;
-            y += FT::GY[dg] * sp;
+            x += GX[dg] * sp;
+            y += GY[dg] * sp;
             sp *= S;
         }
         d.ex[n] = x;
         d.ey[n] = y;
     }
-    for (int n = 0; n < NB; ++n)
+    for (int n = 0; n < nb; ++n)
         for (int j = 0; j < 8; ++j) {
             const int X = d.ex[n] + kDX[j], Y = d.ey[n] + kDY[j];
             if (X >= 0 && Y >= 0 && X < SP && Y < SP) {
                 int hit = kWireAbsent;
-                for (int m = 0; m < NB; ++m)
+                for (int m = 0; m < nb; ++m)
                     if (d.ex[m] == X && d.ey[m] == Y) hit = m;
                 d.src[n][j] = hit;
             } else {
@@ -102,6 +108,7 @@ constexpr WiringData<WiringGeom<FT, P>::NB> make_wiring() {
                 for (int m = 0; m < d.NE; ++m)
                     if (d.epx[m] == X && d.epy[m] == Y) e = m;
                 if (e < 0) {
+                    if (d.NE == kMaxExt) return d;  // (callers reject NE > kMaxExt - 1)
                     e = d.NE++;
                     d.epx[e] = X;
                     d.epy[e] = Y;
@@ -113,12 +120,17 @@ constexpr WiringData<WiringGeom<FT, P>::NB> make_wiring() {
 }
 
 template <class FT, int P>
+constexpr WiringData<WiringGeom<FT, P>::NB> make_wiring() {
+    return make_wiring_from<WiringGeom<FT, P>::NB>(FT::K, FT::S, FT::GX, FT::GY, P);
+}
+
+template <class FT, int P>
 struct Wiring : WiringGeom<FT, P> {
     using G = WiringGeom<FT, P>;
     static constexpr WiringData<G::NB> d = make_wiring<FT, P>();
     static constexpr int NE = d.NE;
     static constexpr int NEP = (NE + 3) & ~3;  // table entries per block (16-B rows)
-    static_assert(NE <= kMaxExt, "too many external positions");
+    static_assert(NE < kMaxExt, "too many external positions");
 };
 
 // compile-time loop: f(std::integral_constant<int, i>) for i in [0, N)

@@ -5,8 +5,7 @@
 // handles with different fractals can coexist (no __constant__ globals).
 #pragma once
 
-#include <cstdint>
-#include <cuda_runtime.h>
+#include "rtc_compat.cuh"
 
 namespace nbbgpu {
 

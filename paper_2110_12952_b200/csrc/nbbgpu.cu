@@ -298,6 +298,7 @@ int choose_tile_level(const HostFrac& F) {
 }
 
 
+#include "jit.inc"
 #include "packed_plan.inc"
 
 }  // namespace
@@ -1483,6 +1484,21 @@ int nbbgpu_active_kernel(nbbgpu_t h, int* kernel, int* tile_level) {
     });
 }
 
+int nbbgpu_packed_program(nbbgpu_t h, int* program, int* block_level) {
+    return guarded([&] {
+        if (!h) raise(NBBGPU_ERR_INVALID, "null handle");
+        int prog = NBBGPU_PROGRAM_NONE, bl = 0;
+        if (resolve_kernel(h) == NBBGPU_KERNEL_PACKED) {
+            ensure_packed_tables(h);
+            const PackedPlan& P = h->pp;
+            prog = P.tag == kTagNone ? NBBGPU_PROGRAM_TABLE : P.tag == kTagJit ? NBBGPU_PROGRAM_JIT : NBBGPU_PROGRAM_BUILTIN;
+            bl = P.tag == kTagNone ? 0 : P.bP;
+        }
+        if (program) *program = prog;
+        if (block_level) *block_level = bl;
+    });
+}
+
 int nbbgpu_stream(nbbgpu_t h, void** stream) {
     return guarded([&] {
         if (!h || !stream) raise(NBBGPU_ERR_INVALID, "null argument");
@@ -1516,3 +1532,21 @@ int nbbgpu_front_device_ptr(nbbgpu_t h, void** out) {
 }  // extern "C"
 
 #include "partition.inc"
+
+int nbbgpu_jit_compile_check(const int32_t* rep, int k, int s, int level, int moore, char* name, uint64_t name_bytes) {
+    return guarded([&] {
+        const HostFrac F = host_frac(rep, k, s, level);
+        const PackedPlan P = build_packed_plan(F, choose_packed_level(F));
+        if (P.tag != kTagJit) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "the packed plan of this descriptor does not use a run-time specialised kernel");
+        const JitShape j = jit_shape_for(P.bP, P.wq, P.SW, P.Cp, F.k);
+        std::vector<char> cubin;
+        std::string lowered, err;
+        if (!jit_compile(jit_source(F), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j), "sm_100a", cubin, lowered, err))
+            raise(NBBGPU_ERR_CUDA, "jit: " + err);
+        if (name && name_bytes) {
+            const std::string out = lowered + " (" + std::to_string(cubin.size()) + " B cubin)";
+            std::strncpy(name, out.c_str(), (size_t)name_bytes - 1);
+            name[name_bytes - 1] = '\0';
+        }
+    });
+}

@@ -19,7 +19,7 @@
 // give the reference's byte layout (cy*w + cx) back on download.
 #pragma once
 
-#include <type_traits>
+#include "rtc_compat.cuh"
 
 #include "blocks.cuh"
 #include "naive.cuh"

@@ -159,6 +159,12 @@ class Simulation:
         _abi.check(_abi.lib().nbbgpu_active_kernel(self._h, C.byref(k), C.byref(q)))
         return {1: "naive", 2: "tiled", 3: "packed", 4: "table"}[k.value], q.value
 
+    def packed_program(self) -> Tuple[str, int]:
+        """("table" | "builtin" | "jit" | "none", micro-block level) of the packed kernel."""
+        prog, bl = C.c_int(), C.c_int()
+        _abi.check(_abi.lib().nbbgpu_packed_program(self._h, C.byref(prog), C.byref(bl)))
+        return {0: "none", 1: "table", 2: "builtin", 3: "jit"}[prog.value], bl.value
+
     def handle(self):
         return self._h
 

@@ -86,3 +86,20 @@ def test_partition_ranges_cover_array():
             assert lo.value == prev
             prev = hi.value
         assert prev == 3 ** r
+
+
+def test_jit_compiles_custom_descriptor_kernels():
+    # a descriptor without built-in wiring gets the ws3 micro-block kernel compiled
+    # for it at run time (NVRTC, no GPU needed); built-in descriptors do not
+    L = _abi.lib()
+    buf = C.create_string_buffer(512)
+    custom = [((6, 3), [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 2)], 12),
+              ((4, 3), [(0, 0), (2, 0), (1, 1), (0, 2)], 10),
+              ((10, 4), [(0, 0), (1, 0), (2, 0), (3, 0), (0, 1), (3, 1), (0, 2), (1, 3), (2, 3), (3, 3)], 7)]
+    for (k, s), reps, level in custom:
+        rc = L.nbbgpu_jit_compile_check(_abi.replica_array(reps), k, s, level, 1, buf, 512)
+        assert rc == 0, L.nbbgpu_last_error()
+        assert b"step_packed_ws3_kernel" in buf.value and b"JitTag" in buf.value
+    T = builtin_descriptor("sierpinski-triangle")
+    rc = L.nbbgpu_jit_compile_check(_abi.replica_array(T.replicas), 3, 2, 12, 1, buf, 512)
+    assert rc == 3 and b"run-time" in L.nbbgpu_last_error()

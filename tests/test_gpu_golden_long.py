@@ -68,3 +68,19 @@ def test_paper_per_cell_kernel_t16(golden_long, maps):
     # tensor cores (mma.sync u8), the paper's one-thread-per-cell kernel
     checked, kern = _walk(golden_long["t16"], kernel="naive", maps=maps, upto=10)
     assert kern[0] == "naive" and checked == [0, 1, 3, 10]
+
+
+@pytest.mark.parametrize("key", ["c9", "t18", "h10", "y8", "h11", "y9", "t20"])
+def test_run_time_specialised_kernel(golden_long, key, monkeypatch):
+    # the descriptor's micro-block wiring compiled at run time (jit.inc) -- the path
+    # every custom descriptor takes -- forced onto the BASELINE configs
+    if key not in golden_long:
+        pytest.skip(f"{key} not in golden_long.json")
+    monkeypatch.setenv("NBBGPU_JIT_FORCE", "1")
+    t = golden_long[key]
+    sim = Simulation(desc_from_trace(t), t["level"], Backend.GpuCompact,
+                     SimOptions(kernel="packed", memory_cap=1 << 42))
+    assert sim.packed_program()[0] == "jit"
+    sim.close()
+    checked, kern = _walk(t, kernel="packed")
+    assert len(checked) >= 2
