@@ -1538,7 +1538,7 @@ int nbbgpu_jit_compile_check(const int32_t* rep, int k, int s, int level, int mo
         const HostFrac F = host_frac(rep, k, s, level);
         const PackedPlan P = build_packed_plan(F, choose_packed_level(F));
         if (P.tag != kTagJit) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "the packed plan of this descriptor does not use a run-time specialised kernel");
-        const JitShape j = jit_shape_for(P.bP, P.wq, P.SW, P.Cp, F.k);
+        const JitShape j = jit_shape_for(P.bP, P.wq, P.split == 2 ? P.SWsplit : P.SW, P.Cp, F.k, P.split);
         std::vector<char> cubin;
         std::string lowered, err;
         if (!jit_compile(jit_source(F), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j), "sm_100a", cubin, lowered, err))
