@@ -18,8 +18,7 @@ SO = os.path.join(HERE, "libnbbgpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["nbbgpu.cu"]
-DEPS = ["common.cuh", "naive.cuh", "tiled.cuh", "maps.cuh", "bb.cuh", "blocks.cuh", "packed.cuh", "layouts.cuh",
-        "partition.inc", "packed_plan.inc", "packed_host.inc", "nbbgpu.cu"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".inc")))
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
