@@ -390,7 +390,6 @@ struct nbbgpu_sim {
     uint32_t* d_pdmask = nullptr;           // [nHc][8] direction masks per 32-slot chunk
     uint32_t* d_phent = nullptr;            // nonzero (chunk, direction) masks, 2 words each
     uint32_t n_hent = 0;
-    unsigned* d_gbar = nullptr;             // grid barrier of the fused multi-step kernel
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
     // profiling (nbbgpu_step_profiled): events around each main step kernel, launch count
@@ -822,7 +821,6 @@ void free_all(nbbgpu_t h) {
     if (h->d_pbt) cudaFree(h->d_pbt);
     if (h->d_pdmask) cudaFree(h->d_pdmask);
     if (h->d_phent) cudaFree(h->d_phent);
-    if (h->d_gbar) cudaFree(h->d_gbar);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
     if (h->d_bblow) cudaFree(h->d_bblow);
     if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);
@@ -1148,19 +1146,9 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
     try {
         if (rk == NBBGPU_KERNEL_PACKED && launch_resident(h, birth, survive, moore, nsteps)) {
             // (all steps on-chip in one single-CTA launch)
-        } else if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h) && !h->comm && !h->p2p) {
-            // every step in one cooperative launch (chunks bound the launch length)
-            for (int64_t done = 0; done < nsteps;) {
-                const int n = (int)std::min<int64_t>(nsteps - done, 1 << 20);
-                launch_steps_fused(h, birth, survive, moore, n);
-                h->cur ^= (n & 1);
-                h->iteration += n;
-                done += n;
-            }
         } else {
             for (int64_t i = 0; i < nsteps; ++i) {
-                if (rk == NBBGPU_KERNEL_PACKED && packed_fusable(h)) launch_steps_fused(h, birth, survive, moore, 1);
-                else launch_step(h, birth, survive, moore);
+                launch_step(h, birth, survive, moore);
                 h->cur ^= 1;
                 ++h->iteration;
                 if (h->p2p) p2p_push(h);             // peer-memory halo of the new front

@@ -83,9 +83,6 @@ struct PackedStepParams {
     // waiting (this and every later step) and the host raises on synchronize
     uint32_t* wait_err;
     uint64_t wait_ns;
-    // stream the group records through L2 as evict-first (TMA cache hint), so the
-    // small per-step tables (ntab, boundary planes, halo words) stay L2-resident
-    int stream_ef;
     // transposed halo gather (HMODE 5): the boundary plane transposed per 32 slots,
     // Bt[(g * nHc + k) * 32 + b] bit i = boundary word 32k + i of tile 32g + b, and
     // per chunk k and direction slot d the mask of chunk k's slots in direction d
@@ -130,8 +127,8 @@ __device__ __forceinline__ void wait_peers(const PackedStepParams& p) {
 }
 
 // Boundary-plane / halo loads: through the read-only path when the data was written
-// by an earlier launch (NC), L2-coherent (ld.global.cg) inside the fused multi-step
-// kernel, where the previous step of the same launch wrote it.
+// by an earlier launch (NC), L2-coherent (ld.global.cg) when peers store into the
+// plane over NVLink while the grid runs (p2p transport).
 template <bool NC>
 __device__ __forceinline__ uint32_t ld_bnd(const uint32_t* p) {
     if constexpr (NC) return __ldg(p);
@@ -670,32 +667,14 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar,
-                                              uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void* dst, uint32_t src, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
-                 "r"(src), "r"(bytes), "l"(pol) : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// record streams of the ws3 kernel: evict-first when p.stream_ef
-__device__ __forceinline__ void rec_g2s(const PackedStepParams& p, uint32_t dst, const void* src, uint32_t bytes,
-                                       uint32_t mbar) {
-    if (p.stream_ef) bulk_g2s_hint(dst, src, bytes, mbar, l2_evict_first_policy());
-    else bulk_g2s(dst, src, bytes, mbar);
-}
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes);
-__device__ __forceinline__ void rec_s2g(const PackedStepParams& p, void* dst, uint32_t src, uint32_t bytes) {
-    if (p.stream_ef) bulk_s2g_hint(dst, src, bytes, l2_evict_first_policy());
-    else bulk_s2g(dst, src, bytes);
+// the record streams of the ws3 kernel (an L2 evict-first hint was measured and dropped: +-2 %)
+__device__ __forceinline__ void rec_g2s(const PackedStepParams&, uint32_t dst, const void* src, uint32_t bytes,
+                                       uint32_t mbar) {
+    bulk_g2s(dst, src, bytes, mbar);
+}
+__device__ __forceinline__ void rec_s2g(const PackedStepParams&, void* dst, uint32_t src, uint32_t bytes) {
+    bulk_s2g(dst, src, bytes);
 }
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
@@ -1044,25 +1023,6 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Grid-wide barrier of a cooperative launch: arrival counter + generation word.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
 // Small levels whose whole packed state fits one SM's shared memory (triangle q=6,
 // r <= 12): ONE CTA runs all nsteps steps on-chip.  Shared memory holds both state
 // buffers in stage layout (per group: record | halo words | zero word) and, per
@@ -1236,140 +1196,6 @@ step_packed_cluster_kernel(const PackedStepParams p, const uint32_t* __restrict_
     for (uint32_t i = tid; i < nmine * p.nSrc; i += blockDim.x) {
         const uint32_t lg = i / p.nSrc, m = i - lg * p.nSrc;
         bdst[(uint64_t)(lg * NC + me) * p.nSrc + m] = F[lg * SWg + __ldg(p.srcidx + m)];
-    }
-}
-
-// All nsteps steps in ONE cooperative launch (persistent, one CTA per SM): per step
-//   phase H: every warp of the grid gathers halo words (halo_task) into H,
-//   grid barrier,
-//   phase S: the warp-specialised TMA-in / TMA-out micro-block pipeline of
-//            step_packed_ws3_kernel over this CTA's groups (ring counters run on
-//            across steps),
-//   grid barrier (records, boundary words complete), swap.
-// No launch gaps and no halo-kernel tail between steps.  Data written by earlier
-// steps of the launch is read L2-coherently (ld.global.cg / TMA), with proxy fences
-// between generic writes and async-proxy reads.
-template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO>
-__global__ void __launch_bounds__(((BlockGeom<FT, P, WQ>::NBLK + 31) / 32 * NGRP + 2) * 32, 1)
-step_packed_fused_kernel(const PackedStepParams p, uint32_t* P0, uint32_t* P1, uint32_t* B0, uint32_t* B1,
-                         int cur0, int nsteps, unsigned* gbar) {
-    using W = Wiring<FT, P>;
-    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
-    constexpr int NCHUNK = (NBLK + 31) / 32;
-    constexpr int NCW = NCHUNK * NGRP;
-    constexpr int NEP = W::NEP;
-    extern __shared__ __align__(16) uint8_t sm[];
-    const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
-    const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
-    uint8_t* st = sm + 16 * (NS + NO);
-    const uint32_t stage_bytes = p.SW * 4, rec_bytes = p.Cp * 4, halo_bytes = p.nHp * 4;
-    uint8_t* outs = st + NS * stage_bytes;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, NCHUNK);
-        }
-        for (int o = 0; o < NO; ++o) {
-            mbar_init(ofull0 + 8 * o, NCHUNK);
-            mbar_init(oempty0 + 8 * o, 1);
-        }
-        mbar_fence_init();
-    }
-    if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[p.Cp + p.nHp] = 0u;  // absent
-    for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
-        reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * rec_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
-    fence_proxy_async_smem();
-    __syncthreads();
-
-    // groups of this CTA per step; l-th of them = g0 + blockIdx.x + l * gridDim.x
-    const uint32_t ng = p.g1 - p.g0;
-    const uint32_t n_mine = blockIdx.x < ng ? (ng - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-    const uint64_t nwarps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    const uint64_t htasks = p.nH ? halo_tasks(p.nH, ng, p.nD) : 0;
-
-    uint32_t KB[9], KS[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-    }
-    const int set = warp < NCW ? warp / NCHUNK : 0, c = warp < NCW ? warp - set * NCHUNK : 0;
-    const uint32_t blk = (uint32_t)c * 32 + lane;
-    const bool active = warp < NCW && blk < (uint32_t)NBLK;
-    uint32_t toff[NEP];
-    {
-        const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
-        static_for<NEP / 4>([&](auto e4) {
-            constexpr int E = decltype(e4)::value;
-            const uint4 v = __ldg(t4 + E);
-            toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
-        });
-    }
-    uint32_t ip = 0, is = 0, ic = (uint32_t)set;  // running group counters (producer, storer, consumers)
-
-    for (int step = 0; step < nsteps; ++step) {
-        const int cur = cur0 ^ (step & 1);
-        const uint32_t* src = cur ? P1 : P0;
-        uint32_t* dst = cur ? P0 : P1;
-        const uint32_t* bsrc = cur ? B1 : B0;
-        uint32_t* bdst = cur ? B0 : B1;
-        // ---- phase H: halo words of every owned group ------------------------------
-        for (uint64_t wi = gwarp; wi < htasks; wi += nwarps_total) halo_task<false>(p, bsrc, p.halo, wi, lane);
-        fence_proxy_async_global();  // H (generic writes) is read by TMA next
-        grid_barrier(gbar);
-        // ---- phase S -----------------------------------------------------------------
-        const uint32_t i_end = (uint32_t)(step + 1) * n_mine;
-        if (warp == NCW) {  // producer
-            if (lane == 0) {
-                fence_proxy_async_global();
-                for (; ip < i_end; ++ip) {
-                    const uint32_t g = p.g0 + blockIdx.x + (ip - (uint32_t)step * n_mine) * gridDim.x;
-                    const uint32_t s = ip % NS;
-                    if (ip >= NS) mbar_wait(empty0 + 8 * s, ((ip / NS) - 1) & 1u);
-                    const uint32_t bar = full0 + 8 * s, dst_s = smem_u32(st + s * stage_bytes);
-                    mbar_expect_tx(bar, rec_bytes + halo_bytes);
-                    bulk_g2s(dst_s, src + (uint64_t)g * p.Cp, rec_bytes, bar);
-                    if (halo_bytes) bulk_g2s(dst_s + rec_bytes, p.halo + (uint64_t)g * p.nHp, halo_bytes, bar);
-                }
-            }
-        } else if (warp == NCW + 1) {  // storer
-            if (lane == 0) {
-                for (; is < i_end; ++is) {
-                    const uint32_t g = p.g0 + blockIdx.x + (is - (uint32_t)step * n_mine) * gridDim.x;
-                    const uint32_t o = is % NO;
-                    mbar_wait(ofull0 + 8 * o, (is / NO) & 1u);
-                    bulk_s2g(dst + (uint64_t)g * p.Cp, smem_u32(outs + o * rec_bytes), rec_bytes);
-                    bulk_wait_read_all();
-                    mbar_arrive(oempty0 + 8 * o);
-                }
-                bulk_wait_all();            // this step's records are in global memory
-                fence_proxy_async_global();
-            }
-        } else {  // consumers
-            for (; ic < i_end; ic += NGRP) {
-                const uint32_t g = p.g0 + blockIdx.x + (ic - (uint32_t)step * n_mine) * gridDim.x;
-                const uint32_t s = ic % NS, o = ic % NO;
-                mbar_wait(full0 + 8 * s, (ic / NS) & 1u);
-                if (ic >= NO) mbar_wait(oempty0 + 8 * o, ((ic / NO) - 1) & 1u);
-                const uint8_t* Sb = st + s * stage_bytes;
-                uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * rec_bytes);
-                const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
-                if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS);
-                if (c == 0)
-                    for (uint32_t m = lane; m < p.nSrc; m += 32)
-                        bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(empty0 + 8 * s);
-                    mbar_arrive(ofull0 + 8 * o);
-                }
-            }
-        }
-        grid_barrier(gbar);  // records + boundary words of this step complete
     }
 }
 

@@ -434,11 +434,8 @@ def test_packed_pinned_host_zero_copy():
     assert np.array_equal(sim.front().data, o.front)
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
-def test_packed_multistep_fused_and_split(monkeypatch, fuse):
-    # many steps per call: one cooperative launch with grid barriers between the
-    # halo and step phases (NBBGPU_FUSE=1), or a halo + step kernel pair per step
-    monkeypatch.setenv("NBBGPU_FUSE", fuse)
+def test_packed_multistep_calls(monkeypatch):
+    # many steps per call: a halo + step kernel pair per step (PDL-chained)
     H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
     for desc, r, q in [(T, 12, 6), (T, 13, 8), (CARPET, 5, 4), (VICSEK, 6, 4), (H, 5, 4)]:
         monkeypatch.setenv("NBBGPU_PACKED_Q", str(q))
@@ -452,7 +449,7 @@ def test_packed_multistep_fused_and_split(monkeypatch, fuse):
                 sim.step(rule, n)
                 for _ in range(n):
                     o.step(rule.birth, rule.survive, rule.moore)
-                assert np.array_equal(sim.front().data, o.front), (desc.name, r, q, n, fuse)
+                assert np.array_equal(sim.front().data, o.front), (desc.name, r, q, n)
             assert sim.iteration() == 12
             sim.close()
 
