@@ -8,7 +8,10 @@ inputs larger than L2 except where noted.  Writes one JSON object to stdout.
              maps; batched lambda/nu maps/s for both variants
   configs[2] carpet r=9, compact vs GPU BB
   configs[3] T r=20 (bench.py) + T r=18 compact vs vectorised BB (largest BB level)
-  configs[4] H-fractal r=11 (1.98e9 cells) and Candy r=8 (4.3e8) compact
+  configs[4] H-fractal r=11 (1.98e9 cells) and Candy r=9 (5.2e9) compact: built-in
+             micro-block wiring, the same wiring compiled at run time (NVRTC, the path
+             every custom descriptor takes; NBBGPU_JIT_FORCE=1), the table-driven
+             program (NBBGPU_GENERIC=1), and a custom descriptor K(n,6,3) at r=12
 """
 import json
 import os
@@ -23,6 +26,7 @@ import torch  # noqa: E402
 
 from paper_2110_12952_b200 import (Backend, SimOptions, Simulation, builtin_descriptor,  # noqa: E402
                                    conway_rule, load_descriptor)
+from paper_2110_12952_b200.descriptor import FractalDescriptor  # noqa: E402
 
 RULE = conway_rule()
 
@@ -32,18 +36,30 @@ def dev_mem_used():
     return total - free
 
 
-def run(desc, level, backend=Backend.GpuCompact, steps=10, warmup=3, kernel="auto", maps="digit"):
+def run(desc, level, backend=Backend.GpuCompact, steps=10, warmup=3, kernel="auto", maps="digit", env=None):
     torch.cuda.synchronize()
     m0 = dev_mem_used()
-    sim = Simulation(desc, level, backend, SimOptions(memory_cap=1 << 42, kernel=kernel, map_variant=maps))
+    saved = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        sim = Simulation(desc, level, backend, SimOptions(memory_cap=1 << 42, kernel=kernel, map_variant=maps))
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     sim.seed_random(42, 0.5)
     sim.step(RULE, warmup)
     ms = sim.step_timed(RULE, steps)
     m1 = dev_mem_used()
     cells = desc.k ** level
     out = {"fractal": desc.name, "level": level, "backend": backend.value,
-           "kernel": "%s q=%d" % sim.active_kernel() if backend == Backend.GpuCompact else
-           ("bb-vectorised" if desc.s in (2, 4) and desc.s ** level % 16 == 0 else "bb-naive"),
+           "kernel": ("%s q=%d" % sim.active_kernel() + (" (%s P=%d)" % sim.packed_program()
+                                                         if sim.active_kernel()[0] == "packed" else ""))
+           if backend == Backend.GpuCompact else
+           ("bb-rows (row-streaming, hole skipping)" if desc.s ** level >= 32 else "bb-naive"),
+           "env": env or {},
            "maps": maps, "steps": steps, "ms_per_step": ms / steps,
            "cell_updates_per_s": cells * steps / (ms / 1e3), "compact_cells": cells,
            "device_bytes_held": sim.peak_bytes(), "device_mem_delta": m1 - m0,
@@ -103,8 +119,15 @@ def main():
     out["config3_T_r18_vs_bb"] = [run(T, 18, steps=20), run(T, 18, steps=20, kernel="tiled"),
                                   run(T, 18, Backend.GpuBoundingBox, steps=3)]
     out["config3_T_r20"] = [run(T, 20, steps=100), run(T, 20, steps=20, kernel="tiled"), run(T, 22, steps=20)]
-    out["config4_generic"] = [run(H, 11, steps=20), run(Y, 9, steps=20), run(Y, 8, steps=20),
-                              run(H, 10, steps=20)]
+    K = FractalDescriptor("k6s3", 6, 3, [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 2)])
+    jit, gen = {"NBBGPU_JIT_FORCE": "1"}, {"NBBGPU_GENERIC": "1"}
+    out["config4_generic"] = [run(H, 11, steps=20), run(H, 11, steps=20, env=jit), run(H, 11, steps=20, env=gen),
+                              run(Y, 9, steps=20), run(Y, 9, steps=20, env=jit), run(Y, 9, steps=20, env=gen),
+                              run(K, 12, steps=20), run(K, 12, steps=20, env=gen),
+                              run(H, 10, steps=20), run(Y, 8, steps=20)]
+    out["bb_baseline"] = [run(Cp, 10, Backend.GpuBoundingBox, steps=3), run(Cp, 11, Backend.GpuBoundingBox, steps=2),
+                          run(H, 9, Backend.GpuBoundingBox, steps=5), run(Y, 7, Backend.GpuBoundingBox, steps=5),
+                          run(Cp, 10, steps=20), run(Cp, 11, steps=20)]
     print(json.dumps(out, indent=1))
 
 

@@ -1,5 +1,5 @@
 """Paper-style backend comparison tables on the GPU (bench.cpp's CSV schema):
-python tools/bench_csv.py > profiles/r1_bench_backends.csv"""
+python tools/bench_csv.py > profiles/r2_bench_backends.csv"""
 import os
 import sys
 
