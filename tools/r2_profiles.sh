@@ -19,3 +19,10 @@ timeout 900 $NCU --set full --import-source on -k regex:step_bb_rows -s 3 -c 1 -
     python tools/prof_step.py --level 16 --backend gpu-bb --steps 5 > $O/ncu_bb.log 2>&1; echo "ncu bb rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_words|bnd_transpose" -s 6 -c 3 -o $O/r2_h11 \
     python tools/prof_step.py --fractal @descriptors/h-fractal.desc --level 11 --kernel packed --steps 5 > $O/ncu_h11.log 2>&1; echo "ncu h11 rc=$?"
+# text summaries (the .ncu-rep files stay only when small: gpurun copies back <= 64 MiB)
+for r in $O/*.ncu-rep; do
+  tools/ncu_summary.sh $r > ${r%.ncu-rep}.txt 2>&1
+  ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>/dev/null
+done
+find $O -name '*.ncu-rep' -size +6M -delete
+du -sh $O; ls -la $O
