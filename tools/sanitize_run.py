@@ -32,13 +32,16 @@ CASES = {
     "carpet_pws": (C, 6, Backend.GpuCompact, "packed", {}, 1),
     "h_bt": (H, 7, Backend.GpuCompact, "packed", {}, 1),
     "candy_split": (Y, 5, Backend.GpuCompact, "packed", {}, 1),
-    "generic": (K63, 6, Backend.GpuCompact, "packed", {}, 1),
+    "jit": (K63, 6, Backend.GpuCompact, "packed", {}, 1),
+    "jit_split": (Y, 5, Backend.GpuCompact, "packed", {"NBBGPU_JIT_FORCE": "1"}, 1),
+    "generic": (K63, 6, Backend.GpuCompact, "packed", {"NBBGPU_GENERIC": "1"}, 1),
     "generic_h": (H, 6, Backend.GpuCompact, "packed", {"NBBGPU_GENERIC": "1"}, 1),
     "tiled": (T, 12, Backend.GpuCompact, "tiled", {}, 1),
     "naive": (T, 10, Backend.GpuCompact, "naive", {}, 1),
     "table": (T, 10, Backend.GpuCompact, "table", {}, 1),
     "bb_s2": (T, 9, Backend.GpuBoundingBox, "auto", {}, 1),
     "bb_s3": (C, 5, Backend.GpuBoundingBox, "auto", {}, 1),
+    "bb_s4": (Y, 4, Backend.GpuBoundingBox, "auto", {}, 1),
     "push_p2p": (T, 12, Backend.GpuCompact, "packed", {}, 2),
     "push_p2p_q8": (T, 17, Backend.GpuCompact, "packed", {}, 2),
 }
