@@ -400,6 +400,10 @@ struct nbbgpu_sim {
     void* d_tab = nullptr;
     int tab_deg = 0;
     int cluster_fit[2] = {-1, -1};          // 8- / 16-CTA resident clusters fit (-1: not queried)
+    // transposed-plane steps (step kernel writes Bt, not B): the front's Bt is valid /
+    // the front's B was not written (bnd_refresh rebuilds it before any B reader)
+    bool bt_front = false;
+    bool bnd_stale = false;
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }

@@ -93,6 +93,10 @@ struct PackedStepParams {
     // SPLIT = 2 (candy CTA pairs): the staged row window of half h is record words
     // [win0[h], win0[h] + win_words)
     uint32_t win0[2], win_words;
+    // per-warp-store kernels on one GPU: instead of the boundary plane, write the
+    // transposed plane Bt (layout of bnd_transpose_kernel) straight from the output
+    // record -- no transpose kernel, no boundary-plane round trip (nullptr: write B)
+    uint32_t* bt_out;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
@@ -817,6 +821,12 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     uint8_t* outs = st + NS * stage_bytes;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    // BTO: per-warp stores + transposed boundary plane written here (p.bt_out).  The
+    // record's output buffer o then has two more barriers: ofull[o] = every chunk warp
+    // wrote its slice (the TW transposing warps wait for it), oempty[o] = the
+    // transposing warps are done reading it (every warp waits before rewriting it)
+    const bool BTO = PWS && SPLIT == 1 && p.bt_out != nullptr;
+    const uint32_t nHc = (p.nSrc + 31) / 32, TW = nHc < (uint32_t)NCHUNK ? nHc : (uint32_t)NCHUNK;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(full0 + 8 * s, HW > 0 ? 2 : 1);  // producer (+ bytes) [+ the halo warp]
@@ -824,7 +834,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
         for (int o = 0; o < NO; ++o) {
             mbar_init(ofull0 + 8 * o, NCHUNK);
-            mbar_init(oempty0 + 8 * o, 1);
+            mbar_init(oempty0 + 8 * o, BTO ? TW : 1);
         }
         mbar_fence_init();
     }
@@ -976,6 +986,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             if (i >= NO) {  // this warp's store from NO groups ago has read its slice
                 if (lane == 0) bulk_wait_read<NO / NGRP - 1>();
                 __syncwarp();
+                if (BTO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);  // ... and the transposers
             }
         } else if (i >= NO) {
             mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
@@ -992,6 +1003,23 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 mbar_arrive(empty0 + 8 * s);
                 rec_s2g(p, dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
                          (w_hi - w_lo) * 4);
+                if (BTO) mbar_arrive(ofull0 + 8 * o);  // release: this slice is written
+            }
+            if (BTO) {
+                // warp c < TW: chunks c, c + TW, ... of 32 boundary slots -- lane l loads
+                // the record word of slot 32k + l, one transpose gives lane b the slot
+                // bits of tile b: Bt[(g nHc + k) 32 + b], a coalesced 128-byte store
+                if ((uint32_t)c < TW) {
+                    mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);  // acquire: the whole record
+                    for (uint32_t k = (uint32_t)c; k < nHc; k += TW) {
+                        const uint32_t m = 32 * k + (uint32_t)lane;
+                        const uint32_t w = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
+                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(w, (uint32_t)lane);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(oempty0 + 8 * o);
+                }
+                continue;
             }
             uint32_t* bg = bdst + (uint64_t)g * p.nSrc;
             if constexpr (REGB) {

@@ -513,3 +513,35 @@ def test_packed_resident_small_levels(monkeypatch, resident):
     _, _, launches = sim.step_profiled(conway_rule(), 50)  # one launch for all 50 steps
     assert launches == (1 if resident == "1" else 50)
     sim.close()
+
+
+def test_transposed_plane_written_by_step_kernel(monkeypatch):
+    # per-warp-store step kernels on one GPU write the next front's transposed
+    # boundary plane (Bt) instead of B; switching the gather mode mid-run, set_cell
+    # and partitioning must rebuild whichever plane is stale (bytes == oracle)
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    K = FractalDescriptor("k6s3", 6, 3, [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 2)])
+    for desc, r in ((H, 6), (CARPET, 6), (K, 6)):
+        o = oracle.Oracle(desc.replicas, desc.k, desc.s, r)
+        o.seed(77, 0.5)
+        sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+        sim.seed_random(77, 0.5)
+        rule = conway_rule()
+        for bt, n in (("1", 3), ("0", 2), ("1", 4), ("1", 1), ("0", 1)):
+            monkeypatch.setenv("NBBGPU_HALO_BT", bt)
+            sim.step(rule, n)
+            for _ in range(n):
+                o.step(rule.birth, rule.survive, rule.moore)
+            assert np.array_equal(sim.front().data, o.front), (desc.name, bt, n)
+            if bt == "1" and n == 4:  # a host write between Bt steps
+                e = next((x, y) for y in range(sim.side()) for x in range(sim.side()) if o.to_compact(x, y))
+                sim.set_cell(e, 1 - sim.cell(e))
+                cx, cy = o.to_compact(*e)
+                o.front[cy * o.w + cx] ^= 1
+        vn = StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)
+        monkeypatch.setenv("NBBGPU_HALO_BT", "1")
+        sim.step(vn, 3)
+        for _ in range(3):
+            o.step(vn.birth, vn.survive, vn.moore)
+        assert np.array_equal(sim.front().data, o.front), desc.name
+        sim.close()
