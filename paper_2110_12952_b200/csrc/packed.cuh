@@ -783,9 +783,12 @@ struct WsGeom {
 // boundary-plane words, two round trips per group, HW groups in flight) into the
 // stage and arrive on its full barrier -- no separate halo kernel.  Pays off when a
 // rank owns few groups (T r=18 / r=20 on 8 GPUs: the halo kernel's fixed latency).
+// BTW > 0 (per-warp-store kernels on one GPU, p.bt_out): BTW extra warps write the
+// transposed boundary plane Bt (bnd_transpose_kernel's layout) from each finished
+// output record -- no transpose kernel and no boundary-plane round trip per step.
 template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1,
-          int HW = 0>
-__global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2 + HW) * 32, 1)
+          int HW = 0, int BTW = 0>
+__global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2 + HW + BTW) * 32, 1)
 step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                        const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
     using W = Wiring<FT, P>;
@@ -821,12 +824,12 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     uint8_t* outs = st + NS * stage_bytes;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // BTO: per-warp stores + transposed boundary plane written here (p.bt_out).  The
-    // record's output buffer o then has two more barriers: ofull[o] = every chunk warp
-    // wrote its slice (the TW transposing warps wait for it), oempty[o] = the
-    // transposing warps are done reading it (every warp waits before rewriting it)
-    const bool BTO = PWS && SPLIT == 1 && p.bt_out != nullptr;
-    const uint32_t nHc = (p.nSrc + 31) / 32, TW = nHc < (uint32_t)NCHUNK ? nHc : (uint32_t)NCHUNK;
+    // BTO: per-warp stores + the transposed boundary plane written by the BTW bt warps.
+    // Output buffer o then uses ofull[o] = every chunk warp wrote its slice (the bt
+    // warps wait for it) and oempty[o] = the bt warps are done reading it (every chunk
+    // warp waits before rewriting the buffer)
+    constexpr bool BTO = PWS && SPLIT == 1 && BTW > 0;
+    static_assert(BTW == 0 || (BTO && HW == 0), "bt warps need per-warp stores, one CTA per record");
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(full0 + 8 * s, HW > 0 ? 2 : 1);  // producer (+ bytes) [+ the halo warp]
@@ -834,7 +837,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
         for (int o = 0; o < NO; ++o) {
             mbar_init(ofull0 + 8 * o, NCHUNK);
-            mbar_init(oempty0 + 8 * o, BTO ? TW : 1);
+            mbar_init(oempty0 + 8 * o, BTO ? BTW : 1);
         }
         mbar_fence_init();
     }
@@ -901,6 +904,27 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                     }
                 }
                 if (lane == 0) mbar_arrive(full0 + 8 * s);  // release: the halo words are visible
+            }
+            return;
+        }
+    }
+    if constexpr (BTO) {
+        if (warp >= NCW + 2) {  // ---- bt warps: chunks b, b + BTW, ... of every record ----------
+            // lane l loads the record word of boundary slot 32k + l; one transpose gives
+            // lane t the slot bits of tile t: Bt[(g nHc + k) 32 + t], 128 coalesced bytes
+            const uint32_t b = (uint32_t)(warp - NCW - 2), nHc = (p.nSrc + 31) / 32;
+            uint32_t i = 0;
+            for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
+                const uint32_t o = i % NO;
+                mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);  // acquire: every slice written
+                const uint32_t* Do = reinterpret_cast<const uint32_t*>(outs + o * out_bytes);
+                for (uint32_t k = b; k < nHc; k += BTW) {
+                    const uint32_t m = 32 * k + (uint32_t)lane;
+                    const uint32_t w = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
+                    p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(w, (uint32_t)lane);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(oempty0 + 8 * o);  // release: buffer o read
             }
             return;
         }
@@ -986,7 +1010,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             if (i >= NO) {  // this warp's store from NO groups ago has read its slice
                 if (lane == 0) bulk_wait_read<NO / NGRP - 1>();
                 __syncwarp();
-                if (BTO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);  // ... and the transposers
+                if constexpr (BTO) mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);  // ... and the bt warps
             }
         } else if (i >= NO) {
             mbar_wait(oempty0 + 8 * o, ((i / NO) - 1) & 1u);
@@ -1003,24 +1027,9 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 mbar_arrive(empty0 + 8 * s);
                 rec_s2g(p, dst + (uint64_t)g * p.Cp + out_off + w_lo, smem_u32(Do + out_off + w_lo),
                          (w_hi - w_lo) * 4);
-                if (BTO) mbar_arrive(ofull0 + 8 * o);  // release: this slice is written
+                if constexpr (BTO) mbar_arrive(ofull0 + 8 * o);  // release: this slice is written
             }
-            if (BTO) {
-                // warp c < TW: chunks c, c + TW, ... of 32 boundary slots -- lane l loads
-                // the record word of slot 32k + l, one transpose gives lane b the slot
-                // bits of tile b: Bt[(g nHc + k) 32 + b], a coalesced 128-byte store
-                if ((uint32_t)c < TW) {
-                    mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);  // acquire: the whole record
-                    for (uint32_t k = (uint32_t)c; k < nHc; k += TW) {
-                        const uint32_t m = 32 * k + (uint32_t)lane;
-                        const uint32_t w = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
-                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(w, (uint32_t)lane);
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(oempty0 + 8 * o);
-                }
-                continue;
-            }
+            if constexpr (BTO) continue;  // the bt warps write the boundary data
             uint32_t* bg = bdst + (uint64_t)g * p.nSrc;
             if constexpr (REGB) {
                 if (k_lo + lane < k_hi) bg[bm0] = Do[bw0];
