@@ -830,6 +830,8 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // warp waits before rewriting the buffer)
     constexpr bool BTO = PWS && SPLIT == 1 && BTW > 0;
     static_assert(BTW == 0 || (BTO && HW == 0), "bt warps need per-warp stores, one CTA per record");
+    static_assert(BTW % NGRP == 0, "bt warps are split evenly over the group sets");
+    constexpr int BTS = BTW / NGRP > 0 ? BTW / NGRP : 1;  // bt warps per group set
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(full0 + 8 * s, HW > 0 ? 2 : 1);  // producer (+ bytes) [+ the halo warp]
@@ -837,7 +839,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
         for (int o = 0; o < NO; ++o) {
             mbar_init(ofull0 + 8 * o, NCHUNK);
-            mbar_init(oempty0 + 8 * o, BTO ? BTW : 1);
+            mbar_init(oempty0 + 8 * o, BTO ? BTS : 1);
         }
         mbar_fence_init();
     }
@@ -912,16 +914,19 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         if (warp >= NCW + 2) {  // ---- bt warps: chunks b, b + BTW, ... of every record ----------
             // lane l loads the record word of boundary slot 32k + l; one transpose gives
             // lane t the slot bits of tile t: Bt[(g nHc + k) 32 + t], 128 coalesced bytes
-            const uint32_t b = (uint32_t)(warp - NCW - 2), nHc = (p.nSrc + 31) / 32;
-            uint32_t i = 0;
-            for (uint32_t g = p.g0 + pair; g < p.g1; g += npairs, ++i) {
+            // bt warp w serves group set w % NGRP (each set's buffers, no head-of-line
+            // blocking between sets), chunks w / NGRP, + BTS, ...
+            const uint32_t w = (uint32_t)(warp - NCW - 2), set = w % NGRP, b = w / NGRP;
+            const uint32_t nHc = (p.nSrc + 31) / 32;
+            uint32_t i = set;
+            for (uint32_t g = p.g0 + pair + set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
                 const uint32_t o = i % NO;
                 mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);  // acquire: every slice written
                 const uint32_t* Do = reinterpret_cast<const uint32_t*>(outs + o * out_bytes);
-                for (uint32_t k = b; k < nHc; k += BTW) {
+                for (uint32_t k = b; k < nHc; k += BTS) {
                     const uint32_t m = 32 * k + (uint32_t)lane;
-                    const uint32_t w = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
-                    p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(w, (uint32_t)lane);
+                    const uint32_t x = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
+                    p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, (uint32_t)lane);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(oempty0 + 8 * o);  // release: buffer o read
