@@ -545,3 +545,39 @@ def test_transposed_plane_written_by_step_kernel(monkeypatch):
             o.step(vn.birth, vn.survive, vn.moore)
         assert np.array_equal(sim.front().data, o.front), desc.name
         sim.close()
+
+
+def test_neighbor_table_kernel():
+    # SimOptions(neighbor_table=True) -> build_neighbor_table (stencil.cpp:401-414) on
+    # the device and the table-driven step (stencil.cpp:340-352): byte-exact
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    for desc, r in ((T, 9), (CARPET, 4), (H, 5), (VICSEK, 5)):
+        _lockstep_vs_oracle(desc, r, conway_rule(), 5 + r, 0.5, 4, kernel="table")
+        _lockstep_vs_oracle(desc, r, StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 6 + r, 0.5, 3,
+                            kernel="table")
+    sim = Simulation(T, 8, Backend.GpuCompact, SimOptions(neighbor_table=True))
+    assert sim.active_kernel()[0] == "table"
+    sim.close()
+
+
+def test_bench_harness_rows_on_gpu():
+    # bench_run / write_csv / read_csv (bench.cpp:83-153) over the GPU backends:
+    # timed rows for gpu-bb, gpu-lambda, gpu-compact (linear and blocked), the
+    # speedup_vs_bb column against the level's gpu-bb row, the CSV round trip
+    import io
+    from paper_2110_12952_b200.benchrec import BenchConfig, bench_run, read_csv, write_csv
+    cfg = BenchConfig(desc=T, levels=[8, 10], block_sizes=[0, 4], reps=2, iters=5)
+    recs = bench_run(cfg)
+    rows = {(r.level, r.backend, r.block_size): r for r in recs}
+    for lvl in (8, 10):
+        bb = rows[(lvl, "gpu-bb", 0)]
+        assert bb.mean_ms > 0 and bb.speedup_vs_bb == 1.0
+        for key in ((lvl, "gpu-lambda", 0), (lvl, "gpu-compact", 0), (lvl, "gpu-compact", 4)):
+            r = rows[key]
+            assert r.mean_ms > 0 and not r.skip_reason, key
+            assert abs(r.speedup_vs_bb - bb.mean_ms / r.mean_ms) < 1e-9 * max(1.0, r.speedup_vs_bb)
+    assert rows[(10, "gpu-compact", 0)].mem_cells == 3 ** 10
+    s = io.StringIO()
+    write_csv(recs, s)
+    back = read_csv(io.StringIO(s.getvalue()))
+    assert [(r.level, r.backend, r.block_size) for r in back] == [(r.level, r.backend, r.block_size) for r in recs]
