@@ -30,6 +30,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tiled.cuh"  // count8, apply_rule_bits (bit-sliced counts and rules)
 
 namespace nbbgpu {
 
@@ -48,30 +49,6 @@ struct BBRowParams {
 
 // 4 bits -> 4 bytes of 0/1
 __device__ __forceinline__ uint32_t bb_spread4(uint32_t nib) { return ((nib & 0xFu) * 0x00204081u) & 0x01010101u; }
-
-// SWAR rule: bytes of cnt in 0..8, alive bytes 0/1 -> next-state bytes 0/1
-template <bool CONWAY>
-__device__ __forceinline__ uint32_t bb_rule(uint32_t cnt, uint32_t alive, uint32_t tb_lo, uint32_t tb_hi,
-                                            uint32_t ts_lo, uint32_t ts_hi, uint32_t b8, uint32_t s8) {
-    if (CONWAY) {
-        // next = ((cnt | alive) == 3) per byte
-        const uint32_t v = (cnt | alive) ^ 0x03030303u;
-        const uint32_t z = ~(((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v | 0x7F7F7F7Fu);  // 0x80 where v == 0
-        return z >> 7;
-    } else {
-        // PRMT lookup of cnt & 7 in the 8-entry birth / survive byte tables
-        const uint32_t c = cnt & 0x07070707u;
-        const uint32_t nib = c | (c >> 4);                  // bytes 0, 2: two 4-bit selectors each
-        const uint32_t sel = __byte_perm(nib, 0, 0x0020);  // 4 nibbles = the 4 counts
-        const uint32_t rb = __byte_perm(tb_lo, tb_hi, sel);
-        const uint32_t rs = __byte_perm(ts_lo, ts_hi, sel);
-        const uint32_t am = alive * 0xFFu;                  // 0x00 / 0xFF per byte
-        uint32_t r = (rs & am) | (rb & ~am);
-        const uint32_t m8 = ((cnt >> 3) & 0x01010101u) * 0xFFu;  // count == 8
-        const uint32_t v8 = (s8 & am) | (b8 & ~am);
-        return (r & ~m8) | (v8 & m8);
-    }
-}
 
 // The coarse bitmap rows / columns a CTA touches, cached in shared memory: rows
 // [cy0, cy0 + nrows), columns [cx0, cx1] (wpr words per row), and column CW - 1
@@ -139,48 +116,30 @@ __device__ __forceinline__ void bb_cp_wait() { asm volatile("cp.async.wait_group
 
 __device__ __forceinline__ int64_t bb_floor16(int64_t v) { return v & ~(int64_t)15; }
 
-// the 32 bytes [off, off + 32) of a ring slot; off & 15 is warp-uniform
-__device__ __forceinline__ void bb_mid32(const uint8_t* slot, uint32_t off, uint32_t m[8]) {
-    const uint32_t a = off & ~15u, o = off & 15u;
-    const uint4 v0 = *reinterpret_cast<const uint4*>(slot + a);
-    const uint4 v1 = *reinterpret_cast<const uint4*>(slot + a + 16);
-    if (o == 0u) {
-        m[0] = v0.x; m[1] = v0.y; m[2] = v0.z; m[3] = v0.w;
-        m[4] = v1.x; m[5] = v1.y; m[6] = v1.z; m[7] = v1.w;
-        return;
-    }
-    const uint4 v2 = *reinterpret_cast<const uint4*>(slot + a + 32);
-    const uint32_t v[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-    const uint32_t sh = 8u * (o & 3u);
-    switch (o >> 2) {  // uniform across the warp: no divergence, static register indices
-    case 0:
+// 32 bytes of 0/1 (8 words) -> 32 bits, bit i = byte i
+__device__ __forceinline__ uint32_t bb_pack32(const uint4 a, const uint4 b) {
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j], v[j + 1], sh);
-        break;
-    case 1:
-#pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 1], v[j + 2], sh);
-        break;
-    case 2:
-#pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 2], v[j + 3], sh);
-        break;
-    default:
-#pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = __funnelshift_r(v[j + 3], v[j + 4], sh);
-        break;
-    }
+    for (int j = 0; j < 8; ++j) bits |= ((w[j] * 0x01020408u) >> 24) << (4 * j);  // b0 + 2 b1 + 4 b2 + 8 b3
+    return bits;
 }
 
-// 0xFF in byte b (0..31) of a 32-byte pair, as word j
-__device__ __forceinline__ uint32_t bb_byte_mask(int b, int j) {
-    return ((unsigned)b < 32u && (b >> 2) == j) ? 0xFFu << (8 * (b & 3)) : 0u;
+// the 32 cells [off, off + 32) of a bit row, and the cells off - 1 (top bit of
+// west) and off + 32 (bit 0 of east); off & 31 is warp-uniform, off >= 1
+__device__ __forceinline__ void bb_bits_window(const uint32_t* row, uint32_t off, uint32_t& v, uint32_t& west,
+                                               uint32_t& east) {
+    const uint32_t w = off >> 5, sh = off & 31;
+    const uint32_t a = row[w], b = row[w + 1];
+    v = __funnelshift_r(a, b, sh);
+    west = sh ? a << (32 - sh) : row[w - 1];
+    east = __funnelshift_r(b, row[w + 2], sh);
 }
 
 // shared-memory layout of step_bb_rows_kernel: NS ring slots, the low table, the
 // coarse cache (kBBCacheWords), the live flags [NS][warps], two mask rows
 constexpr uint32_t kBBCacheWords = 64;
-constexpr int kBBStages = 6;
+constexpr int kBBStages = 6;  // byte ring (rows y+2 .. y+4 in flight)
 constexpr int kBBMaxThreads = 128;
 
 // coarse rows / columns of tile (sx, band): rows y0 - 1 .. y1 + NS, x within
@@ -200,16 +159,23 @@ __device__ __host__ __forceinline__ void bb_tile_cover(const BBRowParams& p, uin
 }
 
 // One CTA per live tile (strip sx of the aligned rows of band b: tiles whose output
-// bytes are all holes are left out of the list on the host); 2 chunks per thread.
+// bytes are all holes are left out of the list on the host); 32 cells per thread.
+// Rows stream in as bytes (cp.async ring, NS slots), each thread packs its own 32
+// bytes of row y + 2 to one bit word (bit ring of 4 rows), and row y is computed
+// bit-sliced: 32 cells per word op (count8 adders + the rule), unpacked to bytes
+// only for the two 16-byte stores.
 template <bool CONWAY, int NS>
 __global__ void __launch_bounds__(kBBMaxThreads, 8)
 step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const uint32_t* __restrict__ lowtab,
                     const uint32_t* __restrict__ coarse, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
-    static_assert(NS >= 4, "rows y-1, y, y+1 plus one in flight");
+    static_assert(NS >= 5, "rows y+3.. in flight while row y+2 is packed");
+    constexpr int NB = 4;  // bit ring: rows y-1 .. y+2
     extern __shared__ __align__(16) uint8_t sm[];
-    const uint32_t W = (p.cps + 4) * 16;  // slot bytes
+    const uint32_t W = (p.cps + 4) * 16;  // byte slot
     const int TPB = blockDim.x, NW = TPB >> 5;
-    uint32_t* lt = reinterpret_cast<uint32_t*>(sm + NS * W);
+    const uint32_t BWS = (uint32_t)TPB + 4;  // bit slot words (+ pad for the shifted windows)
+    uint32_t* bits = reinterpret_cast<uint32_t*>(sm + NS * W);    // [NB][BWS]
+    uint32_t* lt = bits + NB * BWS;
     uint32_t* ccw = lt + p.S * p.lt_words;
     uint32_t* mrow = ccw + kBBCacheWords;                         // [2][TPB + 2]
     uint8_t* flags = reinterpret_cast<uint8_t*>(mrow + 2 * (TPB + 2));  // [NS][NW]
@@ -242,22 +208,19 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         ccw[i] = v;
     }
     for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
+    for (uint32_t i = t; i < NB * BWS; i += TPB) bits[i] = 0u;
     __syncthreads();
 
-    // rule tables (bytes 0/1) for counts 0..7 and the count-8 entries
-    uint32_t tb_lo = 0, tb_hi = 0, ts_lo = 0, ts_hi = 0;
+    uint32_t KB[9], KS[9];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        tb_lo |= ((p.birth >> c) & 1u) << (8 * c);
-        tb_hi |= ((p.birth >> (c + 4)) & 1u) << (8 * c);
-        ts_lo |= ((p.survive >> c) & 1u) << (8 * c);
-        ts_hi |= ((p.survive >> (c + 4)) & 1u) << (8 * c);
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
-    const uint32_t b8 = ((p.birth >> 8) & 1u) * 0x01010101u, s8 = ((p.survive >> 8) & 1u) * 0x01010101u;
 
-    // row rho (-1 .. n) -> the next ring slot; thread t loads chunks 2t+2, 2t+3 of
-    // the segment, threads 0..3 also the margin chunks 0, 1, cps+2, cps+3.  A warp
-    // whose own 64 chunks are holes zero-fills them instead and flags the slot.
+    // row rho (-1 .. n) -> the next byte slot; thread t loads chunks 2t+2, 2t+3 of
+    // the segment, thread 0 also the margin chunks 0, 1 and thread 1 cps+2, cps+3.
+    // A warp whose own 64 chunks are holes loads nothing and flags the slot.
     const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
     auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
         uint8_t* slot = sm + sl * W;
@@ -265,15 +228,34 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         const int64_t x0 = bb_floor16(rn) + wx - rn;
         const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
         if (lane == 0) flags[sl * NW + warp] = live;
-        auto one = [&](uint32_t ch, bool want) {
+        auto one = [&](uint32_t ch) {
             const int64_t a = base + 16 * (int64_t)ch;
-            const bool in = want && a >= 0 && a + 16 <= (int64_t)p.alloc;
-            if (in) bb_cp_async16((uint32_t)__cvta_generic_to_shared(slot + 16 * ch), src + a, 16);
-            else *reinterpret_cast<uint4*>(slot + 16 * ch) = make_uint4(0, 0, 0, 0);
+            const bool in = a >= 0 && a + 16 <= (int64_t)p.alloc;
+            bb_cp_async16((uint32_t)__cvta_generic_to_shared(slot + 16 * ch), in ? src + a : src, in ? 16u : 0u);
         };
-        one(2 * (uint32_t)t + 2, live);
-        one(2 * (uint32_t)t + 3, live);
-        if (t < 4) one(t < 2 ? (uint32_t)t : p.cps + (uint32_t)t, true);
+        if (live) {
+            one(2 * (uint32_t)t + 2);
+            one(2 * (uint32_t)t + 3);
+        }
+        if (t < 2) {
+            one(t == 0 ? 0u : p.cps + 2);
+            one(t == 0 ? 1u : p.cps + 3);
+        }
+    };
+    // the thread's own 32 bytes of byte slot sl -> bit word of bit slot bl
+    auto pack_row = [&](int sl, int bl) {
+        const uint8_t* slot = sm + sl * W;
+        uint32_t* brow = bits + bl * BWS;
+        if (flags[sl * NW + warp]) {
+            const uint4* v = reinterpret_cast<const uint4*>(slot + 32 + 32 * t);
+            brow[1 + t] = bb_pack32(v[0], v[1]);
+        } else {
+            brow[1 + t] = 0u;
+        }
+        if (t < 2) {
+            const uint4* v = reinterpret_cast<const uint4*>(slot + (t == 0 ? 0u : 16 * (p.cps + 2)));
+            brow[t == 0 ? 0 : TPB + 1] = bb_pack32(v[0], v[1]);
+        }
     };
     // membership bits of row y for x in [xs - 16 + 32k, +32), k = 0 .. TPB
     auto mask_row = [&](int64_t y, uint32_t* m) {
@@ -287,39 +269,41 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         }
     };
 
-    int sl_load = 0;  // slot of row y0 - 1 (rows map to slots in order)
+    // prologue: rows y0-1 .. y0+NS-3 in flight, rows y0-1 .. y0+1 packed
     {
         int64_t rn = (y0 - 1) * n;
         for (int i = 0; i < NS - 1; ++i, rn += n) {
-            load_row(y0 - 1 + i, rn, sl_load);
-            sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
+            load_row(y0 - 1 + i, rn, i);
             bb_cp_commit();
         }
     }
+    bb_cp_wait<NS - 4>();  // rows y0-1 .. y0+1 (this thread's copies)
+    for (int i = 0; i < 3; ++i) pack_row(i, i);
     mask_row(y0, mrow);
-    int slU = 0;  // slot of row y - 1
+    int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
+    int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
     int64_t yn = y0 * n;
     int64_t rn_load = (y0 + NS - 2) * n;
-    const uint32_t offM = 32 + 32 * t;
+    const uint32_t offM = 32 + 32 * t;  // the thread's cells in a segment (bit offset == byte offset)
     for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
-        bb_cp_wait<NS - 4>();  // rows <= y + 1 landed (this thread's copies)
-        __syncthreads();       // ... everyone's; slot of row y - 2 and mask row y - 1 are free
+        bb_cp_wait<NS - 5>();  // row y + 2 landed (this thread's copies)
+        __syncthreads();       // rows <= y + 1 packed; slots of rows y - 2 free
         load_row(y + NS - 2, rn_load, sl_load);
         sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
         bb_cp_commit();
+        const int sl2 = (int)((y + 3 - y0) % NS);  // byte slot of row y + 2 (row y0 - 1 in slot 0)
+        const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
+        pack_row(sl2, b2);
         const int par = (int)((y - y0) & 1);
         mask_row(y + 1, mrow + (par ^ 1) * (TPB + 2));
 
-        const int slM = slU + 1 == NS ? 0 : slU + 1, slD = slM + 1 == NS ? 0 : slM + 1;
-        const uint8_t* sU = sm + slU * W;
-        const uint8_t* sM = sm + slM * W;
-        const uint8_t* sD = sm + slD * W;
-        slU = slM;
-        if (!flags[slM * NW + warp]) continue;  // warp-uniform: 1024 bytes of holes stay 0
+        const uint32_t* Ub = bits + bU * BWS;
+        const uint32_t* Mb = bits + bM * BWS;
+        const uint32_t* Db = bits + bD * BWS;
+        bU = bM;
+        if (!flags[(int)((y + 1 - y0) % NS) * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
         const int64_t sty = bb_floor16(yn);
         const int d = (int)(sty - yn);  // -15 .. 0
-        const uint32_t offU = (uint32_t)(sty - n - bb_floor16(yn - n)) + offM;
-        const uint32_t offD = (uint32_t)(sty + n - bb_floor16(yn + n)) + offM;
         const uint32_t* mr = mrow + par * (TPB + 2);
         uint32_t mem = __funnelshift_r(mr[t], mr[t + 1], (uint32_t)(16 + d));
         const int64_t c = sty + xs + 32 * (int64_t)t;
@@ -328,61 +312,38 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
             mem |= bb_member<16>(p, lt, cc, (uint32_t)(n + xc), (uint32_t)(y - 1)) & ((1u << (-xc)) - 1u);
         const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
         if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
-        uint32_t U[8], M[8], D[8];
-        bb_mid32(sM, offM, M);
-        uint32_t E[10];
-        if (p.moore) {
-            bb_mid32(sU, offU, U);
-            bb_mid32(sD, offD, D);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) E[j + 1] = U[j] + M[j] + D[j];  // bytes <= 3
-        } else {
-            bb_mid32(sU, offU, U);
-            bb_mid32(sD, offD, D);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) E[j + 1] = M[j];
-        }
-        // the columns west / east neighbours come from (Moore: vertical sums,
-        // von Neumann: M); the pair's edge bytes from the neighbouring lanes
-        E[0] = __shfl_up_sync(0xFFFFFFFFu, E[8], 1);
-        E[9] = __shfl_down_sync(0xFFFFFFFFu, E[1], 1);
-        if (lane == 0) {
-            uint32_t v = sM[offM - 1];
-            if (p.moore) v += sU[offU - 1] + sD[offD - 1];
-            E[0] = v << 24;
-        }
-        if (lane == 31) {
-            uint32_t v = sM[offM + 32];
-            if (p.moore) v += sU[offU + 32] + sD[offD + 32];
-            E[9] = v;
-        }
         if (mem == 0u) continue;
-        // column edges inside the pair: x = 0 at byte -xc (row y) and n - xc (row
-        // y + 1); x = n - 1 one byte before each
-        const int64_t b2 = n - xc;
-        const bool edge = (uint64_t)(-xc) <= 32u || (uint64_t)b2 <= 32u;
-        uint32_t wm[8], em[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) wm[j] = em[j] = 0u;
-        if (edge) {
-            const int ib1 = (int)(-xc), ib2 = (int)b2;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                wm[j] = bb_byte_mask(ib1, j) | bb_byte_mask(ib2, j);
-                em[j] = bb_byte_mask(ib1 - 1, j) | bb_byte_mask(ib2 - 1, j);
-            }
+        // the three rows: own 32 cells + the cells west / east of them
+        const uint32_t m = Mb[1 + t], mwb = Mb[t], meb = Mb[t + 2];
+        uint32_t u, uwb, ueb, dd, dwb, deb;
+        bb_bits_window(Ub, (uint32_t)(sty - n - bb_floor16(yn - n)) + offM, u, uwb, ueb);
+        bb_bits_window(Db, (uint32_t)(sty + n - bb_floor16(yn + n)) + offM, dd, dwb, deb);
+        // column edges inside the pair: x = 0 at bit -xc (row y) and n - xc (row y + 1);
+        // x = n - 1 one bit before each: no west / east neighbours there
+        const int64_t b1 = -xc, b2e = n - xc;
+        uint32_t wm = 0u, em = 0u;
+        if ((uint64_t)b1 <= 32u || (uint64_t)b2e <= 32u) {
+            if (b1 >= 0 && b1 < 32) wm |= 1u << b1;
+            if (b2e >= 0 && b2e < 32) wm |= 1u << b2e;
+            if (b1 >= 1 && b1 <= 32) em |= 1u << (b1 - 1);
+            if (b2e >= 1 && b2e <= 32) em |= 1u << (b2e - 1);
         }
-        uint32_t out[8];
-#pragma unroll
-        for (int j = 1; j <= 8; ++j) {
-            const uint32_t w = __funnelshift_l(E[j - 1], E[j], 8) & ~wm[j - 1];
-            const uint32_t e = __funnelshift_r(E[j], E[j + 1], 8) & ~em[j - 1];
-            const uint32_t cnt = p.moore ? w + E[j] + e - M[j - 1] : U[j - 1] + D[j - 1] + w + e;
-            const uint32_t r = bb_rule<CONWAY>(cnt, M[j - 1], tb_lo, tb_hi, ts_lo, ts_hi, b8, s8);
-            out[j - 1] = r & bb_spread4(mem >> (4 * (j - 1)));
+        const uint32_t mw = ((m << 1) | (mwb >> 31)) & ~wm, me = ((m >> 1) | (meb << 31)) & ~em;
+        uint32_t r;
+        if (p.moore) {
+            const uint32_t uw = ((u << 1) | (uwb >> 31)) & ~wm, ue = ((u >> 1) | (ueb << 31)) & ~em;
+            const uint32_t dw = ((dd << 1) | (dwb >> 31)) & ~wm, de = ((dd >> 1) | (deb << 31)) & ~em;
+            r = apply_rule_bits<CONWAY>(count8(uw, u, ue, mw, me, dw, dd, de), m, KB, KS);
+        } else {
+            r = apply_rule_bits<false>(count8(u, dd, mw, me, 0u, 0u, 0u, 0u), m, KB, KS);
         }
-        if (mem & 0xFFFFu) *reinterpret_cast<uint4*>(dst + c) = make_uint4(out[0], out[1], out[2], out[3]);
-        if (mem >> 16) *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(out[4], out[5], out[6], out[7]);
+        r &= mem;
+        if (mem & 0xFFFFu)
+            *reinterpret_cast<uint4*>(dst + c) = make_uint4(bb_spread4(r), bb_spread4(r >> 4), bb_spread4(r >> 8),
+                                                            bb_spread4(r >> 12));
+        if (mem >> 16)
+            *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(bb_spread4(r >> 16), bb_spread4(r >> 20),
+                                                                 bb_spread4(r >> 24), bb_spread4(r >> 28));
     }
     bb_cp_wait<0>();
 }

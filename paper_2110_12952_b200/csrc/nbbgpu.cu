@@ -681,8 +681,8 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     if (h->bb_ntiles == 0) return;
     const dim3 grid(h->bb_ntiles);
     const uint32_t tpb = p.cps / 2;
-    const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4 +
-                        2 * (tpb + 2) * 4 + kBBStages * (tpb / 32);
+    const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)4 * (tpb + 4) * 4 +
+                        (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4 + 2 * (tpb + 2) * 4 + kBBStages * (tpb / 32);
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
     if (conway)
