@@ -228,10 +228,13 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         const int64_t x0 = bb_floor16(rn) + wx - rn;
         const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
         if (lane == 0) flags[sl * NW + warp] = live;
+        // (the whole segment inside the buffer: no per-chunk bounds)
+        const bool inside = base >= 0 && base + (int64_t)W <= (int64_t)p.alloc;
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(slot);
         auto one = [&](uint32_t ch) {
             const int64_t a = base + 16 * (int64_t)ch;
-            const bool in = a >= 0 && a + 16 <= (int64_t)p.alloc;
-            bb_cp_async16((uint32_t)__cvta_generic_to_shared(slot + 16 * ch), in ? src + a : src, in ? 16u : 0u);
+            const bool in = inside || (a >= 0 && a + 16 <= (int64_t)p.alloc);
+            bb_cp_async16(sbase + 16 * ch, in ? src + a : src, in ? 16u : 0u);
         };
         if (live) {
             one(2 * (uint32_t)t + 2);
@@ -281,6 +284,7 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
     for (int i = 0; i < 3; ++i) pack_row(i, i);
     mask_row(y0, mrow);
     int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
+    int sl_y = 1 % NS;     // byte slot of row y (row y0 - 1 is in slot 0)
     int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
     int64_t yn = y0 * n;
     int64_t rn_load = (y0 + NS - 2) * n;
@@ -291,7 +295,9 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         load_row(y + NS - 2, rn_load, sl_load);
         sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
         bb_cp_commit();
-        const int sl2 = (int)((y + 3 - y0) % NS);  // byte slot of row y + 2 (row y0 - 1 in slot 0)
+        const int sl_c = sl_y;  // byte slot of row y (its live flags)
+        sl_y = sl_y + 1 == NS ? 0 : sl_y + 1;
+        const int sl2 = sl_c + 2 >= NS ? sl_c + 2 - NS : sl_c + 2;  // byte slot of row y + 2
         const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
         pack_row(sl2, b2);
         const int par = (int)((y - y0) & 1);
@@ -301,7 +307,7 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         const uint32_t* Mb = bits + bM * BWS;
         const uint32_t* Db = bits + bD * BWS;
         bU = bM;
-        if (!flags[(int)((y + 1 - y0) % NS) * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
+        if (!flags[sl_c * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
         const int64_t sty = bb_floor16(yn);
         const int d = (int)(sty - yn);  // -15 .. 0
         const uint32_t* mr = mrow + par * (TPB + 2);
