@@ -43,6 +43,7 @@ struct BBRowParams {
     uint32_t lt_words;  // words per doubled low-table row
     uint32_t cps;       // chunks per strip (2 per thread, multiple of 64, <= 256)
     uint32_t rows;      // rows per CTA (band height)
+    uint32_t ntiles;    // live tiles (the tile list)
     uint32_t birth, survive;
     int moore;
 };
@@ -181,177 +182,188 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
     uint8_t* flags = reinterpret_cast<uint8_t*>(mrow + 2 * (TPB + 2));  // [NS][NW]
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t n = (int64_t)p.n;
-    const uint2 tile = tiles[blockIdx.x];
-    const int64_t y0 = (int64_t)tile.y * p.rows;
-    const int64_t y1 = min(y0 + (int64_t)p.rows, n);
-    const int64_t xs = (int64_t)tile.x * p.cps * 16;  // strip offset within an aligned row
-    BBCoarse cc;
-    uint32_t cy1;
-    bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
-    cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 2;
-    cc.bits = ccw;
-    cc.last = 0;
-    for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry) {
-        const uint64_t b = (uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1;
-        cc.last |= ((__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u) << ry;
-    }
-    for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += TPB) {
-        const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
-        const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
-        const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
-        uint32_t v = 0;
-        if (32 * k < ncols) {
-            v = __funnelshift_r(__ldg(coarse + (b0 >> 5)), __ldg(coarse + (b0 >> 5) + 1), (uint32_t)(b0 & 31));
-            const uint32_t left = ncols - 32 * k;
-            if (left < 32) v &= (1u << left) - 1u;
-        }
-        ccw[i] = v;
-    }
-    for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
-    for (uint32_t i = t; i < NB * BWS; i += TPB) bits[i] = 0u;
-    __syncthreads();
-
     uint32_t KB[9], KS[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
         KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
         KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
-
-    // row rho (-1 .. n) -> the next byte slot; thread t loads chunks 2t+2, 2t+3 of
-    // the segment, thread 0 also the margin chunks 0, 1 and thread 1 cps+2, cps+3.
-    // A warp whose own 64 chunks are holes loads nothing and flags the slot.
-    const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
-    auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
-        uint8_t* slot = sm + sl * W;
-        const int64_t base = bb_floor16(rn) + xs - 32;
-        const int64_t x0 = bb_floor16(rn) + wx - rn;
-        const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
-        if (lane == 0) flags[sl * NW + warp] = live;
-        // (the whole segment inside the buffer: no per-chunk bounds)
-        const bool inside = base >= 0 && base + (int64_t)W <= (int64_t)p.alloc;
-        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(slot);
-        auto one = [&](uint32_t ch) {
-            const int64_t a = base + 16 * (int64_t)ch;
-            const bool in = inside || (a >= 0 && a + 16 <= (int64_t)p.alloc);
-            bb_cp_async16(sbase + 16 * ch, in ? src + a : src, in ? 16u : 0u);
-        };
-        if (live) {
-            one(2 * (uint32_t)t + 2);
-            one(2 * (uint32_t)t + 3);
+    for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
+    // persistent CTAs: tiles blockIdx.x, + gridDim.x, ... (no tail wave of whole tiles)
+    for (uint32_t ti = blockIdx.x; ti < p.ntiles; ti += gridDim.x) {
+        const uint2 tile = tiles[ti];
+        const int64_t y0 = (int64_t)tile.y * p.rows;
+        const int64_t y1 = min(y0 + (int64_t)p.rows, n);
+        const int64_t xs = (int64_t)tile.x * p.cps * 16;  // strip offset within an aligned row
+        BBCoarse cc;
+        uint32_t cy1;
+        bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
+        cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 2;
+        cc.bits = ccw;
+        cc.last = 0;
+        for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry) {
+            const uint64_t b = (uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1;
+            cc.last |= ((__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u) << ry;
         }
-        if (t < 2) {
-            one(t == 0 ? 0u : p.cps + 2);
-            one(t == 0 ? 1u : p.cps + 3);
-        }
-    };
-    // the thread's own 32 bytes of byte slot sl -> bit word of bit slot bl
-    auto pack_row = [&](int sl, int bl) {
-        const uint8_t* slot = sm + sl * W;
-        uint32_t* brow = bits + bl * BWS;
-        if (flags[sl * NW + warp]) {
-            const uint4* v = reinterpret_cast<const uint4*>(slot + 32 + 32 * t);
-            brow[1 + t] = bb_pack32(v[0], v[1]);
-        } else {
-            brow[1 + t] = 0u;
-        }
-        if (t < 2) {
-            const uint4* v = reinterpret_cast<const uint4*>(slot + (t == 0 ? 0u : 16 * (p.cps + 2)));
-            brow[t == 0 ? 0 : TPB + 1] = bb_pack32(v[0], v[1]);
-        }
-    };
-    // membership bits of row y for x in [xs - 16 + 32k, +32), k = 0 .. TPB
-    auto mask_row = [&](int64_t y, uint32_t* m) {
-        if (y >= y1) return;
-        for (int k = t; k <= TPB; k += TPB) {
-            const int64_t x0 = xs - 16 + 32 * (int64_t)k;
+        for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += TPB) {
+            const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
+            const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
+            const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
             uint32_t v = 0;
-            if (x0 < 0) v = bb_member<32>(p, lt, cc, 0u, (uint32_t)y) << 16;  // strip 0: x0 = -16
-            else if (x0 < n) v = bb_member<32>(p, lt, cc, (uint32_t)x0, (uint32_t)y);
-            m[k] = v;
+            if (32 * k < ncols) {
+                v = __funnelshift_r(__ldg(coarse + (b0 >> 5)), __ldg(coarse + (b0 >> 5) + 1), (uint32_t)(b0 & 31));
+                const uint32_t left = ncols - 32 * k;
+                if (left < 32) v &= (1u << left) - 1u;
+            }
+            ccw[i] = v;
         }
-    };
+        for (uint32_t i = t; i < NB * BWS; i += TPB) bits[i] = 0u;
+        __syncthreads();
 
-    // prologue: rows y0-1 .. y0+NS-3 in flight, rows y0-1 .. y0+1 packed
-    {
-        int64_t rn = (y0 - 1) * n;
-        for (int i = 0; i < NS - 1; ++i, rn += n) {
-            load_row(y0 - 1 + i, rn, i);
+
+        // row rho (-1 .. n) -> the next byte slot; thread t loads chunks 2t+2, 2t+3 of
+        // the segment, thread 0 also the margin chunks 0, 1 and thread 1 cps+2, cps+3.
+        // A warp whose own 64 chunks are holes loads nothing and flags the slot.
+        const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
+        auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
+            uint8_t* slot = sm + sl * W;
+            const int64_t base = bb_floor16(rn) + xs - 32;
+            const int64_t x0 = bb_floor16(rn) + wx - rn;
+            const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
+            if (lane == 0) flags[sl * NW + warp] = live;
+            // (the whole segment inside the buffer: no per-chunk bounds)
+            const bool inside = base >= 0 && base + (int64_t)W <= (int64_t)p.alloc;
+            const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(slot);
+            auto one = [&](uint32_t ch) {
+                const int64_t a = base + 16 * (int64_t)ch;
+                const bool in = inside || (a >= 0 && a + 16 <= (int64_t)p.alloc);
+                bb_cp_async16(sbase + 16 * ch, in ? src + a : src, in ? 16u : 0u);
+            };
+            if (live) {
+                one(2 * (uint32_t)t + 2);
+                one(2 * (uint32_t)t + 3);
+            }
+            if (t < 2) {
+                one(t == 0 ? 0u : p.cps + 2);
+                one(t == 0 ? 1u : p.cps + 3);
+            }
+        };
+        // the thread's own 32 bytes of byte slot sl -> bit word of bit slot bl
+        auto pack_row = [&](int sl, int bl) {
+            const uint8_t* slot = sm + sl * W;
+            uint32_t* brow = bits + bl * BWS;
+            if (flags[sl * NW + warp]) {
+                const uint4* v = reinterpret_cast<const uint4*>(slot + 32 + 32 * t);
+                brow[1 + t] = bb_pack32(v[0], v[1]);
+            } else {
+                brow[1 + t] = 0u;
+            }
+            if (t < 2) {
+                const uint4* v = reinterpret_cast<const uint4*>(slot + (t == 0 ? 0u : 16 * (p.cps + 2)));
+                brow[t == 0 ? 0 : TPB + 1] = bb_pack32(v[0], v[1]);
+            }
+        };
+        // membership bits of row y for x in [xs - 16 + 32k, +32), k = 0 .. TPB (a warp
+        // whose row is holes only writes the word lane 31 of the warp before reads)
+        auto mask_row = [&](int64_t y, uint32_t* m, bool live) {
+            if (y >= y1) return;
+            for (int k = t; k <= TPB; k += TPB) {
+                if (!live && k < TPB && lane != 0) {
+                    m[k] = 0u;
+                    continue;
+                }
+                const int64_t x0 = xs - 16 + 32 * (int64_t)k;
+                uint32_t v = 0;
+                if (x0 < 0) v = bb_member<32>(p, lt, cc, 0u, (uint32_t)y) << 16;  // strip 0: x0 = -16
+                else if (x0 < n) v = bb_member<32>(p, lt, cc, (uint32_t)x0, (uint32_t)y);
+                m[k] = v;
+            }
+        };
+
+        // prologue: rows y0-1 .. y0+NS-3 in flight, rows y0-1 .. y0+1 packed
+        {
+            int64_t rn = (y0 - 1) * n;
+            for (int i = 0; i < NS - 1; ++i, rn += n) {
+                load_row(y0 - 1 + i, rn, i);
+                bb_cp_commit();
+            }
+        }
+        __syncwarp();  // lane 0's live flags
+        bb_cp_wait<NS - 4>();  // rows y0-1 .. y0+1 (this thread's copies)
+        for (int i = 0; i < 3; ++i) pack_row(i, i);
+        mask_row(y0, mrow, flags[1 % NS * NW + warp] != 0);
+        int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
+        int sl_y = 1 % NS;     // byte slot of row y (row y0 - 1 is in slot 0)
+        int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
+        int64_t yn = y0 * n;
+        int64_t rn_load = (y0 + NS - 2) * n;
+        const uint32_t offM = 32 + 32 * t;  // the thread's cells in a segment (bit offset == byte offset)
+        for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
+            bb_cp_wait<NS - 5>();  // row y + 2 landed (this thread's copies)
+            __syncthreads();       // rows <= y + 1 packed; slots of rows y - 2 free
+            load_row(y + NS - 2, rn_load, sl_load);
+            sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
             bb_cp_commit();
-        }
-    }
-    bb_cp_wait<NS - 4>();  // rows y0-1 .. y0+1 (this thread's copies)
-    for (int i = 0; i < 3; ++i) pack_row(i, i);
-    mask_row(y0, mrow);
-    int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
-    int sl_y = 1 % NS;     // byte slot of row y (row y0 - 1 is in slot 0)
-    int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
-    int64_t yn = y0 * n;
-    int64_t rn_load = (y0 + NS - 2) * n;
-    const uint32_t offM = 32 + 32 * t;  // the thread's cells in a segment (bit offset == byte offset)
-    for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
-        bb_cp_wait<NS - 5>();  // row y + 2 landed (this thread's copies)
-        __syncthreads();       // rows <= y + 1 packed; slots of rows y - 2 free
-        load_row(y + NS - 2, rn_load, sl_load);
-        sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
-        bb_cp_commit();
-        const int sl_c = sl_y;  // byte slot of row y (its live flags)
-        sl_y = sl_y + 1 == NS ? 0 : sl_y + 1;
-        const int sl2 = sl_c + 2 >= NS ? sl_c + 2 - NS : sl_c + 2;  // byte slot of row y + 2
-        const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
-        pack_row(sl2, b2);
-        const int par = (int)((y - y0) & 1);
-        mask_row(y + 1, mrow + (par ^ 1) * (TPB + 2));
+            const int sl_c = sl_y;  // byte slot of row y (its live flags)
+            sl_y = sl_y + 1 == NS ? 0 : sl_y + 1;
+            const int sl2 = sl_c + 2 >= NS ? sl_c + 2 - NS : sl_c + 2;  // byte slot of row y + 2
+            const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
+            pack_row(sl2, b2);
+            const int par = (int)((y - y0) & 1);
+            const int sl1 = sl_c + 1 == NS ? 0 : sl_c + 1;  // byte slot of row y + 1
+            mask_row(y + 1, mrow + (par ^ 1) * (TPB + 2), flags[sl1 * NW + warp] != 0);
 
-        const uint32_t* Ub = bits + bU * BWS;
-        const uint32_t* Mb = bits + bM * BWS;
-        const uint32_t* Db = bits + bD * BWS;
-        bU = bM;
-        if (!flags[sl_c * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
-        const int64_t sty = bb_floor16(yn);
-        const int d = (int)(sty - yn);  // -15 .. 0
-        const uint32_t* mr = mrow + par * (TPB + 2);
-        uint32_t mem = __funnelshift_r(mr[t], mr[t + 1], (uint32_t)(16 + d));
-        const int64_t c = sty + xs + 32 * (int64_t)t;
-        const int64_t xc = c - yn;  // x of the pair's first byte in row y (< 0: straddles)
-        if (xc < 0)  // strip 0, thread 0: the first -xc bytes end row y - 1
-            mem |= bb_member<16>(p, lt, cc, (uint32_t)(n + xc), (uint32_t)(y - 1)) & ((1u << (-xc)) - 1u);
-        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
-        if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
-        if (mem == 0u) continue;
-        // the three rows: own 32 cells + the cells west / east of them
-        const uint32_t m = Mb[1 + t], mwb = Mb[t], meb = Mb[t + 2];
-        uint32_t u, uwb, ueb, dd, dwb, deb;
-        bb_bits_window(Ub, (uint32_t)(sty - n - bb_floor16(yn - n)) + offM, u, uwb, ueb);
-        bb_bits_window(Db, (uint32_t)(sty + n - bb_floor16(yn + n)) + offM, dd, dwb, deb);
-        // column edges inside the pair: x = 0 at bit -xc (row y) and n - xc (row y + 1);
-        // x = n - 1 one bit before each: no west / east neighbours there
-        const int64_t b1 = -xc, b2e = n - xc;
-        uint32_t wm = 0u, em = 0u;
-        if ((uint64_t)b1 <= 32u || (uint64_t)b2e <= 32u) {
-            if (b1 >= 0 && b1 < 32) wm |= 1u << b1;
-            if (b2e >= 0 && b2e < 32) wm |= 1u << b2e;
-            if (b1 >= 1 && b1 <= 32) em |= 1u << (b1 - 1);
-            if (b2e >= 1 && b2e <= 32) em |= 1u << (b2e - 1);
+            const uint32_t* Ub = bits + bU * BWS;
+            const uint32_t* Mb = bits + bM * BWS;
+            const uint32_t* Db = bits + bD * BWS;
+            bU = bM;
+            if (!flags[sl_c * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
+            const int64_t sty = bb_floor16(yn);
+            const int d = (int)(sty - yn);  // -15 .. 0
+            const uint32_t* mr = mrow + par * (TPB + 2);
+            uint32_t mem = __funnelshift_r(mr[t], mr[t + 1], (uint32_t)(16 + d));
+            const int64_t c = sty + xs + 32 * (int64_t)t;
+            const int64_t xc = c - yn;  // x of the pair's first byte in row y (< 0: straddles)
+            if (xc < 0)  // strip 0, thread 0: the first -xc bytes end row y - 1
+                mem |= bb_member<16>(p, lt, cc, (uint32_t)(n + xc), (uint32_t)(y - 1)) & ((1u << (-xc)) - 1u);
+            const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
+            if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
+            if (mem == 0u) continue;
+            // the three rows: own 32 cells + the cells west / east of them
+            const uint32_t m = Mb[1 + t], mwb = Mb[t], meb = Mb[t + 2];
+            uint32_t u, uwb, ueb, dd, dwb, deb;
+            bb_bits_window(Ub, (uint32_t)(sty - n - bb_floor16(yn - n)) + offM, u, uwb, ueb);
+            bb_bits_window(Db, (uint32_t)(sty + n - bb_floor16(yn + n)) + offM, dd, dwb, deb);
+            // column edges inside the pair: x = 0 at bit -xc (row y) and n - xc (row y + 1);
+            // x = n - 1 one bit before each: no west / east neighbours there
+            const int64_t b1 = -xc, b2e = n - xc;
+            uint32_t wm = 0u, em = 0u;
+            if ((uint64_t)b1 <= 32u || (uint64_t)b2e <= 32u) {
+                if (b1 >= 0 && b1 < 32) wm |= 1u << b1;
+                if (b2e >= 0 && b2e < 32) wm |= 1u << b2e;
+                if (b1 >= 1 && b1 <= 32) em |= 1u << (b1 - 1);
+                if (b2e >= 1 && b2e <= 32) em |= 1u << (b2e - 1);
+            }
+            const uint32_t mw = ((m << 1) | (mwb >> 31)) & ~wm, me = ((m >> 1) | (meb << 31)) & ~em;
+            uint32_t r;
+            if (p.moore) {
+                const uint32_t uw = ((u << 1) | (uwb >> 31)) & ~wm, ue = ((u >> 1) | (ueb << 31)) & ~em;
+                const uint32_t dw = ((dd << 1) | (dwb >> 31)) & ~wm, de = ((dd >> 1) | (deb << 31)) & ~em;
+                r = apply_rule_bits<CONWAY>(count8(uw, u, ue, mw, me, dw, dd, de), m, KB, KS);
+            } else {
+                r = apply_rule_bits<false>(count8(u, dd, mw, me, 0u, 0u, 0u, 0u), m, KB, KS);
+            }
+            r &= mem;
+            if (mem & 0xFFFFu)
+                *reinterpret_cast<uint4*>(dst + c) = make_uint4(bb_spread4(r), bb_spread4(r >> 4), bb_spread4(r >> 8),
+                                                                bb_spread4(r >> 12));
+            if (mem >> 16)
+                *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(bb_spread4(r >> 16), bb_spread4(r >> 20),
+                                                                     bb_spread4(r >> 24), bb_spread4(r >> 28));
         }
-        const uint32_t mw = ((m << 1) | (mwb >> 31)) & ~wm, me = ((m >> 1) | (meb << 31)) & ~em;
-        uint32_t r;
-        if (p.moore) {
-            const uint32_t uw = ((u << 1) | (uwb >> 31)) & ~wm, ue = ((u >> 1) | (ueb << 31)) & ~em;
-            const uint32_t dw = ((dd << 1) | (dwb >> 31)) & ~wm, de = ((dd >> 1) | (deb << 31)) & ~em;
-            r = apply_rule_bits<CONWAY>(count8(uw, u, ue, mw, me, dw, dd, de), m, KB, KS);
-        } else {
-            r = apply_rule_bits<false>(count8(u, dd, mw, me, 0u, 0u, 0u, 0u), m, KB, KS);
-        }
-        r &= mem;
-        if (mem & 0xFFFFu)
-            *reinterpret_cast<uint4*>(dst + c) = make_uint4(bb_spread4(r), bb_spread4(r >> 4), bb_spread4(r >> 8),
-                                                            bb_spread4(r >> 12));
-        if (mem >> 16)
-            *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(bb_spread4(r >> 16), bb_spread4(r >> 20),
-                                                                 bb_spread4(r >> 24), bb_spread4(r >> 28));
+        bb_cp_wait<0>();
+        __syncthreads();  // the next tile reuses the shared memory
     }
-    bb_cp_wait<0>();
 }
 
 // tile liveness: any fractal cell among the coarse cells covering a tile's output

@@ -649,7 +649,7 @@ void ensure_bb_tables(nbbgpu_t h) {
     const uint64_t nsx = (maxch + 2 * kBBMaxThreads - 1) / (2 * kBBMaxThreads);
     p.cps = (uint32_t)(((maxch + nsx - 1) / nsx + 63) / 64 * 64);  // 2 chunks per thread, whole warps
     uint64_t rows = 64;
-    while (rows > 8 && nsx * (((uint64_t)n + rows - 1) / rows) < 4ull * 148) rows /= 2;
+    while (rows > 8 && nsx * (((uint64_t)n + rows - 1) / rows) < 16ull * 148) rows /= 2;
     p.rows = (uint32_t)rows;
     // live tiles: (strip, band) pairs whose output bytes hold a fractal cell
     const uint64_t nbands = ((uint64_t)n + rows - 1) / rows, ntiles = nsx * nbands;
@@ -679,16 +679,19 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.survive = survive;
     p.moore = moore;
     if (h->bb_ntiles == 0) return;
-    const dim3 grid(h->bb_ntiles);
+    p.ntiles = h->bb_ntiles;
     const uint32_t tpb = p.cps / 2;
     const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)4 * (tpb + 4) * 4 +
                         (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4 + 2 * (tpb + 2) * 4 + kBBStages * (tpb / 32);
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
-    if (conway)
-        step_bb_rows_kernel<true, kBBStages><<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
-    else
-        step_bb_rows_kernel<false, kBBStages><<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+    auto kern = conway ? step_bb_rows_kernel<true, kBBStages> : step_bb_rows_kernel<false, kBBStages>;
+    // persistent CTAs (as many as are resident), each looping over tiles
+    int sms = 148, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)tpb, smem));
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(h->bb_ntiles, (uint64_t)std::max(1, per_sm) * sms));
+    kern<<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
