@@ -189,8 +189,7 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
     for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
-    // persistent CTAs: tiles blockIdx.x, + gridDim.x, ... (no tail wave of whole tiles)
-    for (uint32_t ti = blockIdx.x; ti < p.ntiles; ti += gridDim.x) {
+    for (uint32_t ti = blockIdx.x; ti < p.ntiles; ti += gridDim.x) {  // (one tile per CTA)
         const uint2 tile = tiles[ti];
         const int64_t y0 = (int64_t)tile.y * p.rows;
         const int64_t y1 = min(y0 + (int64_t)p.rows, n);

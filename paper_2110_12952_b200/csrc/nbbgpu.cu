@@ -686,12 +686,9 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
     auto kern = conway ? step_bb_rows_kernel<true, kBBStages> : step_bb_rows_kernel<false, kBBStages>;
-    // persistent CTAs (as many as are resident), each looping over tiles
-    int sms = 148, per_sm = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)tpb, smem));
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(h->bb_ntiles, (uint64_t)std::max(1, per_sm) * sms));
-    kern<<<grid, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+    // one CTA per live tile: the block scheduler balances tiles of unequal work
+    // (persistent CTAs over a static tile order measured slower: carpet r=11 16.8 vs 13.4 ms)
+    kern<<<h->bb_ntiles, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
