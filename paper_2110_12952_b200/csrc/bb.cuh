@@ -189,7 +189,8 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
     for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
-    for (uint32_t ti = blockIdx.x; ti < p.ntiles; ti += gridDim.x) {  // (one tile per CTA)
+    {
+        const uint32_t ti = blockIdx.x;  // one live tile per CTA
         const uint2 tile = tiles[ti];
         const int64_t y0 = (int64_t)tile.y * p.rows;
         const int64_t y1 = min(y0 + (int64_t)p.rows, n);
@@ -361,7 +362,6 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
                                                                      bb_spread4(r >> 24), bb_spread4(r >> 28));
         }
         bb_cp_wait<0>();
-        __syncthreads();  // the next tile reuses the shared memory
     }
 }
 
