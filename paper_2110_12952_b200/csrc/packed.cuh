@@ -430,6 +430,61 @@ __device__ __forceinline__ void halo_bt_task(const PackedStepParams& p, uint32_t
     }
 }
 
+// Many groups (HMODE 7), a warp per group in a grid-stride loop: the (chunk,
+// direction) entry list -- the same for every group -- is staged in shared memory
+// once per block, and the next group's neighbour tiles are loaded while the current
+// group's Bt words are in flight (two dependent round trips per group otherwise).
+constexpr int kBtMaxEntries = kBtMaxChunks * 8;
+__device__ __forceinline__ void halo_bt_groups(const PackedStepParams& p, uint32_t* H, uint64_t wi0,
+                                               uint32_t lane) {
+    __shared__ uint32_t bt_scratch[8][(kBtMaxChunks + 8) * 32];  // 256-thread blocks: acc, neighbour tiles
+    __shared__ uint2 ents[kBtMaxEntries];
+    const uint32_t ne = p.nhent < (uint32_t)kBtMaxEntries ? p.nhent : (uint32_t)kBtMaxEntries;
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) ents[e] = __ldg(reinterpret_cast<const uint2*>(p.hent) + e);
+    __syncthreads();
+    uint32_t* acc = bt_scratch[(threadIdx.x >> 5) & 7];  // [nHc][32]
+    uint32_t* st2 = acc + kBtMaxChunks * 32;            // [8][32]
+    const uint32_t nHc = (p.nH + 31) / 32;
+    const uint64_t nw = (uint64_t)(p.g1 - p.g0);
+    const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t t2n[8];
+    auto fetch = [&](uint64_t wi, uint32_t (&t2)[8]) {
+        const uint32_t t = (p.g0 + (uint32_t)wi) * 32 + lane;
+        const bool in = wi < nw && t < p.T;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) t2[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
+    };
+    fetch(wi0, t2n);
+    for (uint64_t wi = wi0; wi < nw; wi += stride) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) st2[d * 32 + lane] = t2n[d];
+        fetch(wi + stride, t2n);  // next group's neighbour tiles, in flight meanwhile
+        const uint32_t g = p.g0 + (uint32_t)wi;
+        for (uint32_t k = 0; k < nHc; ++k) acc[k * 32 + lane] = 0u;
+        for (uint32_t e0 = 0; e0 < ne; e0 += 8) {
+            uint32_t v[8], kk[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                v[u] = 0u;
+                kk[u] = 0u;
+                if (e0 + u < ne) {
+                    const uint2 en = ents[e0 + u];
+                    kk[u] = en.x >> 8;
+                    const uint32_t tt = st2[(en.x & 0xFFu) * 32 + lane];
+                    if (tt != kNoTile) v[u] = __ldcg(p.bt + ((uint64_t)(tt >> 5) * nHc + kk[u]) * 32 + (tt & 31)) & en.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[kk[u] * 32 + lane] |= v[u];
+        }
+        uint32_t* Hg = H + (uint64_t)g * p.nHp;
+        for (uint32_t k = 0; k < nHc; ++k) {
+            const uint32_t out = warp_transpose32(acc[k * 32 + lane], lane);  // lane i: bit b = slot 32k + i of tile b
+            if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
+        }
+    }
+}
+
 // (group, chunk) tasks for few groups: the chunk's directions only, more warps
 __device__ __forceinline__ void halo_bt_chunk_task(const PackedStepParams& p, uint32_t* H, uint32_t g, uint32_t k,
                                                    uint32_t lane) {
@@ -505,8 +560,8 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
         } else if constexpr (HMODE == 5) {
             halo_bt_task_rolled(p, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 7) {
-            __shared__ uint32_t bt_scratch[8][(kBtMaxChunks + 8) * 32];  // 256-thread blocks
-            halo_bt_task(p, H, p.g0 + (uint32_t)wi, lane, bt_scratch[(threadIdx.x >> 5) & 7]);
+            halo_bt_groups(p, H, wi, lane);  // (the whole grid-stride loop)
+            break;
         } else if constexpr (HMODE == 2) {
             halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 1 || HMODE == 3) {
