@@ -69,7 +69,7 @@ enum { NBBGPU_KERNEL_AUTO = 0, NBBGPU_KERNEL_NAIVE = 1, NBBGPU_KERNEL_TILED = 2,
 
 /* lambda / nu map variants: CUDA-core digit loop, or the paper's matrix form on
  * the tensor cores (exact integer MMA, u8 x u8 -> s32). */
-enum { NBBGPU_MAP_DIGIT = 0, NBBGPU_MAP_MMA = 1 };
+enum { NBBGPU_MAP_DIGIT = 0, NBBGPU_MAP_MMA = 1, NBBGPU_MAP_TC05 = 2 };
 
 const char* nbbgpu_last_error(void);
 int nbbgpu_version(void);
@@ -182,7 +182,9 @@ int nbbgpu_stream(nbbgpu_t h, void** stream);
  *   lambda: in = count (cx, cy) int32 pairs -> out = count (x, y) int32 pairs
  *   nu:     in = count (x, y) pairs -> out = count (cx, cy) pairs, (-1, -1) for a
  *           hole or an out-of-box coordinate.
- * variant = NBBGPU_MAP_DIGIT or NBBGPU_MAP_MMA.  device_ms (optional) receives
+ * variant = NBBGPU_MAP_DIGIT (CUDA-core digit loop), NBBGPU_MAP_MMA (mma.sync u8
+ * tensor cores) or NBBGPU_MAP_TC05 (tcgen05.mma kind::i8, TMEM accumulators; levels
+ * <= 32 for both tensor-core forms).  device_ms (optional) receives
  * the kernel time.  The engine runs on its own stream: device buffers must be
  * complete (caller-side synchronisation) before the call. */
 int nbbgpu_lambda_batch(nbbgpu_t h, int variant, const int32_t* in, int32_t* out, int64_t count,

@@ -21,6 +21,7 @@
 #include "../../include/nbbgpu.h"
 #include "common.cuh"
 #include "maps.cuh"
+#include "tc05.cuh"
 #include "bb.cuh"
 #include "naive.cuh"
 #include "tiled.cuh"
@@ -910,8 +911,9 @@ bool storage_index(nbbgpu_t h, int64_t x, int64_t y, uint64_t& idx) {
 void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, int32_t* out,
                    int64_t count, float* ms) {
     if (count < 0) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "count must be >= 0");
-    if (variant != NBBGPU_MAP_DIGIT && variant != NBBGPU_MAP_MMA) raise(NBBGPU_ERR_INVALID, "unknown map variant");
-    if (variant == NBBGPU_MAP_MMA && h->hf.r > 32) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "MMA maps support levels <= 32");
+    if (variant != NBBGPU_MAP_DIGIT && variant != NBBGPU_MAP_MMA && variant != NBBGPU_MAP_TC05)
+        raise(NBBGPU_ERR_INVALID, "unknown map variant");
+    if (variant != NBBGPU_MAP_DIGIT && h->hf.r > 32) raise(NBBGPU_ERR_OUT_OF_DOMAIN, "MMA maps support levels <= 32");
     if (count == 0) { if (ms) *ms = 0.f; return; }
     const size_t bytes = (size_t)count * 8;
     const bool din = is_device_ptr(in), dout = is_device_ptr(out);
@@ -930,6 +932,18 @@ void run_map_batch(nbbgpu_t h, bool is_lambda, int variant, const int32_t* in, i
 #undef NBB_CALL
         } else {
 #define NBB_CALL(K, S, ...) nu_digit_kernel<K, S><<<grid_for(n, 256), 256, 0, h->stream>>>(h->frac, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        }
+    } else if (variant == NBBGPU_MAP_TC05) {
+        // tcgen05 kind::i8, 128 points per CTA tile, persistent CTAs (several per SM)
+        const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 127) / 128, 148ull * 8));
+        if (is_lambda) {
+#define NBB_CALL(K, S, ...) map_tc05_kernel<K, S, true><<<blocks, 128, 0, h->stream>>>(h->frac, h->mt, dI, dO, n)
+            NBB_DISPATCH_KS(h->hf);
+#undef NBB_CALL
+        } else {
+#define NBB_CALL(K, S, ...) map_tc05_kernel<K, S, false><<<blocks, 128, 0, h->stream>>>(h->frac, h->mt, dI, dO, n)
             NBB_DISPATCH_KS(h->hf);
 #undef NBB_CALL
         }

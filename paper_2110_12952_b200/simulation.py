@@ -23,7 +23,7 @@ from .stencil import Backend, Neighborhood, StencilRule
 DEFAULT_MEMORY_CAP = 2 << 30  # kDefaultMemoryCap, proj/include/nbb/grid.hpp:13
 
 KERNELS = {"auto": 0, "naive": 1, "tiled": 2, "packed": 3, "table": 4}
-MAP_VARIANTS = {"digit": 0, "mma": 1}
+MAP_VARIANTS = {"digit": 0, "mma": 1, "tc05": 2}
 
 
 @dataclass

@@ -1,5 +1,6 @@
-"""lambda / nu batch maps on the GPU, both variants (CUDA-core digit loop and the
-exact-integer tensor-core MMA form), against the C oracle restatement of
+"""lambda / nu batch maps on the GPU, all three variants (CUDA-core digit loop, the
+exact-integer tensor-core form on mma.sync and on tcgen05.mma kind::i8 with TMEM
+accumulators), against the C oracle restatement of
 CoordMapper (maps.cpp:80-146): exhaustive at small levels (acceptance C1-C3
 style), random samples at the large configs."""
 import numpy as np
@@ -37,7 +38,7 @@ def oracle_lambda(o, pts):
     return out
 
 
-@pytest.mark.parametrize("variant", ["digit", "mma"])
+@pytest.mark.parametrize("variant", ["digit", "mma", "tc05"])
 @pytest.mark.parametrize("desc,rmax", [(T, 9), (CARPET, 4), (VICSEK, 5), (H, 4), (Y, 3)])
 def test_maps_exhaustive(desc, rmax, variant):
     for r in range(rmax + 1):
@@ -59,7 +60,7 @@ def test_maps_exhaustive(desc, rmax, variant):
         sim.close()
 
 
-@pytest.mark.parametrize("variant", ["digit", "mma"])
+@pytest.mark.parametrize("variant", ["digit", "mma", "tc05"])
 @pytest.mark.parametrize("desc,r", [(T, 20), (T, 16), (CARPET, 9), (H, 11), (Y, 9)])
 def test_maps_random_large(desc, r, variant):
     o = oracle.Oracle(desc.replicas, desc.k, desc.s, r)
