@@ -87,7 +87,7 @@ def maps_throughput(desc, level, n=1 << 26):
     torch.cuda.synchronize()  # the engine runs on its own stream
     back = torch.empty_like(comp)
     res = {}
-    for variant in ("digit", "mma"):
+    for variant in ("digit", "mma", "tc05"):
         sim.lambda_batch_device(comp.data_ptr(), emb.data_ptr(), n, variant)  # warm
         t_l = sim.lambda_batch_device(comp.data_ptr(), emb.data_ptr(), n, variant)
         sim.nu_batch_device(emb.data_ptr(), back.data_ptr(), n, variant)

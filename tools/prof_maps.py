@@ -1,4 +1,4 @@
-"""Drives the batched lambda / nu map kernels (digit loop and tensor-core MMA) and the
+"""Drives the batched lambda / nu map kernels (digit loop, mma.sync and tcgen05 tensor cores) and the
 paper's per-cell step with both map variants, for ncu (T r=16 / r=20)."""
 import os
 import sys
@@ -19,7 +19,8 @@ comp = torch.stack([torch.randint(0, w, (n,), device="cuda", generator=g),
 emb = torch.empty_like(comp)
 back = torch.empty_like(comp)
 torch.cuda.synchronize()
-for variant in ("digit", "mma"):
+for variant in ("digit", "mma", "tc05"):
+    sim.lambda_batch_device(comp.data_ptr(), emb.data_ptr(), n, variant)  # warm
     t_l = sim.lambda_batch_device(comp.data_ptr(), emb.data_ptr(), n, variant)
     t_n = sim.nu_batch_device(emb.data_ptr(), back.data_ptr(), n, variant)
     torch.cuda.synchronize()
