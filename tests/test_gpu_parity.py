@@ -581,3 +581,26 @@ def test_bench_harness_rows_on_gpu():
     write_csv(recs, s)
     back = read_csv(io.StringIO(s.getvalue()))
     assert [(r.level, r.backend, r.block_size) for r in back] == [(r.level, r.backend, r.block_size) for r in recs]
+
+
+@pytest.mark.parametrize("case", ["T16", "C8", "H8", "Y6", "V7"])
+def test_bb_matches_compact_at_scale(case):
+    # the BB kernel's tile list, hole skipping and row streaming at sizes where the
+    # oracle is slow: its state_hash (layout independent, stencil.cpp:196-234) equals
+    # the packed compact kernel's after every step, Moore and von Neumann
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    Y = FractalDescriptor("y", 12, 4, [(1, 0), (2, 0), (0, 1), (1, 1), (2, 1), (3, 1), (0, 2),
+                                      (1, 2), (2, 2), (3, 2), (1, 3), (2, 3)])
+    desc, r = {"T16": (T, 16), "C8": (CARPET, 8), "H8": (H, 8), "Y6": (Y, 6), "V7": (VICSEK, 7)}[case]
+    bb = Simulation(desc, r, Backend.GpuBoundingBox, SimOptions(memory_cap=1 << 40))
+    cp = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+    for s in (bb, cp):
+        s.seed_random(3, 0.45)
+    assert bb.state_hash() == cp.state_hash()
+    for rule in (conway_rule(), StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)):
+        for _ in range(3):
+            bb.step(rule)
+            cp.step(rule)
+            assert bb.state_hash() == cp.state_hash(), (case, rule.to_string())
+    bb.close()
+    cp.close()
