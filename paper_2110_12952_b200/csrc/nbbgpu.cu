@@ -405,9 +405,6 @@ struct nbbgpu_sim {
     // the front's B was not written (bnd_refresh rebuilds it before any B reader)
     bool bt_front = false;
     bool bnd_stale = false;
-    // step_packed_grid_kernel: double-buffered boundary exchange plane + grid barrier
-    uint32_t* d_gbx = nullptr;
-    unsigned* d_gbar = nullptr;
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -833,8 +830,6 @@ void free_all(nbbgpu_t h) {
     if (h->d_bblow) cudaFree(h->d_bblow);
     if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);
     if (h->d_bbtiles) cudaFree(h->d_bbtiles);
-    if (h->d_gbx) cudaFree(h->d_gbx);
-    if (h->d_gbar) cudaFree(h->d_gbar);
     if (h->d_tab) cudaFree(h->d_tab);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);

@@ -1301,134 +1301,6 @@ step_packed_cluster_kernel(const PackedStepParams p, const uint32_t* __restrict_
 // NVLink (CUDA IPC mappings), then -- after a system-scope fence -- add 1 to the
 // arrival counter of every peer it sends to.  The peer's next halo kernel waits on
 // that counter (wait_peers).  Element e has the same index in every rank's plane.
-// Whole-GPU resident multi-step kernel for mid-size states (T r = 14..16: a few
-// groups per SM): a cooperative launch of one CTA per SM, CTA c owns groups
-// g = c (mod grid) in its shared memory for ALL nsteps steps.  The only data that
-// leaves the SM per step are the groups' boundary words, exchanged through a
-// double-buffered global plane bx[step parity] (L2-resident: a few hundred KB),
-// and one grid barrier per step:
-//   halo words of my groups from bx[par] (ld.global.cg + ballots) -> __syncthreads
-//   -> micro-blocks A -> Bn -> __syncthreads -> my new boundary words to bx[par^1]
-//   -> grid barrier.
-// Records cross HBM only on the first load and the last store (the per-step
-// kernels stream every record through HBM twice per step and pay a launch).
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned* a) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-    return v;
-}
-// sense-free grid barrier: bar[0] arrivals, bar[1] generation (persistent across
-// launches; gen = this CTA's expected generation, read before its first arrival)
-__device__ __forceinline__ void grid_sync(unsigned* bar, uint32_t& gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    ++gen;
-    __syncthreads();
-}
-
-template <bool CONWAY, int DEG, class FT, int P, int WQ>
-__global__ void __launch_bounds__(1024, 1)
-step_packed_grid_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                        uint32_t* __restrict__ bdst, uint32_t* __restrict__ bx, unsigned* __restrict__ gbar,
-                        int nsteps) {
-    using W = Wiring<FT, P>;
-    constexpr int NBLK = BlockGeom<FT, P, WQ>::NBLK;
-    constexpr int NCHUNK = (NBLK + 31) / 32;
-    constexpr int NEP = W::NEP;
-    extern __shared__ __align__(16) uint32_t gsm[];
-    const uint32_t NC = gridDim.x, me = blockIdx.x;
-    const uint32_t NG = p.NG, SWg = p.SW, nH = p.nH, nS = p.nSrc;
-    const uint32_t LG = (NG + NC - 1) / NC;                // local group slots per CTA
-    const uint32_t nmine = me < NG ? (NG - me + NC - 1) / NC : 0u;
-    uint32_t* S0 = gsm;
-    uint32_t* S1 = gsm + LG * SWg;
-    uint32_t* hix = gsm + 2 * LG * SWg;                    // [nmine][nH][32]: bx word << 5 | bit, or ~0u
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    uint32_t gen = 0;
-    if (tid == 0) gen = ld_acquire_gpu(gbar + 1);
-    gen = __shfl_sync(0xFFFFFFFFu, gen, 0);  // (only thread 0 uses it)
-    for (uint32_t i = tid; i < 2 * LG * SWg; i += blockDim.x) {
-        const uint32_t lg = (i / SWg) % LG, w = i % SWg, g = lg * NC + me;
-        gsm[i] = (i < LG * SWg && g < NG && w < p.Cp) ? src[(uint64_t)g * p.Cp + w] : 0u;
-    }
-    for (uint32_t i = tid; i < nmine * nH * 32; i += blockDim.x) {
-        const uint32_t l = i & 31, gj = i >> 5, lg = gj / nH, j = gj - lg * nH, g = lg * NC + me;
-        const uint32_t t = g * 32 + l, sl = __ldg(p.slot + j);
-        const uint32_t t2 = t < p.T ? __ldg(p.ntab + ((size_t)((sl >> 16) & 0xFFu) * p.T + t)) : kNoTile;
-        hix[i] = t2 == kNoTile ? 0xFFFFFFFFu : (((t2 >> 5) * nS + (sl & 0xFFFFu)) << 5) | (t2 & 31);
-    }
-    uint32_t KB[9], KS[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < nmine * nS; i += blockDim.x) {  // boundary words of the first state
-        const uint32_t lg = i / nS, m = i - lg * nS;
-        bx[(uint64_t)(lg * NC + me) * nS + m] = S0[lg * SWg + __ldg(p.srcidx + m)];
-    }
-    grid_sync(gbar, gen);
-    const uint64_t plane = (uint64_t)NG * nS;
-    for (int step = 0; step < nsteps; ++step) {
-        uint32_t* A = (step & 1) ? S1 : S0;
-        uint32_t* Bn = (step & 1) ? S0 : S1;
-        const uint32_t* bxc = bx + (step & 1) * plane;
-        uint32_t* bxn = bx + ((step + 1) & 1) * plane;
-        for (uint32_t task = warp; task < nmine * nH; task += nwarps) {  // halo words of my groups
-            const uint32_t x = hix[task * 32 + lane];
-            const uint32_t bit = x == 0xFFFFFFFFu ? 0u : (__ldcg(bxc + (x >> 5)) >> (x & 31)) & 1u;
-            const uint32_t w = __ballot_sync(0xFFFFFFFFu, bit != 0);
-            if (lane == 0) {
-                const uint32_t lg = task / nH;
-                A[lg * SWg + p.Cp + (task - lg * nH)] = w;
-            }
-        }
-        __syncthreads();
-        for (uint32_t item = warp; item < nmine * NCHUNK; item += nwarps) {
-            const uint32_t lg = item / NCHUNK, c = item - lg * NCHUNK, g = lg * NC + me;
-            const uint32_t blk = c * 32 + lane;
-            if (blk < (uint32_t)NBLK) {
-                uint32_t toff[NEP];
-                const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)blk * (NEP / 4);
-                static_for<NEP / 4>([&](auto e4) {
-                    constexpr int E = decltype(e4)::value;
-                    const uint4 v = __ldg(t4 + E);
-                    toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
-                });
-                const uint32_t vmask = g == NG - 1 ? p.lastmask : 0xFFFFFFFFu;
-                block_words_r<FT, P, WQ, CONWAY, DEG>(reinterpret_cast<const uint8_t*>(A + lg * SWg), toff, blk,
-                                                      Bn + lg * SWg, vmask, KB, KS);
-            }
-        }
-        __syncthreads();
-        for (uint32_t i = tid; i < nmine * nS; i += blockDim.x) {  // my new boundary words
-            const uint32_t lg = i / nS, m = i - lg * nS;
-            bxn[(uint64_t)(lg * NC + me) * nS + m] = Bn[lg * SWg + __ldg(p.srcidx + m)];
-        }
-        grid_sync(gbar, gen);  // every boundary word of the new state is visible
-    }
-    const uint32_t* F = (nsteps & 1) ? S1 : S0;
-    for (uint32_t i = tid; i < nmine * p.Cp; i += blockDim.x) {
-        const uint32_t lg = i / p.Cp, w = i - lg * p.Cp;
-        dst[(uint64_t)(lg * NC + me) * p.Cp + w] = F[lg * SWg + w];
-    }
-    for (uint32_t i = tid; i < nmine * nS; i += blockDim.x) {
-        const uint32_t lg = i / nS, m = i - lg * nS;
-        bdst[(uint64_t)(lg * NC + me) * nS + m] = F[lg * SWg + __ldg(p.srcidx + m)];
-    }
-}
-
 __global__ void p2p_push_kernel(const uint32_t* __restrict__ bnd, const uint64_t* __restrict__ elems,
                                 const uint8_t* __restrict__ peer_of, uint64_t n, uint32_t* const* __restrict__ peer_bnd,
                                 uint32_t* const* __restrict__ peer_cnt, uint32_t send_mask) {

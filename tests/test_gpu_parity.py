@@ -604,26 +604,3 @@ def test_bb_matches_compact_at_scale(case):
             assert bb.state_hash() == cp.state_hash(), (case, rule.to_string())
     bb.close()
     cp.close()
-
-
-@pytest.mark.parametrize("grid", ["0", "1"])
-def test_packed_grid_resident_mid_levels(monkeypatch, grid):
-    # T r=14..16 (a few groups per SM): all steps of a call in one cooperative
-    # launch with the state resident in shared memory and a grid barrier per step
-    # (or the per-step kernels): bytes equal the oracle after each call, any rule
-    monkeypatch.setenv("NBBGPU_GRID", grid)
-    for r, steps in ((14, (5, 1, 8)), (15, (3, 2)), (16, (4,))):
-        o = oracle.Oracle(T.replicas, T.k, T.s, r)
-        o.seed(11 + r, 0.5)
-        sim = Simulation(T, r, Backend.GpuCompact, SimOptions(kernel="packed"))
-        sim.seed_random(11 + r, 0.5)
-        for i, n in enumerate(steps):
-            rule = conway_rule() if i % 2 == 0 else StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)
-            sim.step(rule, n)
-            for _ in range(n):
-                o.step(rule.birth, rule.survive, rule.moore)
-            assert np.array_equal(sim.front().data, o.front), (r, n, grid)
-        if r == 16:
-            _, _, launches = sim.step_profiled(conway_rule(), 20)
-            assert launches == (1 if grid == "1" else 20)
-        sim.close()
