@@ -405,6 +405,15 @@ struct nbbgpu_sim {
     // the front's B was not written (bnd_refresh rebuilds it before any B reader)
     bool bt_front = false;
     bool bnd_stale = false;
+    // multi-step calls: captured CUDA graphs of kGraphSteps steps (step_impl)
+    struct StepGraph {
+        uint16_t birth, survive;
+        int moore, cur, kernel;
+        std::string env;  // the per-call tuning knobs the capture saw
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<StepGraph> graphs;
 
     uint8_t* front() const { return buf[cur]; }
     uint8_t* back() const { return buf[cur ^ 1]; }
@@ -800,9 +809,15 @@ void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
 void free_comm(nbbgpu_t h);           // partition.inc
 void exchange_on_stream(nbbgpu_t h);  // partition.inc
 
+void graphs_clear(nbbgpu_t h) {
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
+}
+
 void free_all(nbbgpu_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
+    graphs_clear(h);
     for (auto*& p : h->buf) if (p) { cudaFree(p); p = nullptr; }
     if (h->d_acc) cudaFree(h->d_acc);
     if (h->d_flag) cudaFree(h->d_flag);
@@ -1144,6 +1159,20 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
     });
 }
 
+constexpr int kGraphSteps = 8;  // steps per captured graph (even: the buffers return to their parity)
+
+// the per-call tuning knobs a captured step sequence depends on
+std::string tuning_env() {
+    std::string e;
+    for (const char* k : {"NBBGPU_HALO_WARPS", "NBBGPU_HALO_GROUP", "NBBGPU_HALO_NCH3", "NBBGPU_HALO_LEAN",
+                          "NBBGPU_HALO_BT", "NBBGPU_BT_OUT", "NBBGPU_NO_PDL", "NBBGPU_GENERIC", "NBBGPU_PACKED_Q"}) {
+        const char* v = getenv(k);
+        e += v ? v : "-";
+        e += ';';
+    }
+    return e;
+}
+
 static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, int64_t nsteps,
                       float* ms, float* main_ms = nullptr, uint64_t* launches = nullptr, bool sync = true) {
     check_handle(h);
@@ -1165,13 +1194,58 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
         if (rk == NBBGPU_KERNEL_PACKED && launch_resident(h, birth, survive, moore, nsteps)) {
             // (all steps on-chip in one single-CTA launch)
         } else {
-            for (int64_t i = 0; i < nsteps; ++i) {
+            auto one_step = [&] {
                 launch_step(h, birth, survive, moore);
                 h->cur ^= 1;
                 ++h->iteration;
                 if (h->p2p) p2p_push(h);             // peer-memory halo of the new front
                 else if (h->comm) exchange_on_stream(h);  // NCCL halo of the new front, on-stream
+            };
+            int64_t i = 0;
+            // Long calls on one GPU: after one plain step (the boundary-plane flags are
+            // then in their steady state), kGraphSteps steps at a time are replayed
+            // from a captured CUDA graph -- one host launch instead of one or two per
+            // step (the host enqueue rate bounds small levels: ~3.4 us per PDL launch).
+            const char* ge = getenv("NBBGPU_GRAPHS");
+            if (!(ge && ge[0] == '0') && !h->p2p && !h->comm && !h->prof && nsteps > kGraphSteps) {
+                one_step();
+                ++i;
+                const std::string env = tuning_env();
+                while (i + kGraphSteps <= nsteps) {
+                    nbbgpu_sim::StepGraph* g = nullptr;
+                    for (auto& e : h->graphs)
+                        if (e.birth == birth && e.survive == survive && e.moore == moore && e.cur == h->cur &&
+                            e.kernel == rk && e.env == env)
+                            g = &e;
+                    if (!g) {  // capture (the host state advances as the captured steps run)
+                        const int cur0 = h->cur;
+                        const uint64_t l0c = h->launches;
+                        cudaGraph_t graph = nullptr;
+                        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+                        try {
+                            for (int k = 0; k < kGraphSteps; ++k) one_step();
+                        } catch (...) {
+                            cudaStreamEndCapture(h->stream, &graph);
+                            if (graph) cudaGraphDestroy(graph);
+                            throw;
+                        }
+                        CK(cudaStreamEndCapture(h->stream, &graph));
+                        cudaGraphExec_t exec = nullptr;
+                        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+                        cudaGraphDestroy(graph);
+                        CK(ie);
+                        h->graphs.push_back({birth, survive, moore, cur0, rk, env, exec, h->launches - l0c});
+                        CK(cudaGraphLaunch(exec, h->stream));  // runs the captured steps
+                        i += kGraphSteps;
+                        continue;
+                    }
+                    CK(cudaGraphLaunch(g->exec, h->stream));
+                    h->launches += g->launches;
+                    h->iteration += kGraphSteps;
+                    i += kGraphSteps;
+                }
             }
+            for (; i < nsteps; ++i) one_step();
         }
     } catch (...) {
         h->prof = nullptr;
@@ -1468,6 +1542,7 @@ int nbbgpu_set_kernel(nbbgpu_t h, int kernel) {
             raise(NBBGPU_ERR_OUT_OF_DOMAIN, "no packed tile level for this fractal/level");
         if (h->nranks > 1 && kernel != h->kernel) raise(NBBGPU_ERR_INVALID, "kernel is fixed once partitioned");
         CK(cudaSetDevice(h->device));
+        graphs_clear(h);
         set_layout(h, layout_of_kernel(resolve_kernel_for(h, kernel)));
         h->kernel = kernel;
     });
