@@ -6,7 +6,7 @@ set -u
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/sanitize; mkdir -p $OUT
 TOOLS=${*:-memcheck synccheck racecheck initcheck}
-CASES=$(python -c "import sys; sys.path.insert(0,'tools'); import sanitize_run as s; print(' '.join(s.CASES))")
+CASES="$(python -c "import sys; sys.path.insert(0,'tools'); import sanitize_run as s; print(' '.join(s.CASES))") maps"
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in $TOOLS; do
   for c in $CASES; do

@@ -31,6 +31,9 @@ CASES = {
     "cluster16": (T, 13, Backend.GpuCompact, "packed", {}, 1),
     "carpet_pws": (C, 6, Backend.GpuCompact, "packed", {}, 1),
     "h_bt": (H, 7, Backend.GpuCompact, "packed", {}, 1),
+    "h_bt_warps": (H, 6, Backend.GpuCompact, "packed", {"NBBGPU_HALO_BT": "1"}, 1),
+    "carpet_bt_warps": (C, 6, Backend.GpuCompact, "packed", {"NBBGPU_HALO_BT": "1"}, 1),
+    "graphs": (T, 12, Backend.GpuCompact, "tiled", {}, 1),
     "candy_split": (Y, 5, Backend.GpuCompact, "packed", {}, 1),
     "jit": (K63, 6, Backend.GpuCompact, "packed", {}, 1),
     "jit_split": (Y, 5, Backend.GpuCompact, "packed", {"NBBGPU_JIT_FORCE": "1"}, 1),
@@ -48,6 +51,8 @@ CASES = {
 
 
 def run(name, steps=3):
+    if name == "graphs":
+        steps = 20  # > 8 steps: captured CUDA graph replay
     desc, level, backend, kernel, env, gpus = CASES[name]
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
@@ -79,9 +84,24 @@ def run(name, steps=3):
     return got == want
 
 
+def run_maps():
+    """the three map variants (digit, mma.sync, tcgen05) against each other"""
+    import numpy as np
+    sim = Simulation(T, 12, Backend.GpuCompact, SimOptions())
+    rng = np.random.default_rng(3)
+    pts = np.stack([rng.integers(0, 4096, 3000), rng.integers(0, 4096, 3000)], 1).astype(np.int32)
+    outs = [sim.nu_batch(pts, v)[0] for v in ("digit", "mma", "tc05")]
+    comp = np.stack([rng.integers(0, 729, 3000), rng.integers(0, 729, 3000)], 1).astype(np.int32)
+    outl = [sim.lambda_batch(comp, v)[0] for v in ("digit", "mma", "tc05")]
+    sim.close()
+    ok = all(np.array_equal(outs[0], o) for o in outs) and all(np.array_equal(outl[0], o) for o in outl)
+    print(f"maps: {'ok' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
 if __name__ == "__main__":
     names = sys.argv[1:] or ["all"]
     if names == ["all"]:
-        names = list(CASES)
-    ok = all([run(n) for n in names])
+        names = list(CASES) + ["maps"]
+    ok = all([run_maps() if n == "maps" else run(n) for n in names])
     sys.exit(0 if ok else 1)
