@@ -1160,6 +1160,7 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
 }
 
 constexpr int kGraphSteps = 8;  // steps per captured graph (even: the buffers return to their parity)
+constexpr int64_t kGraphMaxGroups = 2048;  // packed states replayed from graphs by default
 
 // the per-call tuning knobs a captured step sequence depends on
 std::string tuning_env() {
@@ -1206,8 +1207,12 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
             // then in their steady state), kGraphSteps steps at a time are replayed
             // from a captured CUDA graph -- one host launch instead of one or two per
             // step (the host enqueue rate bounds small levels: ~3.4 us per PDL launch).
+            // Only where the host bounds the step rate: replaying captured launches
+            // loses part of the programmatic (PDL) overlap between the kernels (H r=11:
+            // 0.169 -> 0.189 ms per step), so large states keep stream launches.
             const char* ge = getenv("NBBGPU_GRAPHS");
-            if (!(ge && ge[0] == '0') && !h->p2p && !h->comm && !h->prof && nsteps > kGraphSteps) {
+            const bool small = rk == NBBGPU_KERNEL_PACKED && h->pp.NG <= kGraphMaxGroups;
+            if ((ge ? ge[0] == '1' : small) && !h->p2p && !h->comm && !h->prof && nsteps > kGraphSteps) {
                 one_step();
                 ++i;
                 const std::string env = tuning_env();

@@ -437,12 +437,13 @@ __device__ __forceinline__ void halo_bt_task(const PackedStepParams& p, uint32_t
 constexpr int kBtMaxEntries = kBtMaxChunks * 8;
 __device__ __forceinline__ void halo_bt_groups(const PackedStepParams& p, uint32_t* H, uint64_t wi0,
                                                uint32_t lane) {
-    __shared__ uint32_t bt_scratch[8][8 * 32];  // 256-thread blocks: per warp, the neighbour tiles
+    __shared__ uint32_t bt_scratch[8][(kBtMaxChunks + 8) * 32];  // 256-thread blocks: acc, neighbour tiles
     __shared__ uint2 ents[kBtMaxEntries];
     const uint32_t ne = p.nhent < (uint32_t)kBtMaxEntries ? p.nhent : (uint32_t)kBtMaxEntries;
     for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) ents[e] = __ldg(reinterpret_cast<const uint2*>(p.hent) + e);
     __syncthreads();
-    uint32_t* st2 = bt_scratch[(threadIdx.x >> 5) & 7];  // [8][32] neighbour tiles
+    uint32_t* acc = bt_scratch[(threadIdx.x >> 5) & 7];  // [nHc][32]
+    uint32_t* st2 = acc + kBtMaxChunks * 32;            // [8][32]
     const uint32_t nHc = (p.nH + 31) / 32;
     const uint64_t nw = (uint64_t)(p.g1 - p.g0);
     const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -459,20 +460,13 @@ __device__ __forceinline__ void halo_bt_groups(const PackedStepParams& p, uint32
         for (int d = 0; d < 8; ++d) st2[d * 32 + lane] = t2n[d];
         fetch(wi + stride, t2n);  // next group's neighbour tiles, in flight meanwhile
         const uint32_t g = p.g0 + (uint32_t)wi;
-        uint32_t* Hg = H + (uint64_t)g * p.nHp;
-        // the entries are sorted by chunk: one running word per chunk in a register,
-        // transposed and stored when the chunk changes (8 loads in flight per batch)
-        uint32_t cur_k = 0, word = 0;
-        auto flush = [&](uint32_t k, uint32_t w) {
-            const uint32_t out = warp_transpose32(w, lane);  // lane i: bit b = slot 32k + i of tile b
-            if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
-        };
+        for (uint32_t k = 0; k < nHc; ++k) acc[k * 32 + lane] = 0u;
         for (uint32_t e0 = 0; e0 < ne; e0 += 8) {
             uint32_t v[8], kk[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 v[u] = 0u;
-                kk[u] = cur_k;
+                kk[u] = 0u;
                 if (e0 + u < ne) {
                     const uint2 en = ents[e0 + u];
                     kk[u] = en.x >> 8;
@@ -481,16 +475,13 @@ __device__ __forceinline__ void halo_bt_groups(const PackedStepParams& p, uint32
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (kk[u] != cur_k) {  // (uniform across the warp)
-                    flush(cur_k, word);
-                    word = 0u;
-                    cur_k = kk[u];
-                }
-                word |= v[u];
-            }
+            for (int u = 0; u < 8; ++u) acc[kk[u] * 32 + lane] |= v[u];
         }
-        if (ne) flush(cur_k, word);
+        uint32_t* Hg = H + (uint64_t)g * p.nHp;
+        for (uint32_t k = 0; k < nHc; ++k) {
+            const uint32_t out = warp_transpose32(acc[k * 32 + lane], lane);  // lane i: bit b = slot 32k + i of tile b
+            if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
+        }
     }
 }
 
