@@ -99,3 +99,26 @@ def test_large_configs_kernel_agreement(monkeypatch, case):
             assert sims["packed"].state_hash() == sims["tiled"].state_hash(), (case, n)
     for s in sims.values():
         s.close()
+
+
+@pytest.mark.parametrize("case", ["h11", "c10", "k12"])
+def test_long_calls_graphs_and_wide_halos_agree(monkeypatch, case):
+    # many steps per call at full size: the >= 8192-group wide-halo gather, the bt
+    # warps' transposed plane and the captured-graph replay (forced) against the
+    # tiled byte kernel and against stream launches, with a rule switch mid-run
+    from paper_2110_12952_b200.descriptor import FractalDescriptor
+    desc, level = {
+        "h11": (FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)]), 11),
+        "c10": (builtin_descriptor("sierpinski-carpet"), 10),
+        "k12": (FractalDescriptor("k6s3", 6, 3, [(0, 0), (1, 0), (2, 0), (0, 1), (1, 2), (2, 2)]), 11),
+    }[case]
+    hashes = {}
+    for label, kernel, graphs in (("tiled", "tiled", "0"), ("stream", "packed", "0"), ("graphs", "packed", "1")):
+        monkeypatch.setenv("NBBGPU_GRAPHS", graphs)
+        s = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel=kernel, memory_cap=1 << 42))
+        s.seed_random(5, 0.5)
+        s.step(conway_rule(), 19)
+        s.step(StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann), 10)
+        hashes[label] = s.state_hash()
+        s.close()
+    assert hashes["stream"] == hashes["tiled"] == hashes["graphs"], (case, hashes)
