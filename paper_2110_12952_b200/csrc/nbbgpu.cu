@@ -1222,6 +1222,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
                         if (e.birth == birth && e.survive == survive && e.moore == moore && e.cur == h->cur &&
                             e.kernel == rk && e.env == env)
                             g = &e;
+                    if (!g && nsteps - i < 4 * kGraphSteps) break;  // (short call: not worth a capture)
                     if (!g) {  // capture (the host state advances as the captured steps run)
                         const int cur0 = h->cur;
                         const uint64_t l0c = h->launches;
