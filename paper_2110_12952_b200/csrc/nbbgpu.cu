@@ -362,6 +362,11 @@ struct nbbgpu_sim {
     uint32_t* d_pcnt = nullptr;             // my arrival counter (exported by IPC)
     uint32_t p2p_epoch = 0, p2p_nsrc = 0, p2p_send_mask = 0;
     uint64_t* d_p2p_elems = nullptr;        // boundary elements peers need from me
+    // fused push (triangle step kernels): per owned group its (slot | peer << 16) entries
+    uint32_t* d_push_off = nullptr;
+    uint32_t* d_push_ent = nullptr;
+    unsigned* d_push_done = nullptr;
+    bool fused_push = false;                // the last step kernel pushed and signalled
     uint8_t* d_p2p_peer = nullptr;          // ... and which peer
     uint64_t p2p_n = 0;
     uint32_t** d_peer_bnd[2] = {nullptr, nullptr};  // per rank: mapped boundary planes
@@ -857,6 +862,9 @@ void free_all(nbbgpu_t h) {
     h->ipc_opened.clear();
     if (h->d_pcnt) cudaFree(h->d_pcnt);
     if (h->d_p2p_elems) cudaFree(h->d_p2p_elems);
+    if (h->d_push_off) cudaFree(h->d_push_off);
+    if (h->d_push_ent) cudaFree(h->d_push_ent);
+    if (h->d_push_done) cudaFree(h->d_push_done);
     if (h->d_p2p_peer) cudaFree(h->d_p2p_peer);
     for (auto*& q : h->d_peer_bnd) if (q) { cudaFree(q); q = nullptr; }
     if (h->d_peer_cnt) cudaFree(h->d_peer_cnt);
@@ -1199,7 +1207,10 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
                 launch_step(h, birth, survive, moore);
                 h->cur ^= 1;
                 ++h->iteration;
-                if (h->p2p) p2p_push(h);             // peer-memory halo of the new front
+                if (h->p2p) {                        // peer-memory halo of the new front
+                    if (h->fused_push) ++h->p2p_epoch;  // (pushed and signalled by the step kernel)
+                    else p2p_push(h);
+                }
                 else if (h->comm) exchange_on_stream(h);  // NCCL halo of the new front, on-stream
             };
             int64_t i = 0;

@@ -97,6 +97,16 @@ struct PackedStepParams {
     // transposed plane Bt (layout of bnd_transpose_kernel) straight from the output
     // record -- no transpose kernel, no boundary-plane round trip (nullptr: write B)
     uint32_t* bt_out;
+    // peer-memory transport, fused push (triangle kernels, nSrc <= 32): the boundary
+    // words peers need are stored into their planes as each group finishes
+    // (push_off[local group] .. +1: entries m | peer << 16), and the grid's last CTA
+    // bumps every peer's arrival counter once (push_done: CTA count of this launch)
+    const uint32_t* push_off;
+    const uint32_t* push_ent;
+    uint32_t* const* push_bnd;  // per rank: its plane of the new front's parity
+    uint32_t* const* push_cnt;  // per rank: its arrival counter
+    unsigned* push_done;
+    uint32_t push_mask;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
@@ -861,6 +871,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // round trip per group
     constexpr bool PWS = BST && W::BH == 1;
     static_assert(!PWS || NO % NGRP == 0, "per-warp stores reuse an output buffer every NO / NGRP groups");
+    __shared__ unsigned push_warps_done;  // fused peer push: pushing warps finished
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
@@ -887,6 +898,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     static_assert(BTW == 0 || (BTO && HW == 0), "bt warps need per-warp stores, one CTA per record");
     static_assert(BTW % NGRP == 0, "bt warps are split evenly over the group sets");
     constexpr int BTS = BTW / NGRP > 0 ? BTW / NGRP : 1;  // bt warps per group set
+    if (tid == 0) push_warps_done = 0u;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(full0 + 8 * s, HW > 0 ? 2 : 1);  // producer (+ bytes) [+ the halo warp]
@@ -1102,14 +1114,45 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             }
             continue;
         }
-        if (!BST && c == 0 && half == 0)  // boundary plane of the new state (few words)
-            for (uint32_t m = lane; m < p.nSrc; m += 32)
-                bdst[(uint64_t)g * p.nSrc + m] = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+        if (!BST && c == 0 && half == 0) {  // boundary plane of the new state (few words)
+            uint32_t mine = 0u;
+            for (uint32_t m = lane; m < p.nSrc; m += 32) {
+                mine = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
+                bdst[(uint64_t)g * p.nSrc + m] = mine;
+            }
+            if (p.push_off) {  // (nSrc <= 32: lane m holds word m) straight into the peers' planes
+                const uint32_t k0 = __ldg(p.push_off + (g - p.g0)), k1 = __ldg(p.push_off + (g - p.g0) + 1);
+                for (uint32_t kb = k0; kb < k1; kb += 32) {
+                    const uint32_t k = kb + (uint32_t)lane;
+                    const uint32_t e = k < k1 ? __ldg(p.push_ent + k) : 0u;
+                    const uint32_t v = __shfl_sync(0xFFFFFFFFu, mine, e & 31u);
+                    if (k < k1) p.push_bnd[e >> 16][(uint64_t)g * p.nSrc + (e & 0xFFFFu)] = v;
+                }
+            }
+        }
         fence_proxy_async_smem();  // the bulk store reads Do through the async proxy
         __syncwarp();
         if (lane == 0) {
             mbar_arrive(empty0 + 8 * s);
             mbar_arrive(ofull0 + 8 * o);
+        }
+    }
+    if (!BST && p.push_off && c == 0 && half == 0) {
+        // this warp's pushes are done: the CTA's last pushing warp counts the CTA, the
+        // grid's last CTA bumps every peer's counter (system-scope fences in between:
+        // each writer fences before its count, the last one before the bumps)
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) {
+            if (atomicAdd(&push_warps_done, 1u) == (unsigned)(NGRP - 1)) {
+                __threadfence_system();
+                if (atomicAdd(p.push_done, 1u) == gridDim.x - 1) {
+                    atomicExch(p.push_done, 0u);
+                    __threadfence_system();
+                    for (uint32_t r = 0; r < 32; ++r)
+                        if ((p.push_mask >> r) & 1u) atomicAdd_system(p.push_cnt[r], 1u);
+                }
+            }
         }
     }
     if constexpr (PWS)
