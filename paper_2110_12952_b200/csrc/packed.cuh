@@ -871,11 +871,11 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // round trip per group
     constexpr bool PWS = BST && W::BH == 1;
     static_assert(!PWS || NO % NGRP == 0, "per-warp stores reuse an output buffer every NO / NGRP groups");
-    __shared__ unsigned push_warps_done;  // fused peer push: pushing warps finished
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
-    uint8_t* st = sm + 16 * (NS + NO);
+    unsigned& push_warps_done = *reinterpret_cast<unsigned*>(sm + 16 * (NS + NO));  // fused peer push
+    uint8_t* st = sm + 16 * (NS + NO) + 16;
     // SPLIT = 2: each CTA stages only the rows its blocks read (the row window
     // p.win0[half] + [0, p.win_words) of the record; the plan rebases the block
     // tables to it)
