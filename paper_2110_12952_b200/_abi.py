@@ -11,7 +11,8 @@ import os
 from .errors import STATUS_TO_ERROR, NbbError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libnbbgpu.so")
+# NBBGPU_LIB (A/B measurements only): another build of the same library
+SO_PATH = os.environ.get("NBBGPU_LIB") or os.path.join(HERE, "libnbbgpu.so")
 
 # name -> (restype, argtypes); mirrors include/nbbgpu.h
 _P = C.POINTER

@@ -851,8 +851,10 @@ struct WsGeom {
 // BTW > 0 (per-warp-store kernels on one GPU, p.bt_out): BTW extra warps write the
 // transposed boundary plane Bt (bnd_transpose_kernel's layout) from each finished
 // output record -- no transpose kernel and no boundary-plane round trip per step.
+// PUSH (peer-memory transport, triangle): the boundary words peers need are stored
+// into their planes here and the grid's last CTA signals them (p.push_*).
 template <bool CONWAY, int DEG, bool WIDE, class FT, int P, int WQ, int NGRP, int NS, int NO, int SPLIT = 1,
-          int HW = 0, int BTW = 0>
+          int HW = 0, int BTW = 0, bool PUSH = false>
 __global__ void __launch_bounds__((WsGeom<FT, P, WQ, SPLIT>::NCHUNK * NGRP + 2 + HW + BTW) * 32, 1)
 step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                        const uint32_t* __restrict__ bsrc, uint32_t* __restrict__ bdst) {
@@ -1120,7 +1122,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 mine = cell_word<CONWAY, DEG, WIDE>(Sb, p.nbr, __ldg(p.srcidx + m), KB, KS) & vmask;
                 bdst[(uint64_t)g * p.nSrc + m] = mine;
             }
-            if (p.push_off) {  // (nSrc <= 32: lane m holds word m) straight into the peers' planes
+            if constexpr (PUSH) {  // (nSrc <= 32: lane m holds word m) straight into the peers' planes
                 const uint32_t k0 = __ldg(p.push_off + (g - p.g0)), k1 = __ldg(p.push_off + (g - p.g0) + 1);
                 for (uint32_t kb = k0; kb < k1; kb += 32) {
                     const uint32_t k = kb + (uint32_t)lane;
@@ -1137,7 +1139,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             mbar_arrive(ofull0 + 8 * o);
         }
     }
-    if (!BST && p.push_off && c == 0 && half == 0) {
+    if constexpr (PUSH && !BST) if (c == 0 && half == 0) {
         // this warp's pushes are done: the CTA's last pushing warp counts the CTA, the
         // grid's last CTA bumps every peer's counter (system-scope fences in between:
         // each writer fences before its count, the last one before the bumps)
