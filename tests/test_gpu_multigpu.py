@@ -36,8 +36,12 @@ def _compare(desc, level, n, rule, steps, seed=7):
     multi.close()
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("n", [2, 3, 8])
-def test_multigpu_matches_single(n):
+def test_multigpu_matches_single(monkeypatch, n, fused):
+    # fused: the triangle B3/S23 step kernels push the peers' boundary words and
+    # signal them in-kernel; "0": the separate push kernel after every step
+    monkeypatch.setenv("NBBGPU_FUSED_PUSH", fused)
     _compare(T, 12, n, conway_rule(), 6)                     # q=6: in-kernel halo + counters
     _compare(T, 17, n, conway_rule(), 4)                     # q=8
     _compare(CARPET, 5, n, conway_rule(), 5)                 # halo kernel, interleaved records
