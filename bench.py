@@ -171,6 +171,17 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's own compact step (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------
+def workload_config(level):
+    """The workload (identical for both arms: the driver compares the config dicts);
+    how each arm runs it goes under "engine"."""
+    cells = 3 ** level
+    return {"workload": f"sierpinski-triangle K(2^{level},3,2) r={level} compact, B3/S23 Moore "
+                        "(BASELINE.json configs[3]; north-star target)",
+            "level": level, "compact_cells": cells, "seed": SEED, "density": DENSITY,
+            "l2": (f"inputs larger than L2 ({cells / 1e9:.2f} GB of reference bytes; "
+                   f"{(cells + 7) // 8 / 1e9:.2f} GB per packed buffer vs 126 MB L2): no flush")}
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as fh:
@@ -274,8 +285,9 @@ def run_reference(args):
             "steps": steps, "warmup": warmup, "ms_per_step": res["seconds_per_sample"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seed 42, density 0.5)", "impl": "reference",
-            "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore",
-                       "level": args.level, "parallelism": "host threads"},
+            "config": workload_config(args.level),
+            "engine": {"impl": "oracle/_ref: the unmodified reference sources (-O3 -DNDEBUG)",
+                       "parallelism": f"{res['cores']} host threads (parallel_for split)"},
             "cpu_baseline": dict({k: res[k] for k in CPU_KEYS if k in res}, value=value),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -456,15 +468,12 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None,
         "dtype": "u32 bit-sliced (1 bit per cell, 32 tiles per word)" if packed else "u8",
         "data": "synthetic: seed_random(42, 0.5) generated on the device (rng.hpp cell_alive)",
-        "config": {"workload": f"sierpinski-triangle K(2^{args.level},3,2) r={args.level} compact, B3/S23 Moore "
-                               "(BASELINE.json configs[3]; north-star target)",
-                   "level": args.level, "compact_cells": cells, "kernel": f"{kern} (tile level q={q})",
+        "config": workload_config(args.level),
+        "engine": {"kernel": f"{kern} (tile level q={q})",
                    "parallelism": (f"partitioned x{ws} over {n} GPU(s), halo transport {dsim.transport}"
                                    if dsim is not None else "single GPU"),
                    "partitions": ws,
-                   "state_bytes_per_buffer": (cells + 7) // 8 if packed else cells,
-                   "l2": (f"state {((cells + 7) // 8 if packed else cells) / 1e9:.2f} GB per buffer vs 126 MB L2: "
-                          "inputs larger than L2, no flush")},
+                   "state_bytes_per_buffer": (cells + 7) // 8 if packed else cells},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "model": ("packed: 2 bits (read own + write next state, 1 bit each) per compact "

@@ -35,8 +35,8 @@ def test_multirank_bench_matches_single(nproc):  # torch.distributed point-to-po
     multi = _bench(nproc, 14, 29517 + nproc)
     assert multi["final_state_hash"] == single["final_state_hash"]
     # ranks sharing cuda:0: one GPU stepped, nproc partitions
-    assert multi["n_gpus"] == 1 and multi["config"]["partitions"] == nproc
-    assert "packed" in multi["config"]["kernel"]
+    assert multi["n_gpus"] == 1 and multi["engine"]["partitions"] == nproc
+    assert "packed" in multi["engine"]["kernel"]
 
 
 @pytest.mark.parametrize("nproc", [2, 3])
@@ -53,7 +53,7 @@ def test_multirank_p2p_transport_matches_single(nproc):
 
 def test_multirank_auto_transport_picks_p2p():
     out = _bench(2, 12, 29817, transport="auto")
-    assert "halo transport p2p" in out["config"]["parallelism"]
+    assert "halo transport p2p" in out["engine"]["parallelism"]
     assert out["final_state_hash"] == _bench(1, 12, 0)["final_state_hash"]
 
 
@@ -65,7 +65,7 @@ def test_bench_gpus_without_torchrun_relaunches():
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
-    assert line["n_gpus"] == 1 and line["config"]["partitions"] == 2
+    assert line["n_gpus"] == 1 and line["engine"]["partitions"] == 2
     assert line["final_state_hash"] == _bench(1, 14, 0)["final_state_hash"]
 
 
