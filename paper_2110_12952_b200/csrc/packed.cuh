@@ -523,9 +523,11 @@ template <int HMODE, int SPW = 4, bool NC = true>
 __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __restrict__ bsrc,
                                   uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
-    pdl_wait();     // bsrc comes from the previous step kernel
-    wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
-    pdl_trigger();  // the step kernel may launch and run its prologue
+    if constexpr (HMODE != 8) {
+        pdl_wait();     // bsrc comes from the previous step kernel
+        wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
+        pdl_trigger();  // the step kernel may launch and run its prologue
+    }
     const uint64_t nw = HMODE == 6 ? (uint64_t)(p.g1 - p.g0) * ((p.nH + 31) / 32)
                       : HMODE == 2 || HMODE == 5 || HMODE == 7 ? (uint64_t)(p.g1 - p.g0)
                       : HMODE == 1 || HMODE == 3 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
@@ -541,13 +543,27 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
             noff[j] = ((sl >> 16) & 0xFFu) * p.T;
             moff[j] = sl & 0xFFFFu;
         }
-        for (uint32_t g = p.g0 + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); g < p.g1;
-             g += (uint32_t)(((uint64_t)gridDim.x * blockDim.x) >> 5)) {
-            const uint32_t t = g * 32 + lane;
-            const bool in = t < p.T;
+        // the neighbour tiles (static ntab) of this warp's first group are loaded
+        // before the wait for the previous step kernel (PDL: overlaps its tail), and
+        // each next group's while the current group's boundary words are in flight
+        const uint32_t gstride = (uint32_t)(((uint64_t)gridDim.x * blockDim.x) >> 5);
+        uint32_t g = p.g0 + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+        uint32_t t2n[8];
+        auto fetch = [&](uint32_t gg) {
+            const uint32_t t = gg * 32 + lane;
+            const bool in = gg < p.g1 && t < p.T;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t2n[j] = ((uint32_t)j < p.nH && in) ? __ldg(p.ntab + noff[j] + t) : kNoTile;
+        };
+        fetch(g);
+        pdl_wait();     // bsrc comes from the previous step kernel
+        wait_peers(p);  // ... and, with the peer-memory transport, from the peers' pushes
+        pdl_trigger();  // the step kernel may launch and run its prologue
+        for (; g < p.g1; g += gstride) {
             uint32_t t2[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) t2[j] = ((uint32_t)j < p.nH && in) ? __ldg(p.ntab + noff[j] + t) : kNoTile;
+            for (int j = 0; j < 8; ++j) t2[j] = t2n[j];
+            fetch(g + gstride);
             uint32_t v[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
