@@ -70,30 +70,6 @@ __device__ __forceinline__ bool bb_coarse_bit(const BBCoarse& c, uint32_t cx, ui
     return (c.last >> ry) & 1u;
 }
 
-// membership bits of cells (x .. x+NB-1, y), NB = 16 or 32, 0 <= x, y < n; bits at
-// x' >= n are 0.  S >= 32 > NB: the run meets at most two coarse cells.
-template <int NB>
-__device__ __forceinline__ uint32_t bb_member(const BBRowParams& p, const uint32_t* lt, const BBCoarse& cc,
-                                              uint32_t x, uint32_t y) {
-    const uint32_t cx = bb_div(p, x), cy = bb_div(p, y);
-    const uint32_t xl = x - cx * p.S, yl = y - cy * p.S;
-    const uint32_t* row = lt + yl * p.lt_words;
-    const uint32_t w = xl >> 5;
-    constexpr uint32_t ALL = NB == 32 ? 0xFFFFFFFFu : (1u << NB) - 1u;
-    uint32_t bits = __funnelshift_r(row[w], row[w + 1], xl & 31) & ALL;  // doubled row: no wrap
-    const uint32_t split = p.S - xl;  // bits >= split lie in coarse cell cx + 1
-    uint32_t keep = bb_coarse_bit(cc, cx, cy) ? ALL : 0u;
-    if (split < (uint32_t)NB) {
-        const uint32_t lo = (1u << split) - 1u;
-        const bool c1 = cx + 1 < p.CW && bb_coarse_bit(cc, cx + 1, cy);
-        keep = (keep & lo) | (c1 ? (~lo & ALL) : 0u);
-    }
-    bits &= keep;
-    const uint64_t left = p.n - x;
-    if (left < (uint64_t)NB) bits &= (1u << left) - 1u;
-    return bits;
-}
-
 // does row y hold a fractal cell in [x0, x0 + 1024)?  (coarse test, x0 >= 0; a
 // conservative "yes" when the range reaches past the row)
 __device__ __forceinline__ bool bb_run_live(const BBRowParams& p, const BBCoarse& cc, int64_t x0, int64_t y) {
@@ -167,7 +143,7 @@ __device__ __host__ __forceinline__ void bb_tile_cover(const BBRowParams& p, uin
 // only for the two 16-byte stores.
 template <bool CONWAY, int NS>
 __global__ void __launch_bounds__(kBBMaxThreads, 8)
-step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const uint32_t* __restrict__ lowtab,
+step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const uint32_t* __restrict__ memb,
                     const uint32_t* __restrict__ coarse, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
     static_assert(NS >= 5, "rows y+3.. in flight while row y+2 is packed");
     constexpr int NB = 4;  // bit ring: rows y-1 .. y+2
@@ -175,11 +151,11 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
     const uint32_t W = (p.cps + 4) * 16;  // byte slot
     const int TPB = blockDim.x, NW = TPB >> 5;
     const uint32_t BWS = (uint32_t)TPB + 4;  // bit slot words (+ pad for the shifted windows)
+    const uint32_t MWS = (uint32_t)TPB + 4;  // membership words per slot
     uint32_t* bits = reinterpret_cast<uint32_t*>(sm + NS * W);    // [NB][BWS]
-    uint32_t* lt = bits + NB * BWS;
-    uint32_t* ccw = lt + p.S * p.lt_words;
-    uint32_t* mrow = ccw + kBBCacheWords;                         // [2][TPB + 2]
-    uint8_t* flags = reinterpret_cast<uint8_t*>(mrow + 2 * (TPB + 2));  // [NS][NW]
+    uint32_t* mslot = bits + NB * BWS;                            // [NS][MWS] membership bits of the slot
+    uint32_t* ccw = mslot + NS * MWS;
+    uint8_t* flags = reinterpret_cast<uint8_t*>(ccw + kBBCacheWords);  // [NS][NW]
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t n = (int64_t)p.n;
     uint32_t KB[9], KS[9];
@@ -188,180 +164,188 @@ step_bb_rows_kernel(const BBRowParams p, const uint2* __restrict__ tiles, const 
         KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
         KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
     }
-    for (uint32_t i = t; i < p.S * p.lt_words; i += TPB) lt[i] = __ldg(lowtab + i);
+    const uint2 tile = tiles[blockIdx.x];  // one live tile per CTA
+    const int64_t y0 = (int64_t)tile.y * p.rows;
+    const int64_t y1 = min(y0 + (int64_t)p.rows, n);
+    const int64_t xs = (int64_t)tile.x * p.cps * 16;  // strip offset within an aligned row
+    BBCoarse cc;  // (the hole-skip test)
+    uint32_t cy1;
+    bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
+    cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 2;
+    cc.bits = ccw;
+    cc.last = 0;
+    for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += TPB) {
+        const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
+        const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
+        const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
+        uint32_t v = 0;
+        if (32 * k < ncols) {
+            v = __funnelshift_r(__ldg(coarse + (b0 >> 5)), __ldg(coarse + (b0 >> 5) + 1), (uint32_t)(b0 & 31));
+            const uint32_t left = ncols - 32 * k;
+            if (left < 32) v &= (1u << left) - 1u;
+        }
+        ccw[i] = v;
+    }
+    for (uint32_t i = t; i < NB * BWS; i += TPB) bits[i] = 0u;
+    __syncthreads();
+
+    // row rho (-1 .. n) -> the next byte slot; thread t loads chunks 2t+2, 2t+3 of
+    // the segment, thread 0 also the margin chunks 0, 1 and thread 1 cps+2, cps+3,
+    // and the segment's membership words (static bitmap, bit i = linear byte i).
+    // A warp whose own 64 chunks are holes loads nothing and flags the slot.
+    const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
+    const int64_t mwords = ((int64_t)p.alloc + 31) / 32;
+    auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
+        uint8_t* slot = sm + sl * W;
+        const int64_t base = bb_floor16(rn) + xs - 32;
+        const int64_t x0 = bb_floor16(rn) + wx - rn;
+        const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
+        if (lane == 0) flags[sl * NW + warp] = live;
+        // (the whole segment inside the buffer: no per-chunk bounds)
+        const bool inside = base >= 0 && base + (int64_t)W <= (int64_t)p.alloc;
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(slot);
+        auto one = [&](uint32_t ch) {
+            const int64_t a = base + 16 * (int64_t)ch;
+            const bool in = inside || (a >= 0 && a + 16 <= (int64_t)p.alloc);
+            bb_cp_async16(sbase + 16 * ch, in ? src + a : src, in ? 16u : 0u);
+        };
+        if (live) {
+            one(2 * (uint32_t)t + 2);
+            one(2 * (uint32_t)t + 3);
+        }
+        if (t < 2) {
+            one(t == 0 ? 0u : p.cps + 2);
+            one(t == 0 ? 1u : p.cps + 3);
+        }
+        // membership words floor32(base) / 32 + k, k = 0 .. TPB + 2 (thread t: k = t, and
+        // threads 0..2 also k = TPB .. TPB + 2)
+        const int64_t w0 = (base >= 0 ? base : base - 31) / 32;
+        const uint32_t mbase = (uint32_t)__cvta_generic_to_shared(mslot + sl * MWS);
+        for (int k = t; k < TPB + 3; k += TPB) {
+            const int64_t w = w0 + k;
+            const bool in = w >= 0 && w < mwords;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(mbase + 4u * (uint32_t)k),
+                         "l"(in ? memb + w : memb), "r"(in ? 4u : 0u)
+                         : "memory");
+        }
+    };
+    // the thread's own 32 bytes of byte slot sl -> bit word of bit slot bl
+    auto pack_row = [&](int sl, int bl) {
+        const uint8_t* slot = sm + sl * W;
+        uint32_t* brow = bits + bl * BWS;
+        if (flags[sl * NW + warp]) {
+            const uint4* v = reinterpret_cast<const uint4*>(slot + 32 + 32 * t);
+            brow[1 + t] = bb_pack32(v[0], v[1]);
+        } else {
+            brow[1 + t] = 0u;
+        }
+        if (t < 2) {
+            const uint4* v = reinterpret_cast<const uint4*>(slot + (t == 0 ? 0u : 16 * (p.cps + 2)));
+            brow[t == 0 ? 0 : TPB + 1] = bb_pack32(v[0], v[1]);
+        }
+    };
+
+    // prologue: rows y0-1 .. y0+NS-3 in flight, rows y0-1 .. y0+1 packed
     {
-        const uint32_t ti = blockIdx.x;  // one live tile per CTA
-        const uint2 tile = tiles[ti];
-        const int64_t y0 = (int64_t)tile.y * p.rows;
-        const int64_t y1 = min(y0 + (int64_t)p.rows, n);
-        const int64_t xs = (int64_t)tile.x * p.cps * 16;  // strip offset within an aligned row
-        BBCoarse cc;
-        uint32_t cy1;
-        bb_tile_cover(p, tile.x, tile.y, NS, cc.cy0, cy1, cc.cx0, cc.cx1);
-        cc.wpr = (cc.cx1 - cc.cx0 + 1 + 31) / 32 + 2;
-        cc.bits = ccw;
-        cc.last = 0;
-        for (uint32_t ry = 0; ry <= cy1 - cc.cy0; ++ry) {
-            const uint64_t b = (uint64_t)(cc.cy0 + ry) * p.CW + p.CW - 1;
-            cc.last |= ((__ldg(coarse + (b >> 5)) >> (b & 31)) & 1u) << ry;
-        }
-        for (uint32_t i = t; i < (cy1 - cc.cy0 + 1) * cc.wpr; i += TPB) {
-            const uint32_t ry = i / cc.wpr, k = i % cc.wpr;
-            const uint64_t b0 = (uint64_t)(cc.cy0 + ry) * p.CW + cc.cx0 + 32ull * k;  // first bit of word k
-            const uint32_t ncols = cc.cx1 - cc.cx0 + 1;
-            uint32_t v = 0;
-            if (32 * k < ncols) {
-                v = __funnelshift_r(__ldg(coarse + (b0 >> 5)), __ldg(coarse + (b0 >> 5) + 1), (uint32_t)(b0 & 31));
-                const uint32_t left = ncols - 32 * k;
-                if (left < 32) v &= (1u << left) - 1u;
-            }
-            ccw[i] = v;
-        }
-        for (uint32_t i = t; i < NB * BWS; i += TPB) bits[i] = 0u;
-        __syncthreads();
-
-
-        // row rho (-1 .. n) -> the next byte slot; thread t loads chunks 2t+2, 2t+3 of
-        // the segment, thread 0 also the margin chunks 0, 1 and thread 1 cps+2, cps+3.
-        // A warp whose own 64 chunks are holes loads nothing and flags the slot.
-        const int64_t wx = xs + (int64_t)warp * 1024;  // the warp's first byte past floor16(rho n)
-        auto load_row = [&](int64_t rho, int64_t rn, int sl) {  // rn = rho * n
-            uint8_t* slot = sm + sl * W;
-            const int64_t base = bb_floor16(rn) + xs - 32;
-            const int64_t x0 = bb_floor16(rn) + wx - rn;
-            const bool live = rho < 0 || rho >= n || x0 < 0 || bb_run_live(p, cc, x0, rho);
-            if (lane == 0) flags[sl * NW + warp] = live;
-            // (the whole segment inside the buffer: no per-chunk bounds)
-            const bool inside = base >= 0 && base + (int64_t)W <= (int64_t)p.alloc;
-            const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(slot);
-            auto one = [&](uint32_t ch) {
-                const int64_t a = base + 16 * (int64_t)ch;
-                const bool in = inside || (a >= 0 && a + 16 <= (int64_t)p.alloc);
-                bb_cp_async16(sbase + 16 * ch, in ? src + a : src, in ? 16u : 0u);
-            };
-            if (live) {
-                one(2 * (uint32_t)t + 2);
-                one(2 * (uint32_t)t + 3);
-            }
-            if (t < 2) {
-                one(t == 0 ? 0u : p.cps + 2);
-                one(t == 0 ? 1u : p.cps + 3);
-            }
-        };
-        // the thread's own 32 bytes of byte slot sl -> bit word of bit slot bl
-        auto pack_row = [&](int sl, int bl) {
-            const uint8_t* slot = sm + sl * W;
-            uint32_t* brow = bits + bl * BWS;
-            if (flags[sl * NW + warp]) {
-                const uint4* v = reinterpret_cast<const uint4*>(slot + 32 + 32 * t);
-                brow[1 + t] = bb_pack32(v[0], v[1]);
-            } else {
-                brow[1 + t] = 0u;
-            }
-            if (t < 2) {
-                const uint4* v = reinterpret_cast<const uint4*>(slot + (t == 0 ? 0u : 16 * (p.cps + 2)));
-                brow[t == 0 ? 0 : TPB + 1] = bb_pack32(v[0], v[1]);
-            }
-        };
-        // membership bits of row y for x in [xs - 16 + 32k, +32), k = 0 .. TPB (a warp
-        // whose row is holes only writes the word lane 31 of the warp before reads)
-        auto mask_row = [&](int64_t y, uint32_t* m, bool live) {
-            if (y >= y1) return;
-            for (int k = t; k <= TPB; k += TPB) {
-                if (!live && k < TPB && lane != 0) {
-                    m[k] = 0u;
-                    continue;
-                }
-                const int64_t x0 = xs - 16 + 32 * (int64_t)k;
-                uint32_t v = 0;
-                if (x0 < 0) v = bb_member<32>(p, lt, cc, 0u, (uint32_t)y) << 16;  // strip 0: x0 = -16
-                else if (x0 < n) v = bb_member<32>(p, lt, cc, (uint32_t)x0, (uint32_t)y);
-                m[k] = v;
-            }
-        };
-
-        // prologue: rows y0-1 .. y0+NS-3 in flight, rows y0-1 .. y0+1 packed
-        {
-            int64_t rn = (y0 - 1) * n;
-            for (int i = 0; i < NS - 1; ++i, rn += n) {
-                load_row(y0 - 1 + i, rn, i);
-                bb_cp_commit();
-            }
-        }
-        __syncwarp();  // lane 0's live flags
-        bb_cp_wait<NS - 4>();  // rows y0-1 .. y0+1 (this thread's copies)
-        for (int i = 0; i < 3; ++i) pack_row(i, i);
-        mask_row(y0, mrow, flags[1 % NS * NW + warp] != 0);
-        int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
-        int sl_y = 1 % NS;     // byte slot of row y (row y0 - 1 is in slot 0)
-        int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
-        int64_t yn = y0 * n;
-        int64_t rn_load = (y0 + NS - 2) * n;
-        const uint32_t offM = 32 + 32 * t;  // the thread's cells in a segment (bit offset == byte offset)
-        for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
-            bb_cp_wait<NS - 5>();  // row y + 2 landed (this thread's copies)
-            __syncthreads();       // rows <= y + 1 packed; slots of rows y - 2 free
-            load_row(y + NS - 2, rn_load, sl_load);
-            sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
+        int64_t rn = (y0 - 1) * n;
+        for (int i = 0; i < NS - 1; ++i, rn += n) {
+            load_row(y0 - 1 + i, rn, i);
             bb_cp_commit();
-            const int sl_c = sl_y;  // byte slot of row y (its live flags)
-            sl_y = sl_y + 1 == NS ? 0 : sl_y + 1;
-            const int sl2 = sl_c + 2 >= NS ? sl_c + 2 - NS : sl_c + 2;  // byte slot of row y + 2
-            const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
-            pack_row(sl2, b2);
-            const int par = (int)((y - y0) & 1);
-            const int sl1 = sl_c + 1 == NS ? 0 : sl_c + 1;  // byte slot of row y + 1
-            mask_row(y + 1, mrow + (par ^ 1) * (TPB + 2), flags[sl1 * NW + warp] != 0);
-
-            const uint32_t* Ub = bits + bU * BWS;
-            const uint32_t* Mb = bits + bM * BWS;
-            const uint32_t* Db = bits + bD * BWS;
-            bU = bM;
-            if (!flags[sl_c * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
-            const int64_t sty = bb_floor16(yn);
-            const int d = (int)(sty - yn);  // -15 .. 0
-            const uint32_t* mr = mrow + par * (TPB + 2);
-            uint32_t mem = __funnelshift_r(mr[t], mr[t + 1], (uint32_t)(16 + d));
-            const int64_t c = sty + xs + 32 * (int64_t)t;
-            const int64_t xc = c - yn;  // x of the pair's first byte in row y (< 0: straddles)
-            if (xc < 0)  // strip 0, thread 0: the first -xc bytes end row y - 1
-                mem |= bb_member<16>(p, lt, cc, (uint32_t)(n + xc), (uint32_t)(y - 1)) & ((1u << (-xc)) - 1u);
-            const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
-            if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
-            if (mem == 0u) continue;
-            // the three rows: own 32 cells + the cells west / east of them
-            const uint32_t m = Mb[1 + t], mwb = Mb[t], meb = Mb[t + 2];
-            uint32_t u, uwb, ueb, dd, dwb, deb;
-            bb_bits_window(Ub, (uint32_t)(sty - n - bb_floor16(yn - n)) + offM, u, uwb, ueb);
-            bb_bits_window(Db, (uint32_t)(sty + n - bb_floor16(yn + n)) + offM, dd, dwb, deb);
-            // column edges inside the pair: x = 0 at bit -xc (row y) and n - xc (row y + 1);
-            // x = n - 1 one bit before each: no west / east neighbours there
-            const int64_t b1 = -xc, b2e = n - xc;
-            uint32_t wm = 0u, em = 0u;
-            if ((uint64_t)b1 <= 32u || (uint64_t)b2e <= 32u) {
-                if (b1 >= 0 && b1 < 32) wm |= 1u << b1;
-                if (b2e >= 0 && b2e < 32) wm |= 1u << b2e;
-                if (b1 >= 1 && b1 <= 32) em |= 1u << (b1 - 1);
-                if (b2e >= 1 && b2e <= 32) em |= 1u << (b2e - 1);
-            }
-            const uint32_t mw = ((m << 1) | (mwb >> 31)) & ~wm, me = ((m >> 1) | (meb << 31)) & ~em;
-            uint32_t r;
-            if (p.moore) {
-                const uint32_t uw = ((u << 1) | (uwb >> 31)) & ~wm, ue = ((u >> 1) | (ueb << 31)) & ~em;
-                const uint32_t dw = ((dd << 1) | (dwb >> 31)) & ~wm, de = ((dd >> 1) | (deb << 31)) & ~em;
-                r = apply_rule_bits<CONWAY>(count8(uw, u, ue, mw, me, dw, dd, de), m, KB, KS);
-            } else {
-                r = apply_rule_bits<false>(count8(u, dd, mw, me, 0u, 0u, 0u, 0u), m, KB, KS);
-            }
-            r &= mem;
-            if (mem & 0xFFFFu)
-                *reinterpret_cast<uint4*>(dst + c) = make_uint4(bb_spread4(r), bb_spread4(r >> 4), bb_spread4(r >> 8),
-                                                                bb_spread4(r >> 12));
-            if (mem >> 16)
-                *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(bb_spread4(r >> 16), bb_spread4(r >> 20),
-                                                                     bb_spread4(r >> 24), bb_spread4(r >> 28));
         }
-        bb_cp_wait<0>();
+    }
+    __syncwarp();  // lane 0's live flags
+    bb_cp_wait<NS - 4>();  // rows y0-1 .. y0+1 (this thread's copies)
+    for (int i = 0; i < 3; ++i) pack_row(i, i);
+    int sl_load = NS - 1;  // byte slot of the next row to load (y0 + NS - 2)
+    int sl_y = 1 % NS;     // byte slot of row y (row y0 - 1 is in slot 0)
+    int bU = 0;            // bit slot of row y - 1 (rows map to bit slots in order)
+    int64_t yn = y0 * n;
+    int64_t rn_load = (y0 + NS - 2) * n;
+    const uint32_t offM = 32 + 32 * t;  // the thread's cells in a segment (bit offset == byte offset)
+    for (int64_t y = y0; y < y1; ++y, yn += n, rn_load += n) {
+        bb_cp_wait<NS - 5>();  // row y + 2 landed (this thread's copies)
+        __syncthreads();       // rows <= y + 1 packed (and their membership words landed); slots of rows y - 2 free
+        load_row(y + NS - 2, rn_load, sl_load);
+        sl_load = sl_load + 1 == NS ? 0 : sl_load + 1;
+        bb_cp_commit();
+        const int sl_c = sl_y;  // byte slot of row y (its live flags, its membership words)
+        sl_y = sl_y + 1 == NS ? 0 : sl_y + 1;
+        const int sl2 = sl_c + 2 >= NS ? sl_c + 2 - NS : sl_c + 2;  // byte slot of row y + 2
+        const int bM = bU + 1 == NB ? 0 : bU + 1, bD = bM + 1 == NB ? 0 : bM + 1, b2 = bD + 1 == NB ? 0 : bD + 1;
+        pack_row(sl2, b2);
+
+        const uint32_t* Ub = bits + bU * BWS;
+        const uint32_t* Mb = bits + bM * BWS;
+        const uint32_t* Db = bits + bD * BWS;
+        bU = bM;
+        if (!flags[sl_c * NW + warp]) continue;  // warp-uniform: 1024 hole bytes stay 0
+        const int64_t sty = bb_floor16(yn);
+        // the pair's membership: bits (32 + 32 t + (base & 31)) of the slot's words,
+        // base = the slot's first byte (floor16: its bit offset in word 0 is 0 or 16)
+        const uint32_t* ms = mslot + sl_c * MWS;
+        const uint32_t sh = (uint32_t)((sty + xs - 32) & 31);
+        uint32_t mem = __funnelshift_r(ms[1 + t], ms[2 + t], sh);
+        const int64_t c = sty + xs + 32 * (int64_t)t;
+        const int64_t xc = c - yn;  // x of the pair's first byte in row y (< 0: straddles)
+        const int64_t end = y == n - 1 ? (n * n + 15) & ~(int64_t)15 : bb_floor16(yn + n);
+        if (c + 16 >= end) mem &= c >= end ? 0u : 0xFFFFu;
+        if (mem == 0u) continue;
+        // the three rows: own 32 cells + the cells west / east of them
+        const uint32_t m = Mb[1 + t], mwb = Mb[t], meb = Mb[t + 2];
+        uint32_t u, uwb, ueb, dd, dwb, deb;
+        bb_bits_window(Ub, (uint32_t)(sty - n - bb_floor16(yn - n)) + offM, u, uwb, ueb);
+        bb_bits_window(Db, (uint32_t)(sty + n - bb_floor16(yn + n)) + offM, dd, dwb, deb);
+        // column edges inside the pair: x = 0 at bit -xc (row y) and n - xc (row y + 1);
+        // x = n - 1 one bit before each: no west / east neighbours there
+        const int64_t b1 = -xc, b2e = n - xc;
+        uint32_t wm = 0u, em = 0u;
+        if ((uint64_t)b1 <= 32u || (uint64_t)b2e <= 32u) {
+            if (b1 >= 0 && b1 < 32) wm |= 1u << b1;
+            if (b2e >= 0 && b2e < 32) wm |= 1u << b2e;
+            if (b1 >= 1 && b1 <= 32) em |= 1u << (b1 - 1);
+            if (b2e >= 1 && b2e <= 32) em |= 1u << (b2e - 1);
+        }
+        const uint32_t mw = ((m << 1) | (mwb >> 31)) & ~wm, me = ((m >> 1) | (meb << 31)) & ~em;
+        uint32_t r;
+        if (p.moore) {
+            const uint32_t uw = ((u << 1) | (uwb >> 31)) & ~wm, ue = ((u >> 1) | (ueb << 31)) & ~em;
+            const uint32_t dw = ((dd << 1) | (dwb >> 31)) & ~wm, de = ((dd >> 1) | (deb << 31)) & ~em;
+            r = apply_rule_bits<CONWAY>(count8(uw, u, ue, mw, me, dw, dd, de), m, KB, KS);
+        } else {
+            r = apply_rule_bits<false>(count8(u, dd, mw, me, 0u, 0u, 0u, 0u), m, KB, KS);
+        }
+        r &= mem;
+        if (mem & 0xFFFFu)
+            *reinterpret_cast<uint4*>(dst + c) = make_uint4(bb_spread4(r), bb_spread4(r >> 4), bb_spread4(r >> 8),
+                                                            bb_spread4(r >> 12));
+        if (mem >> 16)
+            *reinterpret_cast<uint4*>(dst + c + 16) = make_uint4(bb_spread4(r >> 16), bb_spread4(r >> 20),
+                                                                 bb_spread4(r >> 24), bb_spread4(r >> 28));
+    }
+    bb_cp_wait<0>();
+}
+
+// membership bitmap of the box (static, built once per handle): bit i of word w =
+// linear byte 32 w + i is a fractal cell (0 past n^2)
+__global__ void bb_member_bitmap_kernel(const BBRowParams p, const uint32_t* __restrict__ lowtab,
+                                        const uint32_t* __restrict__ coarse, uint32_t* __restrict__ out,
+                                        uint64_t nwords) {
+    const uint64_t cells = p.n * p.n;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint64_t i = w * 32 + b;
+            if (i >= cells) break;
+            const uint32_t x = (uint32_t)(i % p.n), y = (uint32_t)(i / p.n);
+            const uint32_t cx = bb_div(p, x), cy = bb_div(p, y);
+            const uint32_t xl = x - cx * p.S, yl = y - cy * p.S;
+            const bool lo = (__ldg(lowtab + yl * p.lt_words + (xl >> 5)) >> (xl & 31)) & 1u;
+            const uint64_t cb = (uint64_t)cy * p.CW + cx;
+            const bool hi = (__ldg(coarse + (cb >> 5)) >> (cb & 31)) & 1u;
+            v |= (uint32_t)(lo && hi) << b;
+        }
+        out[w] = v;
     }
 }
 

@@ -322,6 +322,7 @@ struct nbbgpu_sim {
     uint32_t* d_bblow = nullptr;
     uint32_t* d_bbcoarse = nullptr;
     uint2* d_bbtiles = nullptr;     // live (strip, band) tiles
+    uint32_t* d_bbmemb = nullptr;   // membership bitmap of the box (bit = linear byte)
     uint32_t bb_ntiles = 0;
     BBRowParams bbp{};
     bool bb_ready = false;
@@ -682,6 +683,13 @@ void ensure_bb_tables(nbbgpu_t h) {
     for (uint64_t i = 0; i < ntiles; ++i)
         if (live[i]) tiles.push_back(make_uint2((uint32_t)(i % nsx), (uint32_t)(i / nsx)));
     h->bb_ntiles = (uint32_t)tiles.size();
+    // static membership bitmap (n^2 / 8 bytes + pad): one 32-bit load per 32 cells
+    // per row instead of the per-row membership evaluation
+    const uint64_t mwords = (p.alloc + 31) / 32;
+    dmalloc_cap(h->d_bbmemb, mwords * 4, "bounding-box membership bitmap");
+    h->bytes_held += mwords * 4;
+    bb_member_bitmap_kernel<<<grid_for(mwords, 256), 256, 0, h->stream>>>(p, h->d_bblow, h->d_bbcoarse, h->d_bbmemb, mwords);
+    CK(cudaGetLastError());
     dmalloc_cap(h->d_bbtiles, std::max<size_t>(1, tiles.size()) * sizeof(uint2), "bounding-box tile list");
     if (!tiles.empty()) CK(cudaMemcpy(h->d_bbtiles, tiles.data(), tiles.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     h->bb_ready = true;
@@ -697,13 +705,13 @@ void launch_bb_rows(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
     p.ntiles = h->bb_ntiles;
     const uint32_t tpb = p.cps / 2;
     const size_t smem = (size_t)kBBStages * (p.cps + 4) * 16 + (size_t)4 * (tpb + 4) * 4 +
-                        (size_t)p.S * p.lt_words * 4 + kBBCacheWords * 4 + 2 * (tpb + 2) * 4 + kBBStages * (tpb / 32);
+                        (size_t)kBBStages * (tpb + 4) * 4 + kBBCacheWords * 4 + kBBStages * (tpb / 32);
     const bool conway = (birth & 0x1FF) == 0x8 && (survive & 0x1FF) == 0xC && moore;
     if (smem > 48 * 1024) raise(NBBGPU_ERR_CUDA, "internal: bounding-box row ring exceeds 48 KB");  // s <= 16
     auto kern = conway ? step_bb_rows_kernel<true, kBBStages> : step_bb_rows_kernel<false, kBBStages>;
     // one CTA per live tile: the block scheduler balances tiles of unequal work
     // (persistent CTAs over a static tile order measured slower: carpet r=11 16.8 vs 13.4 ms)
-    kern<<<h->bb_ntiles, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bblow, h->d_bbcoarse, h->front(), h->back());
+    kern<<<h->bb_ntiles, tpb, smem, h->stream>>>(p, h->d_bbtiles, h->d_bbmemb, h->d_bbcoarse, h->front(), h->back());
 }
 
 void launch_step(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore) {
@@ -850,6 +858,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_bblow) cudaFree(h->d_bblow);
     if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);
     if (h->d_bbtiles) cudaFree(h->d_bbtiles);
+    if (h->d_bbmemb) cudaFree(h->d_bbmemb);
     if (h->d_tab) cudaFree(h->d_tab);
     if (h->d_blocktab) cudaFree(h->d_blocktab);
     for (auto* p : h->d_sends) if (p) cudaFree(p);
