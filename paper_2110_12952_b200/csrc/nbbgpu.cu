@@ -1177,7 +1177,11 @@ int nbbgpu_seed(nbbgpu_t h, uint64_t seed, double density) {
 }
 
 constexpr int kGraphSteps = 8;  // steps per captured graph (even: the buffers return to their parity)
-constexpr int64_t kGraphMaxGroups = 2048;  // packed states replayed from graphs by default
+// packed states replayed from graphs by default: up to 2^24 cells the device step
+// (<= ~4.5 us) is shorter than the host's ~3.4 us per PDL launch plus overheads
+// (T r=14 4.11 -> 3.85 us/step); above, graphs only lose PDL overlap (T r=16 6.3 ->
+// 7.0 us/step, H r=11 0.169 -> 0.189 ms)
+constexpr uint64_t kGraphMaxCells = 1ull << 24;
 
 // the per-call tuning knobs a captured step sequence depends on
 std::string tuning_env() {
@@ -1231,7 +1235,7 @@ static void step_impl(nbbgpu_t h, uint16_t birth, uint16_t survive, int moore, i
             // loses part of the programmatic (PDL) overlap between the kernels (H r=11:
             // 0.169 -> 0.189 ms per step), so large states keep stream launches.
             const char* ge = getenv("NBBGPU_GRAPHS");
-            const bool small = rk == NBBGPU_KERNEL_PACKED && h->pp.NG <= kGraphMaxGroups;
+            const bool small = rk == NBBGPU_KERNEL_PACKED && h->cells <= kGraphMaxCells;
             if ((ge ? ge[0] == '1' : small) && !h->p2p && !h->comm && !h->prof && nsteps > kGraphSteps) {
                 one_step();
                 ++i;
