@@ -187,6 +187,32 @@ __device__ __forceinline__ void halo4_task(const PackedStepParams& p, const uint
 
 // 32 x 32 bit transpose across a warp: lane i holds row i (bit k = column k) ->
 // lane k holds column k (bit i = row i).  Five shuffle-xor block swaps.
+// XposeLane: the lane's keep masks and rotate amounts, built once before a loop of
+// transposes (the bt warps of the H kernel: step kernel 116 -> 108 us at r=11; the
+// same instruction count, the carpet kernel's schedule loses 6 % with it).
+struct XposeLane {
+    uint32_t K[5], sh[5];
+    __device__ __forceinline__ explicit XposeLane(uint32_t lane) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int j = 16 >> q;
+            const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                                     : j == 2 ? 0x33333333u : 0x55555555u;
+            const bool hi = (lane & j) != 0;
+            K[q] = hi ? ~m : m;
+            sh[q] = hi ? 32 - j : j;
+        }
+    }
+};
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const XposeLane& X) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, 16 >> q);
+        const uint32_t r = __funnelshift_l(y, y, X.sh[q]);
+        x = (x & X.K[q]) | (r & ~X.K[q]);
+    }
+    return x;
+}
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
     // per stage: shuffle, rotate (left by j in the low-half lanes, right by j in the
     // high-half lanes: the wrapped-in bits fall under the mask) and a bit select
@@ -403,42 +429,7 @@ __device__ __forceinline__ void halo_bt_task_rolled(const PackedStepParams& p, u
     }
 }
 
-// Many groups: the nonzero (chunk, direction) pairs come from p.hent (the same for every group),
-// 8 loads in flight per round trip; per-lane accumulators and neighbour tiles live
-// in this warp's shared scratch (sw: kBtMaxChunks + 8 words per lane).
 constexpr int kBtMaxChunks = 16;
-__device__ __forceinline__ void halo_bt_task(const PackedStepParams& p, uint32_t* H, uint32_t g, uint32_t lane,
-                                             uint32_t* sw) {
-    const uint32_t t = g * 32 + lane;
-    const bool in = t < p.T;
-    const uint32_t nHc = (p.nH + 31) / 32;
-    uint32_t* acc = sw;                   // [nHc][32]
-    uint32_t* st2 = sw + kBtMaxChunks * 32;  // [8][32]
-#pragma unroll
-    for (int d = 0; d < 8; ++d) st2[d * 32 + lane] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
-    for (uint32_t k = 0; k < nHc; ++k) acc[k * 32 + lane] = 0u;
-    for (uint32_t e0 = 0; e0 < p.nhent; e0 += 8) {
-        uint32_t v[8], kk[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            v[u] = 0u;
-            kk[u] = 0u;
-            if (e0 + u < p.nhent) {
-                const uint2 en = __ldg(reinterpret_cast<const uint2*>(p.hent) + e0 + u);
-                kk[u] = en.x >> 8;
-                const uint32_t t2 = st2[(en.x & 0xFFu) * 32 + lane];
-                if (t2 != kNoTile) v[u] = __ldcg(p.bt + ((uint64_t)(t2 >> 5) * nHc + kk[u]) * 32 + (t2 & 31)) & en.y;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[kk[u] * 32 + lane] |= v[u];
-    }
-    uint32_t* Hg = H + (uint64_t)g * p.nHp;
-    for (uint32_t k = 0; k < nHc; ++k) {
-        const uint32_t out = warp_transpose32(acc[k * 32 + lane], lane);  // lane i: bit b = slot 32k + i of tile b
-        if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
-    }
-}
 
 // Many groups (HMODE 7), a warp per group in a grid-stride loop: the (chunk,
 // direction) entry list -- the same for every group -- is staged in shared memory
@@ -889,6 +880,14 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // round trip per group
     constexpr bool PWS = BST && W::BH == 1;
     static_assert(!PWS || NO % NGRP == 0, "per-warp stores reuse an output buffer every NO / NGRP groups");
+    // Every stage must belong to ONE group set.  mbarrier waits are by phase parity:
+    // a set waiting for use u + 1 of a stage whose use u (another set's group) has
+    // not landed yet would see the parity of use u - 1 and pass early -- rare (the
+    // TMA of use u completing after later ones), but it corrupted one warp's slice of
+    // one group about once per 10^4 group-steps with NGRP 3 / NS 7.  With NS a
+    // multiple of NGRP, stage s serves groups i = s (mod NS), all of set s % NGRP,
+    // which that set consumes in order, so use u has completed before it waits for u + 1.
+    static_assert(NS % NGRP == 0, "stages are partitioned over the group sets");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
@@ -1003,6 +1002,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             // blocking between sets), chunks w / NGRP, + BTS, ...
             const uint32_t w = (uint32_t)(warp - NCW - 2), set = w % NGRP, b = w / NGRP;
             const uint32_t nHc = (p.nSrc + 31) / 32;
+            const XposeLane X((uint32_t)lane);
             uint32_t i = set;
             for (uint32_t g = p.g0 + pair + set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
                 const uint32_t o = i % NO;
@@ -1011,7 +1011,10 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 for (uint32_t k = b; k < nHc; k += BTS) {
                     const uint32_t m = 32 * k + (uint32_t)lane;
                     const uint32_t x = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
-                    p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, (uint32_t)lane);
+                    if constexpr (std::is_same<FT, HTag>::value)
+                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, X);
+                    else
+                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, (uint32_t)lane);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(oempty0 + 8 * o);  // release: buffer o read
