@@ -523,6 +523,12 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
                       : HMODE == 2 || HMODE == 5 || HMODE == 7 ? (uint64_t)(p.g1 - p.g0)
                       : HMODE == 1 || HMODE == 3 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
                                    : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
+    if constexpr (HMODE == 7) {
+        // every warp of the block enters (the entry list is staged by the whole block
+        // behind a __syncthreads, also in a last block with fewer groups than warps)
+        halo_bt_groups(p, H, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, lane);
+        return;
+    }
     if constexpr (HMODE == 8) {
         // small halos (nH <= 8), warp per group, lean: the slot table is hoisted out
         // of the task loop (uniform), 32-bit offsets, 8 + 8 independent loads and 8
@@ -569,6 +575,7 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
         }
         return;
     }
+    if constexpr (HMODE != 7 && HMODE != 8)
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         if constexpr (HMODE == 6) {
@@ -576,9 +583,6 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
             halo_bt_chunk_task(p, H, p.g0 + gi, w32 - gi * nHc, lane);
         } else if constexpr (HMODE == 5) {
             halo_bt_task_rolled(p, H, p.g0 + (uint32_t)wi, lane);
-        } else if constexpr (HMODE == 7) {
-            halo_bt_groups(p, H, wi, lane);  // (the whole grid-stride loop)
-            break;
         } else if constexpr (HMODE == 2) {
             halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 1 || HMODE == 3) {
