@@ -892,6 +892,9 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // multiple of NGRP, stage s serves groups i = s (mod NS), all of set s % NGRP,
     // which that set consumes in order, so use u has completed before it waits for u + 1.
     static_assert(NS % NGRP == 0, "stages are partitioned over the group sets");
+    // (the in-kernel halo warps wait on the stages' empty barriers the same way: each
+    // stage served by one halo warp, or one set whose consumers finish groups in order)
+    static_assert(HW == 0 || NS % HW == 0 || NGRP == 1, "stages are partitioned over the halo warps");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;

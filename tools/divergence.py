@@ -1,6 +1,7 @@
 """Where two runs of the same seeded state part ways: python tools/divergence.py [FRACTAL:LEVEL] [steps]
+(several FRACTAL:LEVEL:STEPS arguments sweep configurations in one process)
 
-Replays tools/quick_bench.py's preamble (other states created, stepped and freed in
+With DIV_PREAMBLE=1 first replays tools/quick_bench.py's preamble (other states created, stepped and freed in
 the same process), then steps three handles of FRACTAL:LEVEL in lockstep -- A through
 step_profiled, B through step, R on the table-driven program (NBBGPU_JIT=0) -- and
 at the first hash mismatch reports the differing compact cells (tile, group, local
@@ -30,11 +31,18 @@ def make(f, level, env=None):
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1].count(":") == 2:  # sweep
+        for case in sys.argv[1:]:
+            f, level, steps = case.split(":")
+            lockstep(f, int(level), int(steps))
+        return
     f, level = (sys.argv[1] if len(sys.argv) > 1 else "K:12").split(":")
-    level = int(level)
-    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 60
+    lockstep(f, int(level), int(sys.argv[2]) if len(sys.argv) > 2 else 60)
+
+
+def lockstep(f, level, steps):
     rule = conway_rule()
-    if not os.environ.get("DIV_NO_PREAMBLE"):
+    if os.environ.get("DIV_PREAMBLE"):
         for case in ("T:20", "H:11", "H:10", "C:10", "C:11", "C:9"):
             pf, pl = case.split(":")
             s = make(pf, int(pl))
@@ -43,8 +51,8 @@ def main():
             s.step_timed(rule, 50)
             s.step_profiled(rule, 50)
             s.close()
-    A, B, R = make(f, level), make(f, level), make(f, level, {"NBBGPU_JIT": "0"})
-    print("programs", A.packed_program(), B.packed_program(), R.packed_program(), flush=True)
+    A, B, R = make(f, level), make(f, level), make(f, level, {"NBBGPU_JIT": "0", "NBBGPU_GENERIC": "1"})
+    print(f"{f}:{level} programs", A.packed_program(), B.packed_program(), R.packed_program(), flush=True)
     for s in (A, B, R):
         s.seed_random(42, 0.5)
     d = DESCS[f]
@@ -71,7 +79,9 @@ def main():
                       f"local {list(zip((x % wq)[:10].tolist(), (y % wq)[:10].tolist()))}", flush=True)
         break
     else:
-        print(f"no divergence in {steps} steps ({ha:016x})", flush=True)
+        print(f"{f}:{level} no divergence in {steps} steps ({ha:016x})", flush=True)
+    for s in (A, B, R):
+        s.close()
 
 
 if __name__ == "__main__":
