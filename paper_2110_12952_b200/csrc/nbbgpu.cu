@@ -7,8 +7,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <thread>
 #include <cstring>
 #include <exception>
 #include <map>
@@ -332,6 +338,13 @@ struct nbbgpu_sim {
     int64_t iteration = 0;
     unsigned long long* d_acc = nullptr;
     int* d_flag = nullptr;
+    // host <-> device bit-array staging (hostconv.inc): pinned host + device chunk
+    // buffers, a copy stream, per-buffer copy / conversion events
+    uint32_t* xb_host[2] = {nullptr, nullptr};
+    uint32_t* xb_dev[2] = {nullptr, nullptr};
+    uint64_t xb_words = 0;
+    cudaStream_t xb_stream = nullptr;
+    cudaEvent_t xb_dma[2] = {nullptr, nullptr}, xb_conv[2] = {nullptr, nullptr};
     int kernel = NBBGPU_KERNEL_AUTO;
     int map_variant = NBBGPU_MAP_DIGIT;
     uint64_t bytes_held = 0;
@@ -535,6 +548,7 @@ void smem_attr(nbbgpu_t h, K kern, int bytes, bool nonportable_cluster = false) 
     if (nonportable_cluster) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
+#include "hostconv.inc"
 #include "packed_host.inc"
 
 template <int WQ, int K, int S, bool CONWAY>
@@ -834,6 +848,14 @@ void free_all(nbbgpu_t h) {
     for (auto*& p : h->buf) if (p) { cudaFree(p); p = nullptr; }
     if (h->d_acc) cudaFree(h->d_acc);
     if (h->d_flag) cudaFree(h->d_flag);
+    if (h->xb_stream) cudaStreamSynchronize(h->xb_stream);
+    for (int i = 0; i < 2; ++i) {
+        if (h->xb_host[i]) cudaFreeHost(h->xb_host[i]);
+        if (h->xb_dev[i]) cudaFree(h->xb_dev[i]);
+        if (h->xb_dma[i]) cudaEventDestroy(h->xb_dma[i]);
+        if (h->xb_conv[i]) cudaEventDestroy(h->xb_conv[i]);
+    }
+    if (h->xb_stream) cudaStreamDestroy(h->xb_stream);
     for (int m = 0; m < 2; ++m) {
         if (h->d_nbr[m]) cudaFree(h->d_nbr[m]);
         if (h->d_ntab[m]) cudaFree(h->d_ntab[m]);

@@ -1538,6 +1538,33 @@ __device__ __forceinline__ void for_each_run(const PackedGeom& G, uint32_t g, ui
     }
 }
 
+// BITS: the chunk arrives as a bit array (bit i = reference byte i of the chunk,
+// packed on the host: 8x fewer PCIe bytes); otherwise as the reference bytes
+__device__ __forceinline__ void warp_bits_to_shared(uint8_t* sbuf, const uint32_t* bits, uint64_t off, uint32_t n,
+                                                    uint32_t lane) {
+    for (uint32_t k = lane; k < n; k += 32) {
+        const uint64_t b = off + k;
+        sbuf[k] = (uint8_t)((__ldg(bits + (b >> 5)) >> (b & 31)) & 1u);
+    }
+}
+// bytes sbuf[0, n) -> bits [off, off + n) of a zeroed bit array: whole words stored,
+// the (at most two) words shared with a neighbouring run or-ed atomically
+__device__ __forceinline__ void warp_shared_to_bits(const uint8_t* sbuf, uint32_t* bits, uint64_t off, uint32_t n,
+                                                    uint32_t lane) {
+    const uint64_t w0 = off >> 5, w1 = (off + n + 31) >> 5;
+    for (uint64_t w = w0; w < w1; ++w) {
+        const uint64_t b = w * 32 + lane;
+        const bool in = b >= off && b < off + n;
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, in && sbuf[b - off] != 0);
+        const uint32_t mask = __ballot_sync(0xFFFFFFFFu, in);
+        if (lane == 0) {
+            if (mask == 0xFFFFFFFFu) bits[w] = word;
+            else if (word) atomicOr(bits + w, word);
+        }
+    }
+}
+
+template <bool BITS>
 __global__ void __launch_bounds__(kConvWarps * 32)
 pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32_t Y1, uint32_t* __restrict__ P,
             int* __restrict__ bad) {
@@ -1554,7 +1581,11 @@ pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32
         for_each_run(G, g, tlo, thi, [&](uint32_t t0, uint32_t n) {
             const uint32_t X = t0 % G.Wc, Y = t0 / G.Wc;
             const uint64_t off = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
-            warp_copy_run<true>(sb + (t0 - g * 32) * G.WQ, const_cast<uint8_t*>(bytes) + off, n * G.WQ, lane);
+            if constexpr (BITS)
+                warp_bits_to_shared(sb + (t0 - g * 32) * G.WQ, reinterpret_cast<const uint32_t*>(bytes), off,
+                                    n * G.WQ, lane);
+            else
+                warp_copy_run<true>(sb + (t0 - g * 32) * G.WQ, const_cast<uint8_t*>(bytes) + off, n * G.WQ, lane);
         });
         __syncwarp();
         uint32_t lanes = 0;  // tiles of this group inside [tlo, thi)
@@ -1583,6 +1614,7 @@ pack_kernel(PackedGeom G, const uint8_t* __restrict__ bytes, uint32_t Y0, uint32
     }
 }
 
+template <bool BITS>
 __global__ void __launch_bounds__(kConvWarps * 32)
 unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_t Y1, uint8_t* __restrict__ bytes) {
     extern __shared__ __align__(16) uint8_t conv_sm[];
@@ -1603,7 +1635,10 @@ unpack_kernel(PackedGeom G, const uint32_t* __restrict__ P, uint32_t Y0, uint32_
         for_each_run(G, g, tlo, thi, [&](uint32_t t0, uint32_t n) {
             const uint32_t X = t0 % G.Wc, Y = t0 / G.Wc;
             const uint64_t off = ((uint64_t)(Y - Y0) * G.WQ + a) * G.w + (uint64_t)X * G.WQ;
-            warp_copy_run<false>(sb + (t0 - g * 32) * G.WQ, bytes + off, n * G.WQ, lane);
+            if constexpr (BITS)
+                warp_shared_to_bits(sb + (t0 - g * 32) * G.WQ, reinterpret_cast<uint32_t*>(bytes), off, n * G.WQ, lane);
+            else
+                warp_copy_run<false>(sb + (t0 - g * 32) * G.WQ, bytes + off, n * G.WQ, lane);
         });
         __syncwarp();
     }

@@ -209,6 +209,39 @@ def test_packed_chunked_conversions(monkeypatch):
     assert np.array_equal(sim.front().data, o.front)  # unchanged on error
 
 
+@pytest.mark.parametrize("stage", ["4096", "100000", "0"])
+@pytest.mark.parametrize("name,level", [("carpet", 5), ("triangle", 13), ("h", 7)])
+def test_host_bit_transfers(monkeypatch, stage, name, level):
+    # host buffers cross PCIe as bit arrays (host-packed, hostconv.inc) in chunks of
+    # whole coarse rows (odd byte counts: tail words); the bytes path
+    # (NBBGPU_XFER_BYTES=1) must give the same state, bad bytes anywhere are rejected
+    if stage != "0":
+        monkeypatch.setenv("NBBGPU_STAGE_BYTES", stage)
+    desc = {"carpet": CARPET, "triangle": T,
+            "h": FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])}[name]
+    o0 = oracle.Oracle(desc.replicas, desc.k, desc.s, level)
+    o0.seed(11, 0.5)
+    start = o0.front.copy()
+    o0.step(8, 12, True)
+    o0.step(8, 12, True)
+    for xfer_bytes in (False, True):
+        if xfer_bytes:
+            monkeypatch.setenv("NBBGPU_XFER_BYTES", "1")
+        sim = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel="packed"))
+        sim.upload(start)
+        sim.step(conway_rule(), 2)
+        assert np.array_equal(sim.front().data, o0.front), xfer_bytes
+        assert sim.state_hash() == o0.state_hash()
+        for pos in (0, start.size // 2 + 1, start.size - 1):
+            bad = o0.front.copy()
+            bad[pos] = 2 if pos % 2 else 255
+            with pytest.raises(OutOfDomain):
+                sim.upload(bad)
+            sim._front_cache = None
+            assert np.array_equal(sim.front().data, o0.front)  # unchanged on error
+        sim.close()
+
+
 def test_large_levels_hash(golden, golden_long):
     cases = [t for t in golden["traces"] if t["level"] >= 13]
     for key in ("t16", "c9", "t18", "h10", "y8", "h11", "y9", "t20"):
