@@ -408,8 +408,7 @@ struct nbbgpu_sim {
     uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
     uint32_t* d_pbt = nullptr;              // transposed boundary plane (wide halos, single GPU)
     uint32_t* d_pdmask = nullptr;           // [nHc][8] direction masks per 32-slot chunk
-    uint32_t* d_phent = nullptr;            // nonzero (chunk, direction) masks, 2 words each
-    uint32_t n_hent = 0;
+    BtMasks bt_masks{};  // the same masks by value (halo_bt_regs_kernel)
     uint64_t packed_table_bytes = 0;
     int64_t pg0 = 0, pg1 = 0;               // owned groups
     // profiling (nbbgpu_step_profiled): events around each main step kernel, launch count
@@ -875,7 +874,6 @@ void free_all(nbbgpu_t h) {
     if (h->d_phalo) cudaFree(h->d_phalo);
     if (h->d_pbt) cudaFree(h->d_pbt);
     if (h->d_pdmask) cudaFree(h->d_pdmask);
-    if (h->d_phent) cudaFree(h->d_phent);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
     if (h->d_bblow) cudaFree(h->d_bblow);
     if (h->d_bbcoarse) cudaFree(h->d_bbcoarse);

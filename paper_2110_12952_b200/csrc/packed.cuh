@@ -83,13 +83,11 @@ struct PackedStepParams {
     // waiting (this and every later step) and the host raises on synchronize
     uint32_t* wait_err;
     uint64_t wait_ns;
-    // transposed halo gather (HMODE 5): the boundary plane transposed per 32 slots,
+    // transposed halo gather (HMODE 6, halo_bt_regs_kernel): the boundary plane transposed per 32 slots,
     // Bt[(g * nHc + k) * 32 + b] bit i = boundary word 32k + i of tile 32g + b, and
     // per chunk k and direction slot d the mask of chunk k's slots in direction d
     const uint32_t* bt;
     const uint32_t* dmask;  // [nHc][8]
-    const uint32_t* hent;   // the nonzero (chunk, direction) masks: [2e] = k << 8 | d, [2e + 1] = mask
-    uint32_t nhent;
     // SPLIT = 2 (candy CTA pairs): the staged row window of half h is record words
     // [win0[h], win0[h] + win_words)
     uint32_t win0[2], win_words;
@@ -404,83 +402,60 @@ __global__ void bnd_transpose_kernel(const PackedStepParams p, const uint32_t* _
 // (one load each, masked), and one transpose turns lane b's bits into the 32 halo
 // words (no per-source-group passes: the slots of a direction are bits of ONE word
 // of the neighbour tile).
-// Rolled over chunks: per chunk one masked load per present direction (mid-size
-// grids: H r=10 0.031 vs 0.035 ms for the entry list below).
-__device__ __forceinline__ void halo_bt_task_rolled(const PackedStepParams& p, uint32_t* H, uint32_t g,
-                                                    uint32_t lane) {
-    const uint32_t t = g * 32 + lane;
-    const bool in = t < p.T;
-    const uint32_t nHc = (p.nH + 31) / 32;
-    uint32_t t2[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) t2[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
-    uint32_t* Hg = H + (uint64_t)g * p.nHp;
-#pragma unroll 1
-    for (uint32_t k = 0; k < nHc; ++k) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            const uint32_t dm = __ldg(p.dmask + k * 8 + d);
-            if (dm && t2[d] != kNoTile)
-                word |= __ldcg(p.bt + ((uint64_t)(t2[d] >> 5) * nHc + k) * 32 + (t2[d] & 31)) & dm;
-        }
-        const uint32_t out = warp_transpose32(word, lane);  // lane i: bit b = slot 32k + i of tile b
-        if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
-    }
-}
-
 constexpr int kBtMaxChunks = 16;
 
-// Many groups (HMODE 7), a warp per group in a grid-stride loop: the (chunk,
-// direction) entry list -- the same for every group -- is staged in shared memory
-// once per block, and the next group's neighbour tiles are loaded while the current
-// group's Bt words are in flight (two dependent round trips per group otherwise).
-constexpr int kBtMaxEntries = kBtMaxChunks * 8;
-__device__ __forceinline__ void halo_bt_groups(const PackedStepParams& p, uint32_t* H, uint64_t wi0,
-                                               uint32_t lane) {
-    __shared__ uint32_t bt_scratch[8][(kBtMaxChunks + 8) * 32];  // 256-thread blocks: acc, neighbour tiles
-    __shared__ uint2 ents[kBtMaxEntries];
-    const uint32_t ne = p.nhent < (uint32_t)kBtMaxEntries ? p.nhent : (uint32_t)kBtMaxEntries;
-    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) ents[e] = __ldg(reinterpret_cast<const uint2*>(p.hent) + e);
-    __syncthreads();
-    uint32_t* acc = bt_scratch[(threadIdx.x >> 5) & 7];  // [nHc][32]
-    uint32_t* st2 = acc + kBtMaxChunks * 32;            // [8][32]
-    const uint32_t nHc = (p.nH + 31) / 32;
-    const uint64_t nw = (uint64_t)(p.g1 - p.g0);
-    const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+// The per-(chunk, direction) masks of the transposed gather, passed by value: with
+// the chunk count a compile-time constant every mask is a kernel-parameter operand
+// (no shared entry list, no shared accumulators).
+struct BtMasks {
+    uint32_t m[kBtMaxChunks][8];
+};
+
+// Transposed gather, register form (one warp per group, grid-stride): lane = tile b
+// holds the 8 neighbour tiles (the next group's are loaded while this group's Bt
+// words are in flight); per direction one address and, per chunk the direction
+// has slots in, one predicated load + AND/OR into the chunk's register accumulator;
+// then NHC transposes.  ~300 instructions per group instead of ~1000 for round 2's
+// (chunk, direction) entry list in shared memory with shared accumulators (removed).
+template <int NHC>
+__global__ void __launch_bounds__(256) halo_bt_regs_kernel(const PackedStepParams p, const BtMasks M,
+                                                           uint32_t* __restrict__ H) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gstride = (uint32_t)(((uint64_t)gridDim.x * blockDim.x) >> 5);
+    uint32_t g = p.g0 + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
     uint32_t t2n[8];
-    auto fetch = [&](uint64_t wi, uint32_t (&t2)[8]) {
-        const uint32_t t = (p.g0 + (uint32_t)wi) * 32 + lane;
-        const bool in = wi < nw && t < p.T;
+    auto fetch = [&](uint32_t gg) {
+        const uint32_t t = gg * 32 + lane;
+        const bool in = gg < p.g1 && t < p.T;
 #pragma unroll
-        for (int d = 0; d < 8; ++d) t2[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
+        for (int d = 0; d < 8; ++d) t2n[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
     };
-    fetch(wi0, t2n);
-    for (uint64_t wi = wi0; wi < nw; wi += stride) {
+    fetch(g);  // (static table: before the wait for the previous step kernel)
+    pdl_wait();
+    pdl_trigger();
+    const XposeLane X(lane);
+    for (; g < p.g1; g += gstride) {
+        uint32_t t2[8];
 #pragma unroll
-        for (int d = 0; d < 8; ++d) st2[d * 32 + lane] = t2n[d];
-        fetch(wi + stride, t2n);  // next group's neighbour tiles, in flight meanwhile
-        const uint32_t g = p.g0 + (uint32_t)wi;
-        for (uint32_t k = 0; k < nHc; ++k) acc[k * 32 + lane] = 0u;
-        for (uint32_t e0 = 0; e0 < ne; e0 += 8) {
-            uint32_t v[8], kk[8];
+        for (int d = 0; d < 8; ++d) t2[d] = t2n[d];
+        fetch(g + gstride);
+        uint32_t acc[NHC];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                v[u] = 0u;
-                kk[u] = 0u;
-                if (e0 + u < ne) {
-                    const uint2 en = ents[e0 + u];
-                    kk[u] = en.x >> 8;
-                    const uint32_t tt = st2[(en.x & 0xFFu) * 32 + lane];
-                    if (tt != kNoTile) v[u] = __ldcg(p.bt + ((uint64_t)(tt >> 5) * nHc + kk[u]) * 32 + (tt & 31)) & en.y;
-                }
-            }
+        for (int k = 0; k < NHC; ++k) acc[k] = 0u;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[kk[u] * 32 + lane] |= v[u];
+        for (int d = 0; d < 8; ++d) {
+            const bool ok = t2[d] != kNoTile;
+            const uint32_t* b = p.bt + ((t2[d] >> 5) * (uint32_t)NHC) * 32u + (t2[d] & 31u);
+            uint32_t v[NHC];
+#pragma unroll
+            for (int k = 0; k < NHC; ++k) v[k] = (ok && M.m[k][d] != 0u) ? __ldcg(b + 32 * k) : 0u;
+#pragma unroll
+            for (int k = 0; k < NHC; ++k) acc[k] |= v[k] & M.m[k][d];
         }
         uint32_t* Hg = H + (uint64_t)g * p.nHp;
-        for (uint32_t k = 0; k < nHc; ++k) {
-            const uint32_t out = warp_transpose32(acc[k * 32 + lane], lane);  // lane i: bit b = slot 32k + i of tile b
+#pragma unroll
+        for (int k = 0; k < NHC; ++k) {
+            const uint32_t out = warp_transpose32(acc[k], X);  // lane i: bit b = slot 32k + i of tile b
             if (k * 32 + lane < p.nH) Hg[k * 32 + lane] = out;
         }
     }
@@ -520,15 +495,9 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
         pdl_trigger();  // the step kernel may launch and run its prologue
     }
     const uint64_t nw = HMODE == 6 ? (uint64_t)(p.g1 - p.g0) * ((p.nH + 31) / 32)
-                      : HMODE == 2 || HMODE == 5 || HMODE == 7 ? (uint64_t)(p.g1 - p.g0)
+                      : HMODE == 2 ? (uint64_t)(p.g1 - p.g0)
                       : HMODE == 1 || HMODE == 3 ? (uint64_t)(p.g1 - p.g0) * (uint32_t)p.nD
                                    : (uint64_t)(p.g1 - p.g0) * ((p.nH + SPW - 1) / SPW);
-    if constexpr (HMODE == 7) {
-        // every warp of the block enters (the entry list is staged by the whole block
-        // behind a __syncthreads, also in a last block with fewer groups than warps)
-        halo_bt_groups(p, H, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, lane);
-        return;
-    }
     if constexpr (HMODE == 8) {
         // small halos (nH <= 8), warp per group, lean: the slot table is hoisted out
         // of the task loop (uniform), 32-bit offsets, 8 + 8 independent loads and 8
@@ -575,14 +544,12 @@ __global__ void halo_words_kernel(const PackedStepParams p, const uint32_t* __re
         }
         return;
     }
-    if constexpr (HMODE != 7 && HMODE != 8)
+    if constexpr (HMODE != 8)
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         if constexpr (HMODE == 6) {
             const uint32_t nHc = (p.nH + 31) / 32, w32 = (uint32_t)wi, gi = w32 / nHc;
             halo_bt_chunk_task(p, H, p.g0 + gi, w32 - gi * nHc, lane);
-        } else if constexpr (HMODE == 5) {
-            halo_bt_task_rolled(p, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 2) {
             halo_group_task<NC>(p, bsrc, H, p.g0 + (uint32_t)wi, lane);
         } else if constexpr (HMODE == 1 || HMODE == 3) {
