@@ -800,6 +800,87 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
     });
 }
 
+// Stage size in words known at compile time for the built-in tile shapes (stage:
+// Cp record words | nHp halo words | zero word, + 3; build_packed_plan, which the
+// launcher checks against): lets the ws3 consumers address every stage of their set
+// with immediates (block_words_c).  0: run-time stage size.
+template <class FT, int WQ>
+struct StageWordsCT { static constexpr int v = 0; };
+#ifndef NBB_NO_SWC  // (A/B builds: run-time stage size everywhere)
+template <> struct StageWordsCT<HTag, 49> { static constexpr int v = 2608; };        // C 2401, nH 198
+template <> struct StageWordsCT<CarpetTag, 64> { static constexpr int v = 4428; };   // C 4096, nH 328
+#endif
+// (measured, not enabled: T q=8 r=20 133.2 -> 134.8 us, Vicsek r=12/13 neutral; the
+// row-block kernels gain: H r=11 114.1 -> 108.5 us, carpet r=11 432 -> 412 us)
+
+// first own word of block blk in the record (block_words_r's Sw / Sq base)
+template <class FT, int P, int WQ>
+__device__ __forceinline__ uint32_t block_own_base(uint32_t blk) {
+    using W = Wiring<FT, P>;
+    constexpr int BW = W::BW, BH = W::BH, NB = W::NB;
+    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    if constexpr (ILV) return (blk >> 5) * (NB * 32) + (blk & 31);
+    constexpr int BPR = WQ / BW;
+    const uint32_t by = blk / BPR, bx = blk - by * BPR;
+    return by * (BH * WQ) + bx * BW;
+}
+
+// block_words_r with every stage address = the lane's set-relative byte offset +
+// an immediate: tS[E] = external E, own_off = the block's first own word (bytes,
+// both relative to stage 0 of the set), SOFF = this stage's offset from it.
+template <class FT, int P, int WQ, bool CONWAY, int DEG, int SOFF>
+__device__ __forceinline__ void block_words_c(const uint8_t* st, const uint32_t (&tS)[Wiring<FT, P>::NEP],
+                                              uint32_t own_off, uint32_t blk, uint32_t* Do, uint32_t vmask,
+                                              const uint32_t (&KB)[9], const uint32_t (&KS)[9]) {
+    using W = Wiring<FT, P>;
+    constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
+    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    constexpr bool VEC = BH == 1 && BW % 4 == 0 && !ILV;
+    const uint8_t* Sb = st + SOFF;
+    uint32_t own[NB], ext[NEP];
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        constexpr int OW = ILV ? N * 32 : (N / BW) * WQ + N % BW;  // word offset from the block base
+        if constexpr (VEC) {
+            if constexpr (N % 4 == 0) {
+                const uint4 v = *reinterpret_cast<const uint4*>(Sb + own_off + 4 * OW);
+                own[N] = v.x; own[N + 1] = v.y; own[N + 2] = v.z; own[N + 3] = v.w;
+            }
+        } else {
+            own[N] = *reinterpret_cast<const uint32_t*>(Sb + own_off + 4 * OW);
+        }
+    });
+    static_for<NEP>([&](auto e) {
+        constexpr int E = decltype(e)::value;
+        ext[E] = *reinterpret_cast<const uint32_t*>(Sb + tS[E]);
+    });
+    const uint32_t base = block_own_base<FT, P, WQ>(blk);
+    uint32_t* Dw = Do + base;
+    uint32_t res[VEC ? 4 : 1];
+    static_for<NB>([&](auto n) {
+        constexpr int N = decltype(n)::value;
+        uint32_t x[8];
+        static_for<8>([&](auto j) {
+            constexpr int J = decltype(j)::value;
+            constexpr int SJ = W::d.src[N][J];
+            if constexpr (J >= DEG || SJ == kWireAbsent) x[J] = 0u;
+            else if constexpr (SJ >= 0) x[J] = own[SJ];
+            else x[J] = ext[-SJ - 2];
+        });
+        const Count4 cnt = count8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+        const uint32_t r = apply_rule_bits<CONWAY>(cnt, own[N], KB, KS) & vmask;
+        if constexpr (ILV) {
+            Dw[N * 32] = r;
+        } else if constexpr (VEC) {
+            res[N % 4] = r;
+            if constexpr (N % 4 == 3)
+                reinterpret_cast<uint4*>(Dw)[N / 4] = make_uint4(res[0], res[1], res[2], res[3]);
+        } else {
+            Dw[(N / BW) * WQ + N % BW] = r;
+        }
+    });
+}
+
 // Persistent, warp-specialised micro-block step (one CTA per SM), TMA in and out:
 //   producer warp : group record + its halo words (halo_words_kernel output) ->
 //                   NS-stage input ring (cp.async.bulk, full barriers carry the
@@ -861,7 +942,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     static_assert(NS % NGRP == 0, "stages are partitioned over the group sets");
     // (the in-kernel halo warps wait on the stages' empty barriers the same way: each
     // stage served by one halo warp, or one set whose consumers finish groups in order)
-    static_assert(HW == 0 || NS % HW == 0 || NGRP == 1, "stages are partitioned over the halo warps");
+    static_assert(HW == 0 || NS % (HW > 0 ? HW : 1) == 0 || NGRP == 1, "stages are partitioned over the halo warps");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
@@ -974,24 +1055,41 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             // lane t the slot bits of tile t: Bt[(g nHc + k) 32 + t], 128 coalesced bytes
             // bt warp w serves group set w % NGRP (each set's buffers, no head-of-line
             // blocking between sets), chunks w / NGRP, + BTS, ...
+            // The lane's source cells (chunks b, b + BTS, ...) stay in registers; the
+            // buffer is released as soon as its words are read (before the transposes
+            // and the global stores: H r=11 step kernel 108.7 -> ... us)
             const uint32_t w = (uint32_t)(warp - NCW - 2), set = w % NGRP, b = w / NGRP;
             const uint32_t nHc = (p.nSrc + 31) / 32;
             const XposeLane X((uint32_t)lane);
+            // (chunks per bt warp: at most kBtMaxChunks / BTS; H q=4 has 7 chunks)
+            constexpr int KMAX = std::is_same<FT, HTag>::value ? (7 + BTS - 1) / BTS : (kBtMaxChunks + BTS - 1) / BTS;
+            uint32_t sidx[KMAX];
+#pragma unroll
+            for (int kk = 0; kk < KMAX; ++kk) {
+                const uint32_t m = 32 * (b + kk * BTS) + (uint32_t)lane;
+                sidx[kk] = m < p.nSrc ? __ldg(p.srcidx + m) : kNoTile;
+            }
             uint32_t i = set;
             for (uint32_t g = p.g0 + pair + set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
                 const uint32_t o = i % NO;
                 mbar_wait(ofull0 + 8 * o, (i / NO) & 1u);  // acquire: every slice written
                 const uint32_t* Do = reinterpret_cast<const uint32_t*>(outs + o * out_bytes);
-                for (uint32_t k = b; k < nHc; k += BTS) {
-                    const uint32_t m = 32 * k + (uint32_t)lane;
-                    const uint32_t x = m < p.nSrc ? Do[__ldg(p.srcidx + m)] : 0u;
-                    if constexpr (std::is_same<FT, HTag>::value)
-                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, X);
-                    else
-                        p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x, (uint32_t)lane);
-                }
+                uint32_t x[KMAX];
+#pragma unroll
+                for (int kk = 0; kk < KMAX; ++kk)
+                    x[kk] = (b + kk * BTS < nHc && sidx[kk] != kNoTile) ? Do[sidx[kk]] : 0u;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(oempty0 + 8 * o);  // release: buffer o read
+#pragma unroll
+                for (int kk = 0; kk < KMAX; ++kk) {
+                    const uint32_t k = b + kk * BTS;
+                    if (k < nHc) {
+                        if constexpr (std::is_same<FT, HTag>::value)
+                            p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x[kk], X);
+                        else
+                            p.bt_out[((uint64_t)g * nHc + k) * 32 + lane] = warp_transpose32(x[kk], (uint32_t)lane);
+                    }
+                }
             }
             return;
         }
@@ -1069,8 +1167,24 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         if (k_lo + lane < k_hi) { bm0 = __ldg(sorted + k_lo + lane); bw0 = __ldg(p.srcidx + bm0); }
         if (k_lo + 32 + lane < k_hi) { bm1 = __ldg(sorted + k_lo + 32 + lane); bw1 = __ldg(p.srcidx + bm1); }
     }
-    uint32_t i = (uint32_t)set;
-    for (uint32_t g = p.g0 + pair + (uint32_t)set * npairs; g < p.g1; g += NGRP * npairs, i += NGRP) {
+    // compile-time stage size (SWC > 0): the group loop is unrolled over the NS / NGRP
+    // stages of this warp's set, so every external load is ONE ld.shared at the
+    // lane's (set-relative) offset + an immediate (the stage offset) instead of a
+    // multiply-add + add + load per external per group (H: 48 -> 16 instructions of
+    // the 166 per block)
+    constexpr int SWC = SPLIT == 1 ? StageWordsCT<FT, WQ>::v : 0;
+    uint32_t tS[NEP], own_off = 0;
+    if constexpr (SWC > 0) {
+        using BG = BlockGeom<FT, P, WQ>;
+        const uint32_t set_off = (uint32_t)set * (uint32_t)(SWC * 4);
+#pragma unroll
+        for (int e = 0; e < NEP; ++e) tS[e] = set_off + toff[e];
+        own_off = set_off + 4u * block_own_base<FT, P, WQ>(blk);
+        (void)sizeof(BG);
+    }
+    auto group = [&](uint32_t g, uint32_t i, auto soff_c) {
+        constexpr int SOFF = decltype(soff_c)::value;  // byte offset of this stage from set 0's (SWC > 0)
+        (void)SOFF;
         const uint32_t s = i % NS, o = i % NO;
         mbar_wait(full0 + 8 * s, (i / NS) & 1u);
         if constexpr (PWS) {
@@ -1086,7 +1200,11 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         // block_words_r indexes the whole record: shift the slice base back by out_off
         uint32_t* Do = reinterpret_cast<uint32_t*>(outs + o * out_bytes) - out_off;
         const uint32_t vmask = g == p.NG - 1 ? p.lastmask : 0xFFFFFFFFu;
-        if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS, win0);
+        if constexpr (SWC > 0) {
+            if (active) block_words_c<FT, P, WQ, CONWAY, DEG, SOFF>(st, tS, own_off, blk, Do, vmask, KB, KS);
+        } else {
+            if (active) block_words_r<FT, P, WQ, CONWAY, DEG>(Sb, toff, blk, Do, vmask, KB, KS, win0);
+        }
         if constexpr (PWS) {
             fence_proxy_async_smem();  // the bulk store reads this slice through the async proxy
             __syncwarp();
@@ -1096,7 +1214,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                          (w_hi - w_lo) * 4);
                 if constexpr (BTO) mbar_arrive(ofull0 + 8 * o);  // release: this slice is written
             }
-            if constexpr (BTO) continue;  // the bt warps write the boundary data
+            if constexpr (BTO) return;  // the bt warps write the boundary data
             uint32_t* bg = bdst + (uint64_t)g * p.nSrc;
             if constexpr (REGB) {
                 if (k_lo + lane < k_hi) bg[bm0] = Do[bw0];
@@ -1107,7 +1225,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 const uint32_t m = __ldg(sorted + k);
                 bg[m] = Do[__ldg(p.srcidx + m)];
             }
-            continue;
+            return;
         }
         if (!BST && c == 0 && half == 0) {  // boundary plane of the new state (few words)
             uint32_t mine = 0u;
@@ -1130,6 +1248,23 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         if (lane == 0) {
             mbar_arrive(empty0 + 8 * s);
             mbar_arrive(ofull0 + 8 * o);
+        }
+    };
+    {
+        uint32_t i = (uint32_t)set;
+        uint32_t g = p.g0 + pair + (uint32_t)set * npairs;
+        if constexpr (SWC > 0) {
+            constexpr int U = NS / NGRP;  // stages of this set: set + NGRP u, u < U
+            while (g < p.g1) {
+                static_for<U>([&](auto u) {
+                    if (g >= p.g1) return;
+                    group(g, i, std::integral_constant<int, decltype(u)::value * NGRP * SWC * 4>{});
+                    g += NGRP * npairs;
+                    i += NGRP;
+                });
+            }
+        } else {
+            for (; g < p.g1; g += NGRP * npairs, i += NGRP) group(g, i, std::integral_constant<int, 0>{});
         }
     }
     if constexpr (PUSH && !BST) if (c == 0 && half == 0) {
