@@ -1672,7 +1672,8 @@ int nbbgpu_jit_compile_check(const int32_t* rep, int k, int s, int level, int mo
         const JitShape j = jit_shape_for(P.bP, P.wq, P.split == 2 ? P.SWsplit : P.SW, P.Cp, F.k, P.split);
         std::vector<char> cubin;
         std::string lowered, err;
-        if (!jit_compile(jit_source(F), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j), "sm_100a", cubin, lowered, err))
+        if (!jit_compile(jit_source(F, P.wq, j.SPLIT == 1 ? P.SW : 0u), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j),
+                         "sm_100a", cubin, lowered, err))
             raise(NBBGPU_ERR_CUDA, "jit: " + err);
         if (name && name_bytes) {
             const std::string out = lowered + " (" + std::to_string(cubin.size()) + " B cubin)";

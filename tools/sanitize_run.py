@@ -47,11 +47,13 @@ CASES = {
     "bb_s4": (Y, 4, Backend.GpuBoundingBox, "auto", {}, 1),
     "push_p2p": (T, 12, Backend.GpuCompact, "packed", {}, 2),
     "push_p2p_q8": (T, 17, Backend.GpuCompact, "packed", {}, 2),
-    # >= 8192 groups: the many-groups Bt halo gather (HMODE 7), run-time and built-in wiring
+    # >= 2048 groups: the register-form Bt halo gather (halo_bt_regs_kernel), run-time
+    # and built-in wiring; carpet / H: immediate stage addressing + bt warps
     "jit_k11": (K63, 11, Backend.GpuCompact, "packed", {}, 1),
     "carpet_c10": (C, 10, Backend.GpuCompact, "packed", {}, 1),
+    "h_h10": (H, 10, Backend.GpuCompact, "packed", {}, 1),
 }
-BIG = {"jit_k11", "carpet_c10"}  # no naive-kernel reference under the sanitizer (too slow)
+BIG = {"jit_k11", "carpet_c10", "h_h10"}  # no naive-kernel reference under the sanitizer (too slow)
 
 
 def run(name, steps=3):
