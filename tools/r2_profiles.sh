@@ -13,13 +13,13 @@ timeout 900 $NCU --set full --import-source on -k regex:step_packed_ws3 -s 4 -c 
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_step.log 2>&1; echo "ncu step rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:halo_words -s 4 -c 1 -o $O/r2_halo_r20 \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_halo.log 2>&1; echo "ncu halo rc=$?"
-timeout 900 $NCU --set full --import-source on -k regex:step_packed_ws3 -s 3 -c 1 -o $O/r2_jit_k12 \
+timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_bt_regs" -s 4 -c 2 -o $O/r2_jit_k12 \
     python tools/prof_step.py --fractal @descriptors/k6s3.desc --level 12 --kernel packed --steps 5 > $O/ncu_jit.log 2>&1; echo "ncu jit rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:step_bb_rows -s 3 -c 1 -o $O/r2_bb_t16 \
     python tools/prof_step.py --level 16 --backend gpu-bb --steps 5 > $O/ncu_bb.log 2>&1; echo "ncu bb rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:step_bb_rows -s 3 -c 1 -o $O/r2_bb_c10 \
     python tools/prof_step.py --fractal sierpinski-carpet --level 10 --backend gpu-bb --steps 5 > $O/ncu_bb_c10.log 2>&1; echo "ncu bb c10 rc=$?"
-timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_words|bnd_transpose" -s 6 -c 3 -o $O/r2_h11 \
+timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_bt_regs" -s 6 -c 2 -o $O/r2_h11 \
     python tools/prof_step.py --fractal @descriptors/h-fractal.desc --level 11 --kernel packed --steps 5 > $O/ncu_h11.log 2>&1; echo "ncu h11 rc=$?"
 # text summaries (the .ncu-rep files stay only when small: gpurun copies back <= 64 MiB)
 for r in $O/*.ncu-rep; do
