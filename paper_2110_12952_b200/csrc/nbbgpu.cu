@@ -1522,7 +1522,7 @@ void render_view(nbbgpu_t h, uint8_t* dst, int pbm) {
         v.wq = (uint32_t)h->pp.wq;
         v.Wc = (uint32_t)h->pp.Wc;
         v.Cp = (uint32_t)h->pp.Cp;
-        v.ilv = h->pp.ilv ? 1u : 0u;
+        v.ilv = h->pp.ilv;
     }
     v.bg = h->bg;
     const uint64_t n = (uint64_t)h->hf.side, total = n * (pbm ? n + 1 : n);
@@ -1672,7 +1672,7 @@ int nbbgpu_jit_compile_check(const int32_t* rep, int k, int s, int level, int mo
         const JitShape j = jit_shape_for(P.bP, P.wq, P.split == 2 ? P.SWsplit : P.SW, P.Cp, F.k, P.split);
         std::vector<char> cubin;
         std::string lowered, err;
-        if (!jit_compile(jit_source(F, P.wq, j.SPLIT == 1 ? P.SW : 0u), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j),
+        if (!jit_compile(jit_source(F, P.wq, j.SPLIT == 1 ? P.SW : 0u, P.ilv != 0), jit_ws3_expr(true, moore ? 8 : 4, P.wide, P.wq, j),
                          "sm_100a", cubin, lowered, err))
             raise(NBBGPU_ERR_CUDA, "jit: " + err);
         if (name && name_bytes) {

@@ -37,21 +37,35 @@ constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Record word of local cell (row a, column c).  Row-major, except the carpet at
-// WQ = 64 (ilv): its 8-cell row micro-blocks are interleaved so that the 32 blocks
-// of four rows -- one consumer warp -- sit in 32 consecutive words for every cell
-// position n: word = ((a / 4) * 8 + n) * 32 + (a % 4) * 8 + block, c = 8 * block + n.
-// Lane = block then reads and writes conflict-free (row-major blocks start 8 words
-// apart: every shared access of the step kernel conflicted 4- to 8-way).
+// Record word of local cell (row a, column c).  Row-major, except for row
+// micro-blocks of width ilv = BW (the carpet at WQ = 64, run-time specialised
+// level-1 descriptors): the blocks are interleaved so that the 32 blocks of one
+// consumer warp sit in 32 consecutive words for every cell position n: block
+// b = a * (wq / BW) + c / BW, n = c % BW, word = ((b / 32) * BW + n) * 32 + b % 32
+// (carpet: ((a / 4) * 8 + n) * 32 + (a % 4) * 8 + c / 8).  Lane = block then reads
+// and writes conflict-free (row-major blocks start BW words apart: the carpet's
+// shared accesses conflicted 4- to 8-way).  Records hold ceil(blocks / 32) * 32 * BW
+// words (the padding blocks' words carry no cell).
 __host__ __device__ __forceinline__ uint32_t rec_word(uint32_t ilv, uint32_t wq, uint32_t a, uint32_t c) {
-    if (ilv) return (((a >> 2) * 8 + (c & 7)) << 5) + (a & 3) * 8 + (c >> 3);
+    if (ilv) {
+        const uint32_t bc = c / ilv, b = a * (wq / ilv) + bc, n = c - bc * ilv;
+        return ((b >> 5) * ilv + n) * 32 + (b & 31);
+    }
     return a * wq + c;
 }
+constexpr uint32_t kNoLoc = 0xFFFFFFFFu;  // loc[] of a record word that carries no cell
+
+// interleaved records for a run-time specialised tag (jit_source specialises it)
+template <class FT>
+struct TagIlv { static constexpr bool v = false; };
+template <class FT, int P, int WQ>
+constexpr bool rec_ilv() { return (std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64) || (TagIlv<FT>::v && P == 1); }
 
 struct PackedGeom {
     Frac f;
     uint32_t ilv;            // interleaved record layout (rec_word)
     uint32_t q, WQ, C, Cp;   // tile level, tile width, local cells, padded words per group
+    uint32_t Cl;             // record words with a loc entry (C, or Cp for interleaved records)
     uint32_t Wc, Hc, L;      // coarse dims, coarse level r - q
     uint32_t T, NG;          // tiles, groups
     uint32_t sq;             // s^q (embedded tile side)
@@ -749,7 +763,7 @@ __device__ __forceinline__ void block_words_r(const uint8_t* Sb, const uint32_t 
     // stores -- lanes sit BW words apart, so single-word accesses conflict BW/gcd-way
     // interleaved carpet records (rec_word): cell n of block blk at word
     // (blk / 32 * 8 + n) * 32 + blk % 32
-    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    constexpr bool ILV = rec_ilv<FT, P, WQ>();
     constexpr bool VEC = BH == 1 && BW % 4 == 0 && !ILV;
     uint32_t own[NB], ext[NEP];
     if constexpr (ILV) {
@@ -818,7 +832,7 @@ template <class FT, int P, int WQ>
 __device__ __forceinline__ uint32_t block_own_base(uint32_t blk) {
     using W = Wiring<FT, P>;
     constexpr int BW = W::BW, BH = W::BH, NB = W::NB;
-    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    constexpr bool ILV = rec_ilv<FT, P, WQ>();
     if constexpr (ILV) return (blk >> 5) * (NB * 32) + (blk & 31);
     constexpr int BPR = WQ / BW;
     const uint32_t by = blk / BPR, bx = blk - by * BPR;
@@ -834,7 +848,7 @@ __device__ __forceinline__ void block_words_c(const uint8_t* st, const uint32_t 
                                               const uint32_t (&KB)[9], const uint32_t (&KS)[9]) {
     using W = Wiring<FT, P>;
     constexpr int BW = W::BW, BH = W::BH, NB = W::NB, NEP = W::NEP;
-    constexpr bool ILV = std::is_same<FT, CarpetTag>::value && P == 1 && WQ == 64;
+    constexpr bool ILV = rec_ilv<FT, P, WQ>();
     constexpr bool VEC = BH == 1 && BW % 4 == 0 && !ILV;
     const uint8_t* Sb = st + SOFF;
     uint32_t own[NB], ext[NEP];
@@ -984,8 +998,13 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     }
     if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[win_words + p.nHp] = 0u;  // absent
     if (SPLIT == 1)
-        for (uint32_t k = tid; k < NO * (p.Cp - p.C); k += blockDim.x)  // record padding words
-            reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - p.C)) * out_bytes)[p.C + k % (p.Cp - p.C)] = 0u;
+    {
+        // record padding words (interleaved records: the padding blocks' words lie
+        // anywhere in the last chunk -- zero the whole ring once)
+        const uint32_t z0 = rec_ilv<FT, P, WQ>() ? 0u : p.C;
+        for (uint32_t k = tid; k < NO * (p.Cp - z0); k += blockDim.x)
+            reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - z0)) * out_bytes)[z0 + k % (p.Cp - z0)] = 0u;
+    }
     fence_proxy_async_smem();
     __syncthreads();
     pdl_wait();     // the prologue above overlapped the previous kernel's tail (PDL)
@@ -1540,7 +1559,7 @@ template <int K, int S>
 __global__ void seed_packed_kernel(PackedGeom G, const uint32_t* __restrict__ loc, uint32_t* __restrict__ P,
                                    uint64_t seed_mix, double density) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t cpw = (G.C + 31) / 32;  // 32-cell chunks per group
+    const uint32_t cpw = (G.Cl + 31) / 32;  // 32-word chunks per group (record words with a loc entry)
     const uint64_t nw = (uint64_t)G.NG * cpw;
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
          wi += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
@@ -1553,14 +1572,14 @@ __global__ void seed_packed_kernel(PackedGeom G, const uint32_t* __restrict__ lo
         for (uint32_t cc = 0; cc < 32; ++cc) {
             const uint32_t i = i0 + cc;
             bool alive = false;
-            if (tv && i < G.C) {
+            if (tv && i < G.Cl) {
                 const uint32_t l = __ldg(loc + i);
-                alive = cell_alive_mixed(seed_mix, x0 + (l & 0xFFFFu), y0 + (l >> 16), density);
+                if (l != kNoLoc) alive = cell_alive_mixed(seed_mix, x0 + (l & 0xFFFFu), y0 + (l >> 16), density);
             }
             const uint32_t word = __ballot_sync(0xFFFFFFFFu, alive);
             if (lane == cc) mine = word;
         }
-        if (i0 + lane < G.C) P[(uint64_t)g * G.Cp + i0 + lane] = mine;
+        if (i0 + lane < G.Cl) P[(uint64_t)g * G.Cp + i0 + lane] = mine;
     }
 }
 
@@ -1569,7 +1588,7 @@ template <int K, int S>
 __global__ void hash_packed_kernel(PackedGeom G, const uint32_t* __restrict__ loc, const uint32_t* __restrict__ P,
                                    uint32_t g0, uint32_t g1, unsigned long long* out) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t cpw = (G.C + 31) / 32;
+    const uint32_t cpw = (G.Cl + 31) / 32;
     const uint64_t nw = (uint64_t)(g1 - g0) * cpw;
     uint64_t acc = 0;
     for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi < nw;
@@ -1579,8 +1598,8 @@ __global__ void hash_packed_kernel(PackedGeom G, const uint32_t* __restrict__ lo
         const bool tv = t < G.T;
         uint32_t x0 = 0, y0 = 0;
         if (tv) tile_origin<K, S>(G, t, x0, y0);
-        const uint32_t mine = i0 + lane < G.C ? P[(uint64_t)g * G.Cp + i0 + lane] : 0u;
-        const uint32_t l_mine = i0 + lane < G.C ? __ldg(loc + i0 + lane) : 0u;
+        const uint32_t l_mine = i0 + lane < G.Cl ? __ldg(loc + i0 + lane) : kNoLoc;
+        const uint32_t mine = l_mine != kNoLoc ? P[(uint64_t)g * G.Cp + i0 + lane] : 0u;
         for (uint32_t cc = 0; cc < 32; ++cc) {
             const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, cc);
             const uint32_t l = __shfl_sync(0xFFFFFFFFu, l_mine, cc);

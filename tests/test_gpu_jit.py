@@ -77,3 +77,36 @@ def test_builtin_descriptors_through_jit_match(monkeypatch, name, level):
         assert np.array_equal(sims["0"].front().data, sims["1"].front().data)
     for s in sims.values():
         s.close()
+
+
+@pytest.mark.parametrize("ilv", ["0", "1"])
+@pytest.mark.parametrize("name,level", [("k6s3", 11), ("carpet", 10), ("h", 10)])
+def test_jit_many_groups_match_table_program(monkeypatch, name, level, ilv):
+    # >= 2048 groups: the run-time specialised kernel with its bt warps, compile-time
+    # stage size and the register-form transposed gather (halo_bt_regs_kernel) == the
+    # table-driven program (NBBGPU_GENERIC=1, B plane + direct gather), across a rule
+    # switch, a set_cell and odd / even call lengths; with interleaved records
+    # (NBBGPU_JIT_ILV=1: rec_word, padded records) and without
+    monkeypatch.setenv("NBBGPU_JIT_ILV", ilv)
+    desc = {"k6s3": CUSTOM[0][0], "carpet": builtin_descriptor("sierpinski-carpet"),
+            "h": FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])}[name]
+    sims = {}
+    for env in (("NBBGPU_JIT_FORCE", "1"), ("NBBGPU_GENERIC", "1")):
+        monkeypatch.delenv("NBBGPU_JIT_FORCE", raising=False)
+        monkeypatch.delenv("NBBGPU_GENERIC", raising=False)
+        monkeypatch.setenv(*env)
+        s = Simulation(desc, level, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+        s.seed_random(17, 0.5)
+        sims[env[0]] = s
+    assert sims["NBBGPU_JIT_FORCE"].packed_program()[0] == "jit"
+    assert sims["NBBGPU_GENERIC"].packed_program()[0] != "jit"
+    vn = StencilRule(0x49, 0x1A6, Neighborhood.VonNeumann)
+    for rule, n in ((conway_rule(), 3), (vn, 2), ("set", 0), (conway_rule(), 4)):
+        for s in sims.values():
+            if rule == "set":
+                s.set_cell((0, 0), 1 - s.cell((0, 0)))
+            else:
+                s.step(rule, n)
+        assert sims["NBBGPU_JIT_FORCE"].state_hash() == sims["NBBGPU_GENERIC"].state_hash(), (name, rule)
+    for s in sims.values():
+        s.close()
