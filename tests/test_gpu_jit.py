@@ -25,6 +25,8 @@ CUSTOM = [
     (FractalDescriptor("k13s5", 13, 5, [(0, 0), (2, 0), (4, 0), (1, 1), (3, 1), (0, 2), (2, 2), (4, 2),
                                         (1, 3), (3, 3), (0, 4), (2, 4), (4, 4)]), 5),
     (FractalDescriptor("k9s3", 9, 3, [(x, y) for y in range(3) for x in range(3)]), 6),
+    # k = 8 row blocks (BW % 4 == 0): interleaved record words (rec_word, padded records)
+    (FractalDescriptor("k8s3c", 8, 3, [(x, y) for y in range(3) for x in range(3) if (x, y) != (0, 0)]), 6),
 ]
 
 
