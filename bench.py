@@ -454,7 +454,17 @@ def run_ours(args):
         return 0
 
     peak, peak_src = peaks()
-    kernel_ms_per_launch = kernel_ms / args.steps
+    kernel_ms_isolated = kernel_ms / args.steps
+    kernel_ms_per_launch = kernel_ms_isolated
+    timing = ("CUDA events around every step kernel launch (second pass of K steps; the events "
+              "serialise the launches, so each launch is timed without its PDL overlap)")
+    if ws == 1 and launches == args.steps:
+        # one launch per step (the step kernel gathers its halo words itself): the timed
+        # region is exactly K launches of this kernel, so its average launch duration is
+        # the timed region / K, PDL overlap of consecutive launches included
+        kernel_ms_per_launch = step_ms / args.steps
+        timing = ("one launch per step: CUDA events around the K back-to-back launches of the timed "
+                  "region on the engine stream / K")
     packed = kern == "packed"
     # algorithmic bytes per launch: packed layout = read + write 1 bit per owned cell
     # (SURVEY.md 8d's packed model); byte layouts = 2 B per owned cell
@@ -480,6 +490,7 @@ def run_ours(args):
                                "cell-update x owned cells per launch (SURVEY.md 8d packed model)" if packed else
                                "2 B per compact cell-update (SURVEY.md 8d) x owned cells per launch"),
                      "peak_source": peak_src, "kernel_ms_per_launch": kernel_ms_per_launch,
+                     "kernel_timing": timing, "kernel_ms_isolated": kernel_ms_isolated,
                      "model_2B": {"achieved": achieved_2b, "frac": achieved_2b / peak,
                                   "note": "the reference's 1 byte per cell (grid.hpp:15); > 1 means the "
                                           "packed layout moves fewer bytes than the byte model assumes"}},

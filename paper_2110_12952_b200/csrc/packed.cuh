@@ -1030,6 +1030,52 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         if (warp >= NCW + 2) {  // ---- halo warps: group i = hw (mod HW) --------------------
             const uint32_t hw = (uint32_t)(warp - NCW - 2);
             uint32_t i = hw;
+            if (p.nH <= 8) {
+                // (triangle: <= 8 slots) the slot table in registers; the next group's
+                // neighbour tiles are loaded while this group's boundary words are in
+                // flight, and both before the wait for the stage -- only the 8 stores
+                // need it
+                uint32_t noff[8], moff[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t sl = (uint32_t)j < p.nH ? __ldg(p.slot + j) : 0u;
+                    noff[j] = ((sl >> 16) & 0xFFu) * p.T;
+                    moff[j] = sl & 0xFFFFu;
+                }
+                const uint32_t gstep = HW * npairs;
+                uint32_t t2n[8];
+                auto fetch = [&](uint32_t gg) {
+                    const uint32_t t = gg * 32 + lane;
+                    const bool in = gg < p.g1 && t < p.T;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) t2n[j] = ((uint32_t)j < p.nH && in) ? __ldg(p.ntab + noff[j] + t) : kNoTile;
+                };
+                uint32_t g = p.g0 + pair + hw * npairs;
+                fetch(g);
+                for (; g < p.g1; g += gstep, i += HW) {
+                    uint32_t t2[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) t2[j] = t2n[j];
+                    fetch(g + gstep);
+                    uint32_t v[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        v[j] = t2[j] != kNoTile ? __ldcg(bsrc + (size_t)(t2[j] >> 5) * p.nSrc + moff[j]) >> (t2[j] & 31) : 0u;
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t word = __ballot_sync(0xFFFFFFFFu, (v[j] & 1u) != 0);
+                        if (lane == (uint32_t)j) mine = word;
+                    }
+                    const uint32_t s = i % NS;
+                    if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
+                    uint32_t* Hs = reinterpret_cast<uint32_t*>(st + s * stage_bytes) + win_words;
+                    if ((uint32_t)lane < p.nH) Hs[lane] = mine;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(full0 + 8 * s);  // release: the halo words are visible
+                }
+                return;
+            }
             for (uint32_t g = p.g0 + pair + hw * npairs; g < p.g1; g += HW * npairs, i += HW) {
                 const uint32_t s = i % NS;
                 if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
