@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(256) halo_bt_regs_kernel(const PackedStepParam
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             const bool ok = t2[d] != kNoTile;
-            const uint32_t* b = p.bt + ((t2[d] >> 5) * (uint32_t)NHC) * 32u + (t2[d] & 31u);
+            const uint32_t* b = p.bt + (uint64_t)(t2[d] >> 5) * (NHC * 32u) + (t2[d] & 31u);
             uint32_t v[NHC];
 #pragma unroll
             for (int k = 0; k < NHC; ++k) v[k] = (ok && M.m[k][d] != 0u) ? __ldcg(b + 32 * k) : 0u;
@@ -1005,6 +1005,89 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         for (uint32_t k = tid; k < NO * (p.Cp - z0); k += blockDim.x)
             reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - z0)) * out_bytes)[z0 + k % (p.Cp - z0)] = 0u;
     }
+    // ---- in-kernel halo warps (<= 8 slots): slot table + the first group's neighbour
+    // tiles (static ntab), before the PDL wait
+    // (T q=8; the q=6 kernel with 8 group sets spills with them live across its prologue)
+    constexpr bool HW_HOIST = HW > 0 && !BTO && WQ == 81;
+    uint32_t hw_noff[8], hw_moff[8], hw_t2n[8];
+    auto hw_tables = [&]() {
+        if (warp >= NCW + 2 && p.nH <= 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t sl = (uint32_t)j < p.nH ? __ldg(p.slot + j) : 0u;
+                hw_noff[j] = ((sl >> 16) & 0xFFu) * p.T;
+                hw_moff[j] = sl & 0xFFFFu;
+            }
+            const uint32_t gg = p.g0 + pair + (uint32_t)(warp - NCW - 2) * npairs, t = gg * 32 + lane;
+            const bool in = gg < p.g1 && t < p.T;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hw_t2n[j] = ((uint32_t)j < p.nH && in) ? __ldg(p.ntab + hw_noff[j] + t) : kNoTile;
+        }
+    };
+    if constexpr (HW_HOIST) hw_tables();
+    // ---- consumer tables (block offsets, output slice, boundary sources): plan data
+    // that no kernel writes, so they are loaded before the PDL wait and overlap the
+    // previous kernel's tail (the boundary-source search is ~11 dependent load pairs
+    // per lane: a visible share of a step when a CTA owns a few groups)
+    uint32_t KB[9], KS[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
+    }
+    const int set = warp / NCHUNK, c = warp - set * NCHUNK;
+    const uint32_t lblk = (uint32_t)c * 32 + lane;
+    const bool active = lblk < (uint32_t)NBLK;
+    const uint32_t blk = half * (uint32_t)NBLK + lblk;
+    uint32_t toff[NEP];
+    {
+        const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
+        static_for<NEP / 4>([&](auto e4) {
+            constexpr int E = decltype(e4)::value;
+            const uint4 v = __ldg(t4 + E);
+            toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
+        });
+    }
+    // PWS: this warp's output slice [w_lo, w_hi) (slice words) and its boundary
+    // sources [k_lo, k_hi) of the cell-sorted list
+    uint32_t w_lo = 0, w_hi = 0, k_lo = 0, k_hi = 0;
+    if constexpr (PWS) {
+        w_lo = (uint32_t)c * 32 * W::BW;
+        w_hi = c == NCHUNK - 1 ? out_words : w_lo + 32 * W::BW;
+        const uint32_t* sorted = p.srcidx + p.nSrc;
+        for (uint32_t k = lane; k < p.nSrc; k += 32) {
+            const uint32_t cell = __ldg(p.srcidx + __ldg(sorted + k));
+            k_lo += cell < out_off + w_lo;
+            k_hi += cell < out_off + w_hi;
+        }
+        k_lo = __reduce_add_sync(0xFFFFFFFFu, k_lo);
+        k_hi = __reduce_add_sync(0xFFFFFFFFu, k_hi);
+    }
+    // up to 64 boundary sources of the slice: (m, word) pairs held in registers
+    // (carpet r=9 0.0207 -> 0.0188 ms; candy, with few sources per warp, keeps the
+    // loop: 0.238 vs 0.244 ms)
+    constexpr bool REGB = PWS && !std::is_same<FT, CandyTag>::value;
+    uint32_t bm0 = 0, bw0 = 0, bm1 = 0, bw1 = 0;
+    if constexpr (REGB) {
+        const uint32_t* sorted = p.srcidx + p.nSrc;
+        if (k_lo + lane < k_hi) { bm0 = __ldg(sorted + k_lo + lane); bw0 = __ldg(p.srcidx + bm0); }
+        if (k_lo + 32 + lane < k_hi) { bm1 = __ldg(sorted + k_lo + 32 + lane); bw1 = __ldg(p.srcidx + bm1); }
+    }
+    // compile-time stage size (SWC > 0): the group loop is unrolled over the NS / NGRP
+    // stages of this warp's set, so every external load is ONE ld.shared at the
+    // lane's (set-relative) offset + an immediate (the stage offset) instead of a
+    // multiply-add + add + load per external per group (H: 48 -> 16 instructions of
+    // the 166 per block)
+    constexpr int SWC = SPLIT == 1 ? StageWordsCT<FT, WQ>::v : 0;
+    uint32_t tS[NEP], own_off = 0;
+    if constexpr (SWC > 0) {
+        using BG = BlockGeom<FT, P, WQ>;
+        const uint32_t set_off = (uint32_t)set * (uint32_t)(SWC * 4);
+#pragma unroll
+        for (int e = 0; e < NEP; ++e) tS[e] = set_off + toff[e];
+        own_off = set_off + 4u * block_own_base<FT, P, WQ>(blk);
+        (void)sizeof(BG);
+    }
     fence_proxy_async_smem();
     __syncthreads();
     pdl_wait();     // the prologue above overlapped the previous kernel's tail (PDL)
@@ -1034,16 +1117,12 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                 // (triangle: <= 8 slots) the slot table in registers; the next group's
                 // neighbour tiles are loaded while this group's boundary words are in
                 // flight, and both before the wait for the stage -- only the 8 stores
-                // need it
-                uint32_t noff[8], moff[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t sl = (uint32_t)j < p.nH ? __ldg(p.slot + j) : 0u;
-                    noff[j] = ((sl >> 16) & 0xFFu) * p.T;
-                    moff[j] = sl & 0xFFFFu;
-                }
+                // need it (the table and the first group's tiles: before the PDL wait)
+                if constexpr (!HW_HOIST) hw_tables();
+                uint32_t* const noff = hw_noff;
+                uint32_t* const moff = hw_moff;
+                uint32_t* const t2n = hw_t2n;
                 const uint32_t gstep = HW * npairs;
-                uint32_t t2n[8];
                 auto fetch = [&](uint32_t gg) {
                     const uint32_t t = gg * 32 + lane;
                     const bool in = gg < p.g1 && t < p.T;
@@ -1051,7 +1130,6 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
                     for (int j = 0; j < 8; ++j) t2n[j] = ((uint32_t)j < p.nH && in) ? __ldg(p.ntab + noff[j] + t) : kNoTile;
                 };
                 uint32_t g = p.g0 + pair + hw * npairs;
-                fetch(g);
                 for (; g < p.g1; g += gstep, i += HW) {
                     uint32_t t2[8];
 #pragma unroll
@@ -1188,65 +1266,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         return;
     }
     // ---- consumers ---------------------------------------------------------------------
-    uint32_t KB[9], KS[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        KB[i] = ((p.birth >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-        KS[i] = ((p.survive >> i) & 1u) ? 0xFFFFFFFFu : 0u;
-    }
-    const int set = warp / NCHUNK, c = warp - set * NCHUNK;
-    const uint32_t lblk = (uint32_t)c * 32 + lane;
-    const bool active = lblk < (uint32_t)NBLK;
-    const uint32_t blk = half * (uint32_t)NBLK + lblk;
-    uint32_t toff[NEP];
-    {
-        const uint4* t4 = reinterpret_cast<const uint4*>(p.btab) + (size_t)(active ? blk : 0) * (NEP / 4);
-        static_for<NEP / 4>([&](auto e4) {
-            constexpr int E = decltype(e4)::value;
-            const uint4 v = __ldg(t4 + E);
-            toff[4 * E] = v.x; toff[4 * E + 1] = v.y; toff[4 * E + 2] = v.z; toff[4 * E + 3] = v.w;
-        });
-    }
-    // PWS: this warp's output slice [w_lo, w_hi) (slice words) and its boundary
-    // sources [k_lo, k_hi) of the cell-sorted list
-    uint32_t w_lo = 0, w_hi = 0, k_lo = 0, k_hi = 0;
-    if constexpr (PWS) {
-        w_lo = (uint32_t)c * 32 * W::BW;
-        w_hi = c == NCHUNK - 1 ? out_words : w_lo + 32 * W::BW;
-        const uint32_t* sorted = p.srcidx + p.nSrc;
-        for (uint32_t k = lane; k < p.nSrc; k += 32) {
-            const uint32_t cell = __ldg(p.srcidx + __ldg(sorted + k));
-            k_lo += cell < out_off + w_lo;
-            k_hi += cell < out_off + w_hi;
-        }
-        k_lo = __reduce_add_sync(0xFFFFFFFFu, k_lo);
-        k_hi = __reduce_add_sync(0xFFFFFFFFu, k_hi);
-    }
-    // up to 64 boundary sources of the slice: (m, word) pairs held in registers
-    // (carpet r=9 0.0207 -> 0.0188 ms; candy, with few sources per warp, keeps the
-    // loop: 0.238 vs 0.244 ms)
-    constexpr bool REGB = PWS && !std::is_same<FT, CandyTag>::value;
-    uint32_t bm0 = 0, bw0 = 0, bm1 = 0, bw1 = 0;
-    if constexpr (REGB) {
-        const uint32_t* sorted = p.srcidx + p.nSrc;
-        if (k_lo + lane < k_hi) { bm0 = __ldg(sorted + k_lo + lane); bw0 = __ldg(p.srcidx + bm0); }
-        if (k_lo + 32 + lane < k_hi) { bm1 = __ldg(sorted + k_lo + 32 + lane); bw1 = __ldg(p.srcidx + bm1); }
-    }
-    // compile-time stage size (SWC > 0): the group loop is unrolled over the NS / NGRP
-    // stages of this warp's set, so every external load is ONE ld.shared at the
-    // lane's (set-relative) offset + an immediate (the stage offset) instead of a
-    // multiply-add + add + load per external per group (H: 48 -> 16 instructions of
-    // the 166 per block)
-    constexpr int SWC = SPLIT == 1 ? StageWordsCT<FT, WQ>::v : 0;
-    uint32_t tS[NEP], own_off = 0;
-    if constexpr (SWC > 0) {
-        using BG = BlockGeom<FT, P, WQ>;
-        const uint32_t set_off = (uint32_t)set * (uint32_t)(SWC * 4);
-#pragma unroll
-        for (int e = 0; e < NEP; ++e) tS[e] = set_off + toff[e];
-        own_off = set_off + 4u * block_own_base<FT, P, WQ>(blk);
-        (void)sizeof(BG);
-    }
+    // (per-warp tables: set up before the PDL wait, see above)
     auto group = [&](uint32_t g, uint32_t i, auto soff_c) {
         constexpr int SOFF = decltype(soff_c)::value;  // byte offset of this stage from set 0's (SWC > 0)
         (void)SOFF;
