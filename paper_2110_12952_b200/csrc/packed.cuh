@@ -998,13 +998,9 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     }
     if (tid < NS) reinterpret_cast<uint32_t*>(st + tid * stage_bytes)[win_words + p.nHp] = 0u;  // absent
     if (SPLIT == 1)
-    {
-        // record padding words (interleaved records: the padding blocks' words lie
-        // anywhere in the last chunk -- zero the whole ring once)
-        const uint32_t z0 = rec_ilv<FT, P, WQ>() ? 0u : p.C;
-        for (uint32_t k = tid; k < NO * (p.Cp - z0); k += blockDim.x)
-            reinterpret_cast<uint32_t*>(outs + (k / (p.Cp - z0)) * out_bytes)[z0 + k % (p.Cp - z0)] = 0u;
-    }
+        for (int o = 0; o < NO; ++o)  // record padding words (interleaved records: the
+            for (uint32_t k = p.C + tid; k < p.Cp; k += blockDim.x)  // padding blocks' words carry no cell
+                reinterpret_cast<uint32_t*>(outs + o * out_bytes)[k] = 0u;
     // ---- in-kernel halo warps (<= 8 slots): slot table + the first group's neighbour
     // tiles (static ntab), before the PDL wait
     // (T q=8; the q=6 kernel with 8 group sets spills with them live across its prologue)
