@@ -11,7 +11,7 @@ timeout 600 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/r2_
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches.log 2>&1; echo "launches rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:step_packed_ws3 -s 4 -c 1 -o $O/r2_step_r20 \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_step.log 2>&1; echo "ncu step rc=$?"
-timeout 900 $NCU --set full --import-source on -k regex:halo_words -s 4 -c 1 -o $O/r2_halo_r20 \
+timeout 900 $NCU --set full --import-source on -k regex:halo_words -s 4 -c 1 -o $O/r2_halo_r20 env NBBGPU_HALO_WARPS=0 \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_halo.log 2>&1; echo "ncu halo rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_bt_regs" -s 4 -c 2 -o $O/r2_jit_k12 \
     python tools/prof_step.py --fractal @descriptors/k6s3.desc --level 12 --kernel packed --steps 5 > $O/ncu_jit.log 2>&1; echo "ncu jit rc=$?"
