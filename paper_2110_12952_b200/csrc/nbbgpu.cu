@@ -406,7 +406,8 @@ struct nbbgpu_sim {
     uint32_t* d_ploc = nullptr;
     uint32_t* d_pbtab = nullptr;            // micro-block external offsets
     uint32_t* d_phalo = nullptr;            // per step: halo words [NG][nHp]
-    uint32_t* d_pbt = nullptr;              // transposed boundary plane (wide halos, single GPU)
+    uint32_t* d_pbt = nullptr;              // transposed boundary plane (wide halos, single GPU) of pk[0]
+    uint32_t* d_pbt1 = nullptr;             // ... of pk[1] (bt_buf)
     uint32_t* d_pdmask = nullptr;           // [nHc][8] direction masks per 32-slot chunk
     BtMasks bt_masks{};  // the same masks by value (halo_bt_regs_kernel)
     uint64_t packed_table_bytes = 0;
@@ -873,6 +874,7 @@ void free_all(nbbgpu_t h) {
     if (h->d_pbtab) cudaFree(h->d_pbtab);
     if (h->d_phalo) cudaFree(h->d_phalo);
     if (h->d_pbt) cudaFree(h->d_pbt);
+    if (h->d_pbt1) cudaFree(h->d_pbt1);
     if (h->d_pdmask) cudaFree(h->d_pdmask);
     if (h->d_lowmask) cudaFree(h->d_lowmask);
     if (h->d_bblow) cudaFree(h->d_bblow);

@@ -75,6 +75,15 @@ struct PackedGeom {
 // word of the 256-byte arrival-counter allocation that holds the peer-wait error flag
 constexpr uint32_t kPeerErrWord = 16;
 
+constexpr int kBtMaxChunks = 16;
+
+// The per-(chunk, direction) masks of the transposed gather, passed by value: with
+// the chunk count a compile-time constant every mask is a kernel-parameter operand
+// (no shared entry list, no shared accumulators).
+struct BtMasks {
+    uint32_t m[kBtMaxChunks][8];
+};
+
 struct PackedStepParams {
     uint32_t C, Cp, SW;      // local cells, words per group record, words per smem stage
     uint32_t nH, nHp, nSrc;  // halo slots (padded to 4), boundary sources
@@ -109,6 +118,8 @@ struct PackedStepParams {
     // transposed plane Bt (layout of bnd_transpose_kernel) straight from the output
     // record -- no transpose kernel, no boundary-plane round trip (nullptr: write B)
     uint32_t* bt_out;
+    // in-kernel Bt gather (HW halo warps with bt warps): the per-(chunk, direction) masks
+    BtMasks btm;
     // peer-memory transport, fused push (triangle kernels, nSrc <= 32): the boundary
     // words peers need are stored into their planes as each group finishes
     // (push_off[local group] .. +1: entries m | peer << 16), and the grid's last CTA
@@ -416,15 +427,6 @@ __global__ void bnd_transpose_kernel(const PackedStepParams p, const uint32_t* _
 // (one load each, masked), and one transpose turns lane b's bits into the 32 halo
 // words (no per-source-group passes: the slots of a direction are bits of ONE word
 // of the neighbour tile).
-constexpr int kBtMaxChunks = 16;
-
-// The per-(chunk, direction) masks of the transposed gather, passed by value: with
-// the chunk count a compile-time constant every mask is a kernel-parameter operand
-// (no shared entry list, no shared accumulators).
-struct BtMasks {
-    uint32_t m[kBtMaxChunks][8];
-};
-
 // Transposed gather, register form (one warp per group, grid-stride): lane = tile b
 // holds the 8 neighbour tiles (the next group's are loaded while this group's Bt
 // words are in flight); per direction one address and, per chunk the direction
@@ -981,7 +983,11 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // warps wait for it) and oempty[o] = the bt warps are done reading it (every chunk
     // warp waits before rewriting the buffer)
     constexpr bool BTO = PWS && SPLIT == 1 && BTW > 0;
-    static_assert(BTW == 0 || (BTO && HW == 0), "bt warps need per-warp stores, one CTA per record");
+    static_assert(BTW == 0 || BTO, "bt warps need per-warp stores, one CTA per record");
+    // HG: with bt warps, the HW halo warps gather each group's halo words from the
+    // previous step's transposed plane p.bt (halo_bt_regs_kernel's body) into the stage
+    constexpr bool HG = BTO && HW > 0;
+    constexpr int HG_NHC = std::is_same<FT, HTag>::value ? 7 : std::is_same<FT, CarpetTag>::value ? 11 : 1;
     static_assert(BTW % NGRP == 0, "bt warps are split evenly over the group sets");
     constexpr int BTS = BTW / NGRP > 0 ? BTW / NGRP : 1;  // bt warps per group set
     if (tid == 0) push_warps_done = 0u;
@@ -1105,7 +1111,53 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
         return;
     }
-    if constexpr (HW > 0) {
+    if constexpr (HG) {
+        if (warp >= NCW + 2 && warp < NCW + 2 + HW) {  // ---- Bt gather warps: group i = hw (mod HW)
+            constexpr int NHC = HG_NHC;
+            const uint32_t hw = (uint32_t)(warp - NCW - 2), gstep = HW * npairs;
+            const XposeLane X((uint32_t)lane);
+            uint32_t t2n[8];
+            auto fetch = [&](uint32_t gg) {
+                const uint32_t t = gg * 32 + lane;
+                const bool in = gg < p.g1 && t < p.T;
+#pragma unroll
+                for (int d = 0; d < 8; ++d) t2n[d] = (d < p.nD && in) ? __ldg(p.ntab + ((size_t)d * p.T + t)) : kNoTile;
+            };
+            uint32_t i = hw, g = p.g0 + pair + hw * npairs;
+            fetch(g);
+            for (; g < p.g1; g += gstep, i += HW) {
+                uint32_t t2[8];
+#pragma unroll
+                for (int d = 0; d < 8; ++d) t2[d] = t2n[d];
+                fetch(g + gstep);
+                uint32_t acc[NHC];
+#pragma unroll
+                for (int k = 0; k < NHC; ++k) acc[k] = 0u;
+#pragma unroll
+                for (int d = 0; d < 8; ++d) {
+                    const bool ok = t2[d] != kNoTile;
+                    const uint32_t* b = p.bt + (uint64_t)(t2[d] >> 5) * (NHC * 32u) + (t2[d] & 31u);
+                    uint32_t v[NHC];
+#pragma unroll
+                    for (int k = 0; k < NHC; ++k) v[k] = (ok && p.btm.m[k][d] != 0u) ? __ldcg(b + 32 * k) : 0u;
+#pragma unroll
+                    for (int k = 0; k < NHC; ++k) acc[k] |= v[k] & p.btm.m[k][d];
+                }
+#pragma unroll
+                for (int k = 0; k < NHC; ++k) acc[k] = warp_transpose32(acc[k], X);
+                const uint32_t s = i % NS;
+                if (i >= NS) mbar_wait(empty0 + 8 * s, ((i / NS) - 1) & 1u);
+                uint32_t* Hs = reinterpret_cast<uint32_t*>(st + s * stage_bytes) + win_words;
+#pragma unroll
+                for (int k = 0; k < NHC; ++k)
+                    if (k * 32 + lane < p.nH) Hs[k * 32 + lane] = acc[k];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full0 + 8 * s);  // release: the halo words are visible
+            }
+            return;
+        }
+    }
+    if constexpr (HW > 0 && !HG) {
         if (warp >= NCW + 2) {  // ---- halo warps: group i = hw (mod HW) --------------------
             const uint32_t hw = (uint32_t)(warp - NCW - 2);
             uint32_t i = hw;
@@ -1189,7 +1241,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
         }
     }
     if constexpr (BTO) {
-        if (warp >= NCW + 2) {  // ---- bt warps: chunks b, b + BTW, ... of every record ----------
+        if (warp >= NCW + 2 + (HG ? HW : 0)) {  // ---- bt warps: chunks b, b + BTW, ... of every record
             // lane l loads the record word of boundary slot 32k + l; one transpose gives
             // lane t the slot bits of tile t: Bt[(g nHc + k) 32 + t], 128 coalesced bytes
             // bt warp w serves group set w % NGRP (each set's buffers, no head-of-line
@@ -1197,7 +1249,7 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
             // The lane's source cells (chunks b, b + BTS, ...) stay in registers; the
             // buffer is released as soon as its words are read (before the transposes
             // and the global stores: H r=11 step kernel 108.7 -> ... us)
-            const uint32_t w = (uint32_t)(warp - NCW - 2), set = w % NGRP, b = w / NGRP;
+            const uint32_t w = (uint32_t)(warp - NCW - 2 - (HG ? HW : 0)), set = w % NGRP, b = w / NGRP;
             const uint32_t nHc = (p.nSrc + 31) / 32;
             const XposeLane X((uint32_t)lane);
             // (chunks per bt warp: at most kBtMaxChunks / BTS; H q=4 has 7 chunks)

@@ -507,6 +507,42 @@ def test_packed_in_kernel_halo_warps(monkeypatch, hw):
     sim.close()
 
 
+def test_in_kernel_bt_gather(monkeypatch):
+    # carpet / H on one GPU: after a step whose bt warps wrote the transposed plane, the
+    # next step kernel's gather warps read it themselves (no halo kernel; Bt double
+    # buffered by front parity).  Bytes == oracle at small levels (forced on), and the
+    # same hashes as the halo-kernel path across rule switches (non-B3/S23 steps take
+    # the halo kernel), set_cell and odd / even call lengths at H r=9 / carpet r=9
+    H = FractalDescriptor("h", 7, 3, [(0, 0), (2, 0), (0, 1), (1, 1), (2, 1), (0, 2), (2, 2)])
+    monkeypatch.setenv("NBBGPU_HALO_INK", "1")
+    monkeypatch.setenv("NBBGPU_HALO_BT", "1")
+    for desc, r in ((H, 6), (H, 7), (CARPET, 6)):
+        _lockstep_vs_oracle(desc, r, conway_rule(), 61 + r, 0.5, 6, kernel="packed")
+    monkeypatch.delenv("NBBGPU_HALO_BT")
+    other = StencilRule(0x49, 0x1A6, Neighborhood.Moore)
+    seq = [(conway_rule(), 1), (conway_rule(), 4), (other, 1), (conway_rule(), 3), ("set", 0), (conway_rule(), 5)]
+    for desc, r in ((H, 9), (CARPET, 9)):
+        got = {}
+        for ink in ("1", "0"):
+            monkeypatch.setenv("NBBGPU_HALO_INK", ink)
+            sim = Simulation(desc, r, Backend.GpuCompact, SimOptions(kernel="packed", memory_cap=1 << 40))
+            sim.seed_random(5 + r, 0.5)
+            hs = []
+            for rule, n in seq:
+                if rule == "set":
+                    sim.set_cell((0, 0), 1 - sim.cell((0, 0)))
+                    continue
+                sim.step(rule, n)
+                hs.append(sim.state_hash())
+            _, _, launches = sim.step_profiled(conway_rule(), 10)
+            hs.append(sim.state_hash())
+            got[ink] = hs
+            if ink == "1":  # one launch per step once the front's Bt exists
+                assert launches == 10, (desc.name, launches)
+            sim.close()
+        assert got["1"] == got["0"], desc.name
+
+
 @pytest.mark.parametrize("env", [("NBBGPU_HALO_GROUP", "1"), ("NBBGPU_HALO_GROUP", "0"),
                                  ("NBBGPU_HALO_NCH3", "1"), ("NBBGPU_HALO_NCH3", "0"),
                                  ("NBBGPU_HALO_BT", "1"), ("NBBGPU_HALO_LEAN", "1")])
