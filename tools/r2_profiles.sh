@@ -21,6 +21,8 @@ timeout 900 $NCU --set full --import-source on -k regex:step_bb_rows -s 3 -c 1 -
     python tools/prof_step.py --fractal sierpinski-carpet --level 10 --backend gpu-bb --steps 5 > $O/ncu_bb_c10.log 2>&1; echo "ncu bb c10 rc=$?"
 timeout 900 $NCU --set full --import-source on -k regex:"step_packed_ws3|halo_bt_regs" -s 6 -c 2 -o $O/r2_h11 \
     python tools/prof_step.py --fractal @descriptors/h-fractal.desc --level 11 --kernel packed --steps 5 > $O/ncu_h11.log 2>&1; echo "ncu h11 rc=$?"
+timeout 900 $NCU --set full --import-source on -k regex:step_packed_ws3 -s 4 -c 1 -o $O/r2_c9 \
+    python tools/prof_step.py --fractal sierpinski-carpet --level 9 --kernel packed --steps 6 > $O/ncu_c9.log 2>&1; echo "ncu c9 rc=$?"
 # text summaries (the .ncu-rep files stay only when small: gpurun copies back <= 64 MiB)
 for r in $O/*.ncu-rep; do
   tools/ncu_summary.sh $r > ${r%.ncu-rep}.txt 2>&1
