@@ -919,10 +919,12 @@ struct WsGeom {
     static_assert(SPLIT == 1 || (Wiring<FT, P>::BH == 1 && WQ % SPLIT == 0), "SPLIT needs P = 1 row blocks");
 };
 
-// HW > 0: HW extra warps gather each group's halo words in-kernel (ntab rows +
-// boundary-plane words, two round trips per group, HW groups in flight) into the
-// stage and arrive on its full barrier -- no separate halo kernel.  Pays off when a
-// rank owns few groups (T r=18 / r=20 on 8 GPUs: the halo kernel's fixed latency).
+// HW > 0: HW extra warps gather each group's halo words in-kernel into the stage and
+// arrive on its full barrier -- no separate halo kernel.  Without bt warps (<= 8
+// slots: triangle, Vicsek): ntab rows + boundary-plane words and ballots, the next
+// group's neighbour tiles prefetched and the loads issued before the stage wait.
+// With bt warps (HG: carpet, small H): the register-form transposed gather from the
+// previous front's Bt plane (p.bt; this launch writes the other parity, p.bt_out).
 // BTW > 0 (per-warp-store kernels on one GPU, p.bt_out): BTW extra warps write the
 // transposed boundary plane Bt (bnd_transpose_kernel's layout) from each finished
 // output record -- no transpose kernel and no boundary-plane round trip per step.
