@@ -433,7 +433,10 @@ __global__ void bnd_transpose_kernel(const PackedStepParams p, const uint32_t* _
 // has slots in, one predicated load + AND/OR into the chunk's register accumulator;
 // then NHC transposes.  ~300 instructions per group instead of ~1000 for round 2's
 // (chunk, direction) entry list in shared memory with shared accumulators (removed).
-template <int NHC>
+// NZ (NHC <= 8): bit 8k + d set iff chunk k has slots in direction d -- the plan's
+// pattern, compiled in at run time (jit.inc) so the absent (chunk, direction) pairs
+// cost nothing; all ones: every pair tested against its mask at run time.
+template <int NHC, unsigned long long NZ = ~0ull>
 __global__ void __launch_bounds__(256) halo_bt_regs_kernel(const PackedStepParams p, const BtMasks M,
                                                            uint32_t* __restrict__ H) {
     const uint32_t lane = threadIdx.x & 31;
@@ -464,9 +467,13 @@ __global__ void __launch_bounds__(256) halo_bt_regs_kernel(const PackedStepParam
             const uint32_t* b = p.bt + (uint64_t)(t2[d] >> 5) * (NHC * 32u) + (t2[d] & 31u);
             uint32_t v[NHC];
 #pragma unroll
-            for (int k = 0; k < NHC; ++k) v[k] = (ok && M.m[k][d] != 0u) ? __ldcg(b + 32 * k) : 0u;
+            for (int k = 0; k < NHC; ++k) {
+                const bool pair = NHC > 8 || ((NZ >> (8 * k + d)) & 1ull);  // (compile-time)
+                v[k] = (pair && ok && M.m[k][d] != 0u) ? __ldcg(b + 32 * k) : 0u;
+            }
 #pragma unroll
-            for (int k = 0; k < NHC; ++k) acc[k] |= v[k] & M.m[k][d];
+            for (int k = 0; k < NHC; ++k)
+                if (NHC > 8 || ((NZ >> (8 * k + d)) & 1ull)) acc[k] |= v[k] & M.m[k][d];
         }
         uint32_t* Hg = H + (uint64_t)g * p.nHp;
 #pragma unroll
