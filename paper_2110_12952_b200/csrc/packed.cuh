@@ -966,8 +966,13 @@ step_packed_ws3_kernel(const PackedStepParams p, const uint32_t* __restrict__ sr
     // which that set consumes in order, so use u has completed before it waits for u + 1.
     static_assert(NS % NGRP == 0, "stages are partitioned over the group sets");
     // (the in-kernel halo warps wait on the stages' empty barriers the same way: each
-    // stage served by one halo warp, or one set whose consumers finish groups in order)
-    static_assert(HW == 0 || NS % (HW > 0 ? HW : 1) == 0 || NGRP == 1, "stages are partitioned over the halo warps");
+    // stage served by one halo warp, or one set whose consumers finish groups in order
+    // AND at most NS halo warps: a halo warp reaching group g has seen group g - HW - NS
+    // consumed, so the stage's use before last (g - 2 NS) is complete and the parity
+    // wait for g - NS cannot pass early; with HW > NS it could -- the warp would fill a
+    // stage still being read and arrive on the wrong phase of its full barrier)
+    static_assert(HW == 0 || NS % (HW > 0 ? HW : 1) == 0 || (NGRP == 1 && HW <= NS),
+                  "stages are partitioned over the halo warps");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t full0 = smem_u32(sm), empty0 = full0 + 8 * NS;
     const uint32_t ofull0 = empty0 + 8 * NS, oempty0 = ofull0 + 8 * NO;
